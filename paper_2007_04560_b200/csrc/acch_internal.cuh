@@ -1,0 +1,118 @@
+// Internal declarations shared by the libacch_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/acch_b200.h"
+
+#define ACCH_MAX_ORDER 32
+
+// ---------------------------------------------------------------------------
+// Device-side descriptors (passed by value to kernels)
+// ---------------------------------------------------------------------------
+
+struct GridDev {
+    int dim;
+    int periodic;
+    int nx, ny, nz;          // nz == 1 in 2D
+    long long n;             // cells
+    double ih2[3];           // 1 / h^2 per axis (x, y, z)
+    double ih[3];            // 1 / h per axis
+    double cell_volume;
+};
+
+struct ParamsDev {
+    double alpha, beta, gamma, theta, rho;
+    int order;
+    double c1[ACCH_MAX_ORDER];   // 1 / ((2s+1) 2s)   (physics.py:178-182)
+    double c2[ACCH_MAX_ORDER];   // 1 / (2s+1)
+};
+
+// coefficient planes of the matrix-free Jacobian, SoA, each N doubles
+enum { CO_S = 0, CO_D, CO_CBAR, CO_GU, CO_CU, CO_CV, CO_GV, CO_NFIELDS };
+
+// ---------------------------------------------------------------------------
+// Host-side context
+// ---------------------------------------------------------------------------
+
+struct acch_ctx {
+    GridDev g;
+    ParamsDev p;
+    acch_grid_desc desc;
+    int device = 0;
+    cudaStream_t stream = 0;
+    // reduction scratch: per-block partials + a completion counter + results
+    double *d_partials = nullptr;     // [kRedBlocks * kRedSlots]
+    unsigned int *d_counter = nullptr;
+    double *d_result = nullptr;       // [kRedSlots]
+    double *h_result = nullptr;       // pinned mirror
+    // Krylov workspace (lazily sized)
+    double *d_krylov = nullptr;       // (restart + 1) * 2N
+    int krylov_cols = 0;
+    double *d_work = nullptr;         // 3 * 2N: z (precond out), r, t
+    double *d_h = nullptr;            // small device array for Hessenberg column
+    long long launches = 0;
+};
+
+constexpr int kRedBlocks = 296;   // 2 x 148 SMs; fixed -> deterministic reductions
+constexpr int kRedSlots = 40;     // up to 40 simultaneous sums per reduction pass
+constexpr int kRedThreads = 256;
+
+// error helpers -------------------------------------------------------------
+void acch_set_error(const std::string &msg);
+acch_status acch_cuda_fail(cudaError_t e, const char *where);
+
+#define ACCH_CUDA(call)                                                  \
+    do {                                                                 \
+        cudaError_t _e = (call);                                         \
+        if (_e != cudaSuccess) return acch_cuda_fail(_e, #call);         \
+    } while (0)
+
+#define ACCH_LAUNCHED(ctx)                                               \
+    do {                                                                 \
+        (ctx)->launches++;                                               \
+        cudaError_t _e = cudaGetLastError();                             \
+        if (_e != cudaSuccess) return acch_cuda_fail(_e, "kernel launch"); \
+    } while (0)
+
+// results of a reduction pass are read back through the pinned mirror
+acch_status acch_fetch_results(acch_ctx *ctx, int count);
+
+// ---------------------------------------------------------------------------
+// Launchers implemented in stencil.cu / krylov.cu (return acch_status)
+// ---------------------------------------------------------------------------
+
+acch_status launch_residual(acch_ctx *ctx, const double *x_old, double dt, const double *x,
+                            double *F);   // results: [0] = ||F||^2, [1] = gap
+acch_status launch_jacobian_prepare(acch_ctx *ctx, const double *x_old, double dt,
+                                    const double *x, double *coef);
+acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w,
+                          double *y);
+acch_status launch_jacobian_blocks(acch_ctx *ctx, const double *coef, double dt, double *out);
+
+// multi-dot: results[q] = <V_q, w> (q < m), results[m] = <w, w>; V_q = V + q * ld
+acch_status launch_mdot(acch_ctx *ctx, const double *V, long long ld, int m, const double *w,
+                        long long n);
+// w -= sum_q h[q] V_q (h on device); results[0] = <w, w>
+acch_status launch_mupdate(acch_ctx *ctx, const double *V, long long ld, int m, const double *h,
+                           double *w, long long n);
+// y = alpha_dev[0] * x   (alpha read on device; inv == 1 -> 1 / alpha)
+acch_status launch_scale(acch_ctx *ctx, const double *alpha_dev, int inv, const double *x,
+                         double *y, long long n);
+// t = sum_q y[q] V_q (y on device)
+acch_status launch_combine(acch_ctx *ctx, const double *V, long long ld, int m, const double *y,
+                           double *t, long long n);
+// y = a * x + b * y (host scalars)
+acch_status launch_axpby(acch_ctx *ctx, double a, const double *x, double b, double *y, long long n);
+// generic reductions: [0] = <a, b>
+acch_status launch_dot(acch_ctx *ctx, const double *a, const double *b, long long n);
+
+// Schwarz (schwarz.cu)
+acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z);
+
+// stencil offsets (x, y, z) with |dx|+|dy|+|dz| <= 2, fixed order
+int stencil_offsets(int dim, int (*off)[3]);

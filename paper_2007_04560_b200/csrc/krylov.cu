@@ -1,0 +1,386 @@
+// Krylov kernels and the restarted GMRES driver (linalg.py:403-506).
+//
+// Vectors are 2N fp64; the basis V is (restart+1) contiguous columns owned by
+// the context.  Orthogonalisation:
+//   ortho = 0  modified Gram-Schmidt, one dot + one axpy per basis vector,
+//              the reference's exact operation order (linalg.py:462-471);
+//   ortho = 1  classical Gram-Schmidt with the reference's conditional second
+//              pass (||w|| < ||w_0||/2): one fused multi-dot (which also
+//              yields ||w_0||^2) and one fused update (which yields ||w||^2)
+//              per pass, i.e. 2 sweeps over the basis instead of 2(j+1).
+// All dots are deterministic (fixed-order reduction, reduce.cuh).  The host
+// keeps the (restart+1) x restart Hessenberg matrix and Givens rotations,
+// exactly as the reference, and reads back one small vector per iteration.
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "acch_internal.cuh"
+#include "reduce.cuh"
+
+namespace {
+
+template <int NS>
+__global__ void __launch_bounds__(kRedThreads)
+mdot_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ w, long long n,
+            double *partials, unsigned int *counter, double *result)
+{
+    double acc[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double wi = w[i];
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s)
+            if (s < m) acc[s] += V[s * ld + i] * wi;
+        acc[NS - 1] += wi * wi;
+    }
+    int ops[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) ops[s] = RED_SUM;
+    double v[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) v[s] = acc[s];
+    // slot NS-1 holds ||w||^2; move_slot_kernel relocates it to slot m
+    reduce_finish<NS>(v, ops, partials, counter, result);
+}
+
+// after mdot: result[NS-1] holds <w,w>; fix-up kernel moves it to result[m]
+__global__ void move_slot_kernel(double *result, int from, int to)
+{
+    if (threadIdx.x == 0 && blockIdx.x == 0) result[to] = result[from];
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kRedThreads)
+mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ h, double *__restrict__ w,
+               long long n, double *partials, unsigned int *counter, double *result)
+{
+    __shared__ double sh[NS];
+    if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[threadIdx.x] : 0.0;
+    __syncthreads();
+    double acc = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double wi = w[i];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+            if (s < m) wi -= sh[s] * V[s * ld + i];
+        w[i] = wi;
+        acc += wi * wi;
+    }
+    double v[1] = {acc};
+    const int ops[1] = {RED_SUM};
+    reduce_finish<1>(v, ops, partials, counter, result);
+}
+
+template <int NS>
+__global__ void combine_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ y,
+                               double *__restrict__ t, long long n)
+{
+    __shared__ double sy[NS];
+    if (threadIdx.x < NS) sy[threadIdx.x] = threadIdx.x < m ? y[threadIdx.x] : 0.0;
+    __syncthreads();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        double acc = 0.0;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+            if (s < m) acc += sy[s] * V[s * ld + i];
+        t[i] = acc;
+    }
+}
+
+__global__ void dot_kernel(const double *__restrict__ a, const double *__restrict__ b, long long n, double *partials,
+                           unsigned int *counter, double *result)
+{
+    double acc = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        acc += a[i] * b[i];
+    double v[1] = {acc};
+    const int ops[1] = {RED_SUM};
+    reduce_finish<1>(v, ops, partials, counter, result);
+}
+
+// w -= h_dev[0] * v
+__global__ void axpy_dev_kernel(const double *__restrict__ hdev, const double *__restrict__ v, double *__restrict__ w,
+                                long long n)
+{
+    const double h = *hdev;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        w[i] -= h * v[i];
+}
+
+__global__ void axpby_kernel(double a, const double *__restrict__ x, double b, double *__restrict__ y, long long n)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = a * x[i] + b * y[i];
+}
+
+__global__ void scale_kernel(double a, const double *__restrict__ x, double *__restrict__ y, long long n)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        y[i] = x[i] / a;
+}
+
+int vgrid(long long n)
+{
+    long long b = (n + kRedThreads * 4 - 1) / (kRedThreads * 4);
+    return (int)std::max<long long>(1, std::min<long long>(b, 4 * 148));
+}
+int rgrid(long long n)
+{
+    long long b = (n + kRedThreads * 4 - 1) / (kRedThreads * 4);
+    return (int)std::max<long long>(1, std::min<long long>(b, kRedBlocks));
+}
+
+}  // namespace
+
+// results[0..m-1] = <V_q, w>, results[m] = <w, w>, written to `out` (device)
+static acch_status mdot_to(acch_ctx *ctx, const double *V, long long ld, int m, const double *w, long long n,
+                           double *out)
+{
+    const int G = rgrid(n);
+#define MDOT_CASE(NS)                                                                                            \
+    mdot_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, w, n, ctx->d_partials, ctx->d_counter, out); \
+    move_slot_kernel<<<1, 32, 0, ctx->stream>>>(out, NS - 1, m);                                               \
+    ctx->launches += 1;
+    if (m + 1 <= 4) { MDOT_CASE(4) }
+    else if (m + 1 <= 8) { MDOT_CASE(8) }
+    else if (m + 1 <= 16) { MDOT_CASE(16) }
+    else if (m + 1 <= 33) { MDOT_CASE(33) }
+    else { acch_set_error("mdot: too many vectors (restart > 32)"); return ACCH_ERR_INVALID_ARG; }
+#undef MDOT_CASE
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+static acch_status mupdate_to(acch_ctx *ctx, const double *V, long long ld, int m, const double *h, double *w,
+                              long long n, double *out)
+{
+    const int G = rgrid(n);
+#define MUP_CASE(NS) \
+    mupdate_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter, out);
+    if (m <= 4) { MUP_CASE(4) }
+    else if (m <= 8) { MUP_CASE(8) }
+    else if (m <= 16) { MUP_CASE(16) }
+    else if (m <= 32) { MUP_CASE(32) }
+    else { acch_set_error("mupdate: too many vectors"); return ACCH_ERR_INVALID_ARG; }
+#undef MUP_CASE
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+static acch_status combine(acch_ctx *ctx, const double *V, long long ld, int m, const double *y, double *t, long long n)
+{
+    const int G = vgrid(n);
+    if (m <= 8) combine_kernel<8><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, y, t, n);
+    else if (m <= 16) combine_kernel<16><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, y, t, n);
+    else if (m <= 32) combine_kernel<32><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, y, t, n);
+    else { acch_set_error("combine: too many vectors"); return ACCH_ERR_INVALID_ARG; }
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_dot(acch_ctx *ctx, const double *a, const double *b, long long n)
+{
+    dot_kernel<<<rgrid(n), kRedThreads, 0, ctx->stream>>>(a, b, n, ctx->d_partials, ctx->d_counter, ctx->d_result);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+static acch_status dot_to(acch_ctx *ctx, const double *a, const double *b, long long n, double *out)
+{
+    dot_kernel<<<rgrid(n), kRedThreads, 0, ctx->stream>>>(a, b, n, ctx->d_partials, ctx->d_counter, out);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_axpby(acch_ctx *ctx, double a, const double *x, double b, double *y, long long n)
+{
+    axpby_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(a, x, b, y, n);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+static acch_status scale_by(acch_ctx *ctx, double a, const double *x, double *y, long long n)
+{
+    scale_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(a, x, y, n);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+static acch_status ensure_krylov(acch_ctx *ctx, int restart)
+{
+    const long long nv = 2 * ctx->g.n;
+    if (ctx->d_krylov && ctx->krylov_cols >= restart + 1) return ACCH_OK;
+    if (ctx->d_krylov) cudaFree(ctx->d_krylov);
+    if (ctx->d_work) cudaFree(ctx->d_work);
+    ctx->d_krylov = nullptr;
+    ctx->d_work = nullptr;
+    ACCH_CUDA(cudaMalloc(&ctx->d_krylov, sizeof(double) * nv * (restart + 1)));
+    ACCH_CUDA(cudaMalloc(&ctx->d_work, sizeof(double) * nv * 3));
+    ctx->krylov_cols = restart + 1;
+    return ACCH_OK;
+}
+
+static acch_status fetch(acch_ctx *ctx, double *host, const double *dev, int count)
+{
+    ACCH_CUDA(cudaMemcpyAsync(ctx->h_result, dev, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
+    ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int i = 0; i < count; ++i) host[i] = ctx->h_result[i];
+    return ACCH_OK;
+}
+
+#define TRY(x)                                   \
+    do {                                         \
+        acch_status _s = (x);                    \
+        if (_s != ACCH_OK) return _s;            \
+    } while (0)
+
+acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precond *pc, const double *b, double *x,
+                       double rel_tol, double abs_tol, int restart, int max_it, int ortho, int *iterations,
+                       int *converged, double *residual_norm)
+{
+    if (restart < 1 || restart > 32) {
+        acch_set_error("gmres: restart must be in [1, 32]");
+        return ACCH_ERR_INVALID_ARG;
+    }
+    TRY(ensure_krylov(ctx, restart));
+    const long long n = 2 * ctx->g.n;
+    double *V = ctx->d_krylov;
+    double *Z = ctx->d_work, *R = ctx->d_work + n, *T = ctx->d_work + 2 * n;
+    double *dh = ctx->d_h;      // [0..63] scratch for dots
+    auto col = [&](int j) { return V + (long long)j * n; };
+
+    double tmp[64];
+    TRY(dot_to(ctx, b, b, n, dh));
+    TRY(fetch(ctx, tmp, dh, 1));
+    const double bnorm = sqrt(tmp[0]);
+    const double tol = std::max(rel_tol * bnorm, abs_tol);
+
+    ACCH_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, ctx->stream));
+    ACCH_CUDA(cudaMemcpyAsync(R, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    double res_norm = bnorm;
+    int total = 0;
+    std::vector<double> H((restart + 1) * restart), cs(restart), sn(restart), gv(restart + 1), y(restart);
+    auto h = [&](int i, int j) -> double & { return H[i * restart + j]; };
+
+    for (;;) {
+        if (res_norm <= tol) {
+            *iterations = total; *converged = 1; *residual_norm = res_norm;
+            return ACCH_OK;
+        }
+        if (total >= max_it) {
+            *iterations = total; *converged = 0; *residual_norm = res_norm;
+            return ACCH_OK;
+        }
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(cs.begin(), cs.end(), 0.0);
+        std::fill(sn.begin(), sn.end(), 0.0);
+        std::fill(gv.begin(), gv.end(), 0.0);
+        TRY(scale_by(ctx, res_norm, R, col(0), n));
+        gv[0] = res_norm;
+        int j = 0;
+        bool breakdown = false;
+        while (j < restart && total < max_it) {
+            const double *zj = col(j);
+            if (pc) {
+                TRY(precond_apply_impl(pc, col(j), Z));
+                zj = Z;
+            }
+            double *w = col(j + 1);
+            TRY(launch_matvec(ctx, coef, dt, zj, w));
+            double norm_before, norm_after;
+            if (ortho == 1) {
+                TRY(mdot_to(ctx, V, n, j + 1, w, n, dh));
+                TRY(mupdate_to(ctx, V, n, j + 1, dh, w, n, dh + 40));
+                TRY(fetch(ctx, tmp, dh, 41));
+                for (int i = 0; i <= j; ++i) h(i, j) = tmp[i];
+                norm_before = sqrt(tmp[j + 1]);
+                norm_after = sqrt(tmp[40]);
+                if (norm_after < 0.5 * norm_before) {
+                    TRY(mdot_to(ctx, V, n, j + 1, w, n, dh));
+                    TRY(mupdate_to(ctx, V, n, j + 1, dh, w, n, dh + 40));
+                    TRY(fetch(ctx, tmp, dh, 41));
+                    for (int i = 0; i <= j; ++i) h(i, j) += tmp[i];
+                    norm_after = sqrt(tmp[40]);
+                }
+            } else {
+                TRY(dot_to(ctx, w, w, n, dh + 40));
+                for (int i = 0; i <= j; ++i) {
+                    TRY(dot_to(ctx, col(i), w, n, dh + i));
+                    axpy_dev_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(dh + i, col(i), w, n);
+                    ACCH_LAUNCHED(ctx);
+                }
+                TRY(dot_to(ctx, w, w, n, dh + 41));
+                TRY(fetch(ctx, tmp, dh, 42));
+                for (int i = 0; i <= j; ++i) h(i, j) = tmp[i];
+                norm_before = sqrt(tmp[40]);
+                norm_after = sqrt(tmp[41]);
+                if (norm_after < 0.5 * norm_before) {
+                    for (int i = 0; i <= j; ++i) {
+                        TRY(dot_to(ctx, col(i), w, n, dh + i));
+                        axpy_dev_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(dh + i, col(i), w, n);
+                        ACCH_LAUNCHED(ctx);
+                    }
+                    TRY(dot_to(ctx, w, w, n, dh + 41));
+                    TRY(fetch(ctx, tmp, dh, 42));
+                    for (int i = 0; i <= j; ++i) h(i, j) += tmp[i];
+                    norm_after = sqrt(tmp[41]);
+                }
+            }
+            h(j + 1, j) = norm_after;
+            total += 1;
+            for (int i = 0; i < j; ++i) {
+                const double t = cs[i] * h(i, j) + sn[i] * h(i + 1, j);
+                h(i + 1, j) = -sn[i] * h(i, j) + cs[i] * h(i + 1, j);
+                h(i, j) = t;
+            }
+            const double denom = hypot(h(j, j), h(j + 1, j));
+            if (denom == 0.0) {
+                breakdown = true;
+                break;
+            }
+            cs[j] = h(j, j) / denom;
+            sn[j] = h(j + 1, j) / denom;
+            h(j, j) = denom;
+            h(j + 1, j) = 0.0;
+            gv[j + 1] = -sn[j] * gv[j];
+            gv[j] = cs[j] * gv[j];
+            j += 1;
+            if (norm_after == 0.0) {
+                breakdown = true;
+                break;
+            }
+            TRY(scale_by(ctx, norm_after, w, w, n));
+            if (fabs(gv[j]) <= tol) break;
+        }
+        if (j > 0) {
+            // upper-triangular solve H[:j,:j] y = g[:j] (solve_triangular, linalg.py:500)
+            for (int i = j - 1; i >= 0; --i) {
+                double s = gv[i];
+                for (int k = i + 1; k < j; ++k) s -= h(i, k) * y[k];
+                y[i] = s / h(i, i);
+            }
+            ACCH_CUDA(cudaMemcpyAsync(dh, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, ctx->stream));
+            TRY(combine(ctx, V, n, j, dh, T, n));
+            if (pc) {
+                TRY(precond_apply_impl(pc, T, Z));
+                TRY(launch_axpby(ctx, 1.0, Z, 1.0, x, n));
+            } else {
+                TRY(launch_axpby(ctx, 1.0, T, 1.0, x, n));
+            }
+            // the host array y is reused next cycle: make sure the copy landed
+            ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        TRY(launch_matvec(ctx, coef, dt, x, R));
+        TRY(launch_axpby(ctx, 1.0, b, -1.0, R, n));
+        TRY(dot_to(ctx, R, R, n, dh));
+        TRY(fetch(ctx, tmp, dh, 1));
+        res_norm = sqrt(tmp[0]);
+        if (breakdown && res_norm > tol) {
+            *iterations = total; *converged = 0; *residual_norm = res_norm;
+            return ACCH_OK;
+        }
+    }
+}

@@ -1,0 +1,678 @@
+// Fused fp64 stencil kernels of the implicit AC/CH step on sm_100a.
+//
+//   residual      F(U'; U^n)                       scheme.py:323-354
+//   jac_prepare   7 coefficient planes of J(U')    scheme.py:427-470
+//   matvec        y = J w, matrix-free             scheme.py:471-484, linalg.py:67-68
+//   jac_blocks    explicit 2x2 stencil blocks of J (for ILU factorisation)
+//
+// Data layout: solver vectors are interleaved (u, v) per cell, x fastest,
+// read as double2 (16 B per cell, fully coalesced).  No ghost cells are
+// stored: periodic wrap / Neumann mirror are index arithmetic.
+//
+// The residual and matvec are radius-2 stencils by composition (a flux
+// divergence of a Laplacian-containing field).  Both kernels tile the x-y
+// plane (TX x TY threads, one output cell each) and march along z, keeping a
+// 3-plane ring of the inputs (tile + 2 halo) and of the intermediate field
+// (G_u, or dG_u; tile + 1 halo) in shared memory, so every input byte is read
+// from HBM once per sweep and the expensive entropy chords are evaluated only
+// on the tile + 1 halo.
+#include "acch_internal.cuh"
+#include "physics.cuh"
+#include "reduce.cuh"
+#include "jacobian.cuh"
+
+namespace {
+
+constexpr int RTX = 32, RTY = 8;     // residual tile
+constexpr int MTX = 32, MTY = 8;     // matvec tile
+constexpr int ZCHUNK = 32;           // z planes per block (3D)
+
+__host__ __device__ constexpr int ring_depth(int dim) { return dim == 3 ? 3 : 1; }
+
+// ---------------------------------------------------------------------------
+// residual
+// ---------------------------------------------------------------------------
+
+template <int DIM, int TX, int TY>
+struct ResidualSmem {
+    static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2, R = ring_depth(DIM);
+    static constexpr size_t xbytes = sizeof(double2) * R * HX * HY;
+    static constexpr size_t gbytes = sizeof(double) * R * GX * GY;
+    static constexpr size_t bytes = 2 * xbytes + 3 * gbytes;
+};
+
+template <int DIM, int TX, int TY>
+__global__ void __launch_bounds__(TX *TY)
+residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ xo_g,
+                const double2 *__restrict__ xn_g, double2 *__restrict__ F, double *partials,
+                unsigned int *counter, double *result)
+{
+    using L = ResidualSmem<DIM, TX, TY>;
+    constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, NT = TX * TY;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2 *sxn = reinterpret_cast<double2 *>(smem_raw);
+    double2 *sxo = sxn + R * HX * HY;
+    double *sGu = reinterpret_cast<double *>(sxo + R * HX * HY);
+    double *sGv = sGu + R * GX * GY;
+    double *sCb = sGv + R * GX * GY;
+
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    const int zb = (DIM == 3) ? blockIdx.z * ZCHUNK : 0;
+    const int ze = (DIM == 3) ? min(zb + ZCHUNK, nz) : 1;
+    const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
+
+    auto load_plane = [&](int kk) {
+        const int slot = (DIM == 3) ? ((kk % 3) + 3) % 3 : 0;
+        const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
+        for (int i = tid; i < HX * HY; i += NT) {
+            const int hx = i % HX, hy = i / HX;
+            const int gx = wrap_coord(x0 + hx - 2, nx, g.periodic);
+            const int gy = wrap_coord(y0 + hy - 2, ny, g.periodic);
+            const long long c = ((long long)gz * ny + gy) * nx + gx;
+            sxn[slot * HX * HY + i] = __ldg(xn_g + c);
+            sxo[slot * HX * HY + i] = __ldg(xo_g + c);
+        }
+    };
+
+    // G_u, G_v (scheme.py:270-287) and cbar (scheme.py:223-232) on tile + 1 halo of plane kk
+    auto compute_g = [&](int kk) {
+        const int s0 = (DIM == 3) ? ((kk % 3) + 3) % 3 : 0;
+        const int sm = (DIM == 3) ? (((kk - 1) % 3) + 3) % 3 : 0;
+        const int sp = (DIM == 3) ? (((kk + 1) % 3) + 3) % 3 : 0;
+        for (int i = tid; i < GX * GY; i += NT) {
+            const int gx = i % GX, gy = i / GX;
+            const int c = (gy + 1) * HX + (gx + 1);
+            const double2 n0 = sxn[s0 * HX * HY + c], o0 = sxo[s0 * HX * HY + c];
+            const double2 nxm = sxn[s0 * HX * HY + c - 1], nxp = sxn[s0 * HX * HY + c + 1];
+            const double2 nym = sxn[s0 * HX * HY + c - HX], nyp = sxn[s0 * HX * HY + c + HX];
+            const double2 oxm = sxo[s0 * HX * HY + c - 1], oxp = sxo[s0 * HX * HY + c + 1];
+            const double2 oym = sxo[s0 * HX * HY + c - HX], oyp = sxo[s0 * HX * HY + c + HX];
+            // Laplacian, axes summed x, y, z (grid.py:263-271)
+            double lun = (nxp.x - 2.0 * n0.x + nxm.x) * ihx;
+            double lvn = (nxp.y - 2.0 * n0.y + nxm.y) * ihx;
+            double luo = (oxp.x - 2.0 * o0.x + oxm.x) * ihx;
+            double lvo = (oxp.y - 2.0 * o0.y + oxm.y) * ihx;
+            lun += (nyp.x - 2.0 * n0.x + nym.x) * ihy;
+            lvn += (nyp.y - 2.0 * n0.y + nym.y) * ihy;
+            luo += (oyp.x - 2.0 * o0.x + oym.x) * ihy;
+            lvo += (oyp.y - 2.0 * o0.y + oym.y) * ihy;
+            if (DIM == 3) {
+                const double2 nzm = sxn[sm * HX * HY + c], nzp = sxn[sp * HX * HY + c];
+                const double2 ozm = sxo[sm * HX * HY + c], ozp = sxo[sp * HX * HY + c];
+                lun += (nzp.x - 2.0 * n0.x + nzm.x) * ihz;
+                lvn += (nzp.y - 2.0 * n0.y + nzm.y) * ihz;
+                luo += (ozp.x - 2.0 * o0.x + ozm.x) * ihz;
+                lvo += (ozp.y - 2.0 * o0.y + ozm.y) * ihz;
+            }
+            double phi, psi, dummy;
+            entropy_chord<false>(n0.x + n0.y, o0.x + o0.y, P, 0, phi, dummy);
+            entropy_chord<false>(n0.x - n0.y, o0.x - o0.y, P, 0, psi, dummy);
+            const double gu = -0.5 * P.alpha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) -
+                              0.5 * P.gamma * (lun + luo);
+            const double gv = -0.5 * P.beta * (n0.y + o0.y) + P.theta * (phi - psi) -
+                              0.5 * P.gamma * (lvn + lvo);
+            const int o = s0 * GX * GY + i;
+            sGu[o] = gu;
+            sGv[o] = gv;
+            sCb[o] = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
+        }
+    };
+
+    double acc_norm = 0.0, acc_gap = INFINITY;
+    const int x = x0 + tx, y = y0 + ty;
+    const bool active = x < nx && y < ny;
+    const bool per = g.periodic != 0;
+
+    if (DIM == 3) {
+        load_plane(zb - 2);
+        load_plane(zb - 1);
+        load_plane(zb);
+        __syncthreads();
+        compute_g(zb - 1);
+        __syncthreads();
+        load_plane(zb + 1);
+        __syncthreads();
+        compute_g(zb);
+    } else {
+        load_plane(0);
+        __syncthreads();
+        compute_g(0);
+    }
+    __syncthreads();
+
+    for (int k = zb; k < ze; ++k) {
+        if (DIM == 3) {
+            load_plane(k + 2);
+            __syncthreads();
+            compute_g(k + 1);
+            __syncthreads();
+        }
+        if (active) {
+            const int s0 = (DIM == 3) ? k % 3 : 0;
+            const int sm = (DIM == 3) ? (k + 2) % 3 : 0;
+            const int sp = (DIM == 3) ? (k + 1) % 3 : 0;
+            const int gc = (ty + 1) * GX + (tx + 1);
+            const double G0 = sGu[s0 * GX * GY + gc], C0 = sCb[s0 * GX * GY + gc];
+            // div(cbar grad G_u), flux form (grid.py:274-298); a Neumann wall face
+            // carries no flux (mirrored ghost: g[ghost] - g[cell] == 0).
+            double div = 0.0;
+            {
+                const bool lo = per || x > 0, hi = per || x < nx - 1;
+                const double fp = hi ? 0.5 * (C0 + sCb[s0 * GX * GY + gc + 1]) * (sGu[s0 * GX * GY + gc + 1] - G0) : 0.0;
+                const double fm = lo ? 0.5 * (C0 + sCb[s0 * GX * GY + gc - 1]) * (G0 - sGu[s0 * GX * GY + gc - 1]) : 0.0;
+                div += (fp - fm) * ihx;
+            }
+            {
+                const bool lo = per || y > 0, hi = per || y < ny - 1;
+                const double fp = hi ? 0.5 * (C0 + sCb[s0 * GX * GY + gc + GX]) * (sGu[s0 * GX * GY + gc + GX] - G0) : 0.0;
+                const double fm = lo ? 0.5 * (C0 + sCb[s0 * GX * GY + gc - GX]) * (G0 - sGu[s0 * GX * GY + gc - GX]) : 0.0;
+                div += (fp - fm) * ihy;
+            }
+            if (DIM == 3) {
+                const bool lo = per || k > 0, hi = per || k < nz - 1;
+                const double fp = hi ? 0.5 * (C0 + sCb[sp * GX * GY + gc]) * (sGu[sp * GX * GY + gc] - G0) : 0.0;
+                const double fm = lo ? 0.5 * (C0 + sCb[sm * GX * GY + gc]) * (G0 - sGu[sm * GX * GY + gc]) : 0.0;
+                div += (fp - fm) * ihz;
+            }
+            const int xc = (ty + 2) * HX + (tx + 2);
+            const double2 n0 = sxn[s0 * HX * HY + xc], o0 = sxo[s0 * HX * HY + xc];
+            double2 f;
+            f.x = (n0.x - o0.x) / dt - div;
+            f.y = (n0.y - o0.y) / dt + (C0 / P.rho) * sGv[s0 * GX * GY + gc];
+            F[((long long)k * ny + y) * nx + x] = f;
+            acc_norm += f.x * f.x + f.y * f.y;
+            acc_gap = fmin(acc_gap, cell_gap(n0.x, n0.y));
+            if (isnan(n0.x) || isnan(n0.y)) acc_gap = NAN;
+        }
+        if (DIM == 3) __syncthreads();
+    }
+    double v[2] = {acc_norm, acc_gap};
+    const int ops[2] = {RED_SUM, RED_MIN};
+    reduce_finish<2>(v, ops, partials, counter, result);
+}
+
+// ---------------------------------------------------------------------------
+// Jacobian coefficient planes (one thread per cell)
+// ---------------------------------------------------------------------------
+
+__global__ void jac_prepare_kernel(GridDev g, ParamsDev P, const double2 *__restrict__ xo,
+                                   const double2 *__restrict__ xn, double *__restrict__ coef)
+{
+    const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= g.n) return;
+    const int x = (int)(c % g.nx), y = (int)((c / g.nx) % g.ny), z = (int)(c / ((long long)g.nx * g.ny));
+    const double2 n0 = xn[c], o0 = xo[c];
+    double lun = 0.0, lvn = 0.0, luo = 0.0, lvo = 0.0;
+    for (int a = 0; a < g.dim; ++a) {
+        int cm[3] = {x, y, z}, cp[3] = {x, y, z};
+        const int na = a == 0 ? g.nx : (a == 1 ? g.ny : g.nz);
+        cm[a] = wrap_coord(cm[a] - 1, na, g.periodic);
+        cp[a] = wrap_coord(cp[a] + 1, na, g.periodic);
+        const long long im = ((long long)cm[2] * g.ny + cm[1]) * g.nx + cm[0];
+        const long long ip = ((long long)cp[2] * g.ny + cp[1]) * g.nx + cp[0];
+        const double2 nm = xn[im], np_ = xn[ip], om = xo[im], op = xo[ip];
+        lun += (np_.x - 2.0 * n0.x + nm.x) * g.ih2[a];
+        lvn += (np_.y - 2.0 * n0.y + nm.y) * g.ih2[a];
+        luo += (op.x - 2.0 * o0.x + om.x) * g.ih2[a];
+        lvo += (op.y - 2.0 * o0.y + om.y) * g.ih2[a];
+    }
+    double phi, psi, dp, dq;
+    entropy_chord<true>(n0.x + n0.y, o0.x + o0.y, P, 0, phi, dp);
+    entropy_chord<true>(n0.x - n0.y, o0.x - o0.y, P, 0, psi, dq);
+    const long long N = g.n;
+    coef[CO_S * N + c] = P.theta * (dp + dq);
+    coef[CO_D * N + c] = P.theta * (dp - dq);
+    coef[CO_CBAR * N + c] = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
+    coef[CO_GU * N + c] = -0.5 * P.alpha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) - 0.5 * P.gamma * (lun + luo);
+    coef[CO_CU * N + c] = (1.0 - 2.0 * n0.x) * (0.25 - n0.y * n0.y);    // physics.py:133-135
+    coef[CO_CV * N + c] = -2.0 * n0.y * n0.x * (1.0 - n0.x);
+    coef[CO_GV * N + c] = -0.5 * P.beta * (n0.y + o0.y) + P.theta * (phi - psi) - 0.5 * P.gamma * (lvn + lvo);
+}
+
+// ---------------------------------------------------------------------------
+// matrix-free Jacobian matvec
+//   dG_u = (-alpha/2 + S) w_u + D w_v - gamma/2 lap(w_u)
+//   eta  = (c_u w_u + c_v w_v) / 2            (linearised trapezoidal mobility)
+//   y_u  = w_u/dt - div(cbar grad dG_u) - div(eta_face grad G_u)
+//   y_v  = w_v/dt + cbar/rho (D w_u + (-beta/2 + S) w_v - gamma/2 lap(w_v)) + G_v/rho eta
+// term-for-term the operator assembled at scheme.py:471-482.
+// ---------------------------------------------------------------------------
+
+template <int DIM, int TX, int TY>
+struct MatvecSmem {
+    static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2, R = ring_depth(DIM);
+    static constexpr size_t bytes = sizeof(double2) * R * HX * HY + 4 * sizeof(double) * R * GX * GY;
+};
+
+template <int DIM, int TX, int TY>
+__global__ void __launch_bounds__(TX *TY)
+matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
+              const double2 *__restrict__ w_g, double2 *__restrict__ yout)
+{
+    using L = MatvecSmem<DIM, TX, TY>;
+    constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, NT = TX * TY;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2 *sw = reinterpret_cast<double2 *>(smem_raw);
+    double *sdG = reinterpret_cast<double *>(sw + R * HX * HY);
+    double *sEt = sdG + R * GX * GY;
+    double *sCb = sEt + R * GX * GY;
+    double *sGu = sCb + R * GX * GY;
+
+    const long long N = g.n;
+    const double *__restrict__ cS = coef + CO_S * N;
+    const double *__restrict__ cD = coef + CO_D * N;
+    const double *__restrict__ cC = coef + CO_CBAR * N;
+    const double *__restrict__ cG = coef + CO_GU * N;
+    const double *__restrict__ cU = coef + CO_CU * N;
+    const double *__restrict__ cV = coef + CO_CV * N;
+    const double *__restrict__ cGv = coef + CO_GV * N;
+
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int nx = g.nx, ny = g.ny, nz = g.nz;
+    const int zb = (DIM == 3) ? blockIdx.z * ZCHUNK : 0;
+    const int ze = (DIM == 3) ? min(zb + ZCHUNK, nz) : 1;
+    const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
+    const double hg = 0.5 * P.gamma;
+    const bool per = g.periodic != 0;
+
+    auto load_plane = [&](int kk) {
+        const int slot = (DIM == 3) ? ((kk % 3) + 3) % 3 : 0;
+        const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
+        for (int i = tid; i < HX * HY; i += NT) {
+            const int hx = i % HX, hy = i / HX;
+            const int gx = wrap_coord(x0 + hx - 2, nx, g.periodic);
+            const int gy = wrap_coord(y0 + hy - 2, ny, g.periodic);
+            sw[slot * HX * HY + i] = __ldg(w_g + ((long long)gz * ny + gy) * nx + gx);
+        }
+    };
+
+    auto compute_dg = [&](int kk) {
+        const int s0 = (DIM == 3) ? ((kk % 3) + 3) % 3 : 0;
+        const int sm = (DIM == 3) ? (((kk - 1) % 3) + 3) % 3 : 0;
+        const int sp = (DIM == 3) ? (((kk + 1) % 3) + 3) % 3 : 0;
+        const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
+        for (int i = tid; i < GX * GY; i += NT) {
+            const int gx = i % GX, gy = i / GX;
+            const int ex = wrap_coord(x0 + gx - 1, nx, g.periodic);
+            const int ey = wrap_coord(y0 + gy - 1, ny, g.periodic);
+            const long long c = ((long long)gz * ny + ey) * nx + ex;
+            const int h = (gy + 1) * HX + (gx + 1);
+            const double2 w0 = sw[s0 * HX * HY + h];
+            double lap = (sw[s0 * HX * HY + h + 1].x - 2.0 * w0.x + sw[s0 * HX * HY + h - 1].x) * ihx;
+            lap += (sw[s0 * HX * HY + h + HX].x - 2.0 * w0.x + sw[s0 * HX * HY + h - HX].x) * ihy;
+            if (DIM == 3) lap += (sw[sp * HX * HY + h].x - 2.0 * w0.x + sw[sm * HX * HY + h].x) * ihz;
+            const int o = s0 * GX * GY + i;
+            sdG[o] = (-0.5 * P.alpha + __ldg(cS + c)) * w0.x + __ldg(cD + c) * w0.y - hg * lap;
+            sEt[o] = 0.5 * (__ldg(cU + c) * w0.x + __ldg(cV + c) * w0.y);
+            sCb[o] = __ldg(cC + c);
+            sGu[o] = __ldg(cG + c);
+        }
+    };
+
+    const int x = x0 + tx, y = y0 + ty;
+    const bool active = x < nx && y < ny;
+
+    if (DIM == 3) {
+        load_plane(zb - 2);
+        load_plane(zb - 1);
+        load_plane(zb);
+        __syncthreads();
+        compute_dg(zb - 1);
+        __syncthreads();
+        load_plane(zb + 1);
+        __syncthreads();
+        compute_dg(zb);
+    } else {
+        load_plane(0);
+        __syncthreads();
+        compute_dg(0);
+    }
+    __syncthreads();
+
+    for (int k = zb; k < ze; ++k) {
+        if (DIM == 3) {
+            load_plane(k + 2);
+            __syncthreads();
+            compute_dg(k + 1);
+            __syncthreads();
+        }
+        if (active) {
+            const int s0 = (DIM == 3) ? k % 3 : 0;
+            const int sm = (DIM == 3) ? (k + 2) % 3 : 0;
+            const int sp = (DIM == 3) ? (k + 1) % 3 : 0;
+            const int gc = (ty + 1) * GX + (tx + 1);
+            const int b0 = s0 * GX * GY + gc;
+            const double dG0 = sdG[b0], E0 = sEt[b0], C0 = sCb[b0], G0 = sGu[b0];
+            double d1 = 0.0, d2 = 0.0;
+            auto face = [&](int bn, double ih, bool lo_ok, bool hi_ok, int bm) {
+                if (hi_ok) {
+                    d1 += 0.5 * (C0 + sCb[bn]) * (sdG[bn] - dG0) * ih;
+                    d2 += 0.5 * (E0 + sEt[bn]) * (sGu[bn] - G0) * ih;
+                }
+                if (lo_ok) {
+                    d1 -= 0.5 * (C0 + sCb[bm]) * (dG0 - sdG[bm]) * ih;
+                    d2 -= 0.5 * (E0 + sEt[bm]) * (G0 - sGu[bm]) * ih;
+                }
+            };
+            face(b0 + 1, ihx, per || x > 0, per || x < nx - 1, b0 - 1);
+            face(b0 + GX, ihy, per || y > 0, per || y < ny - 1, b0 - GX);
+            if (DIM == 3) face(sp * GX * GY + gc, ihz, per || k > 0, per || k < nz - 1, sm * GX * GY + gc);
+
+            const int h = (ty + 2) * HX + (tx + 2);
+            const double2 w0 = sw[s0 * HX * HY + h];
+            double lapv = (sw[s0 * HX * HY + h + 1].y - 2.0 * w0.y + sw[s0 * HX * HY + h - 1].y) * ihx;
+            lapv += (sw[s0 * HX * HY + h + HX].y - 2.0 * w0.y + sw[s0 * HX * HY + h - HX].y) * ihy;
+            if (DIM == 3) lapv += (sw[sp * HX * HY + h].y - 2.0 * w0.y + sw[sm * HX * HY + h].y) * ihz;
+            const long long c = ((long long)k * ny + y) * nx + x;
+            const double S = __ldg(cS + c), D = __ldg(cD + c), Gv = __ldg(cGv + c);
+            double2 out;
+            out.x = w0.x / dt - d1 - d2;
+            out.y = w0.y / dt + (C0 / P.rho) * (D * w0.x + (-0.5 * P.beta + S) * w0.y - hg * lapv) + (Gv / P.rho) * E0;
+            yout[c] = out;
+        }
+        if (DIM == 3) __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// explicit Jacobian blocks on the radius-2 stencil
+// ---------------------------------------------------------------------------
+
+template <int DIM>
+__global__ void jac_blocks_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
+                                  double *__restrict__ out, int noff)
+{
+    const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (c >= g.n) return;
+    const int x = (int)(c % g.nx), y = (int)((c / g.nx) % g.ny), z = (int)(c / ((long long)g.nx * g.ny));
+    double blk[25][4];
+    jac_row_blocks<DIM>(g, P, dt, coef, x, y, z, blk, noff);
+    for (int o = 0; o < noff; ++o)
+        for (int e = 0; e < 4; ++e) out[(c * noff + o) * 4 + e] = blk[o][e];
+}
+
+// ---------------------------------------------------------------------------
+// elementwise / reduction helpers on the state
+// ---------------------------------------------------------------------------
+
+__global__ void chord_kernel(ParamsDev P, const double *a, const double *b, long long n, int force_exact,
+                             double *val, double *der)
+{
+    const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double v, d = 0.0;
+    if (der) entropy_chord<true>(a[i], b[i], P, force_exact, v, d);
+    else entropy_chord<false>(a[i], b[i], P, force_exact, v, d);
+    val[i] = v;
+    if (der) der[i] = d;
+}
+
+__global__ void gap_kernel(long long n, const double2 *__restrict__ x, double *partials, unsigned int *counter,
+                           double *result)
+{
+    double gmin = INFINITY;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double2 s = x[i];
+        const double c = cell_gap(s.x, s.y);
+        gmin = red_combine(gmin, c, RED_MIN);
+    }
+    double v[1] = {gmin};
+    const int ops[1] = {RED_MIN};
+    reduce_finish<1>(v, ops, partials, counter, result);
+}
+
+// energy (physics.py:313-331, grad_sq_avg grid.py:249-260), mass, max|v|
+__global__ void diagnostics_kernel(GridDev g, ParamsDev P, const double2 *__restrict__ x, double *partials,
+                                   unsigned int *counter, double *result)
+{
+    double e = 0.0, m = 0.0, vmax = -INFINITY;
+    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < g.n; c += (long long)gridDim.x * blockDim.x) {
+        const int xi = (int)(c % g.nx), yi = (int)((c / g.nx) % g.ny), zi = (int)(c / ((long long)g.nx * g.ny));
+        const double2 s = x[c];
+        double gsu = 0.0, gsv = 0.0;
+        for (int a = 0; a < g.dim; ++a) {
+            int cm[3] = {xi, yi, zi}, cp[3] = {xi, yi, zi};
+            const int na = a == 0 ? g.nx : (a == 1 ? g.ny : g.nz);
+            cm[a] = wrap_coord(cm[a] - 1, na, g.periodic);
+            cp[a] = wrap_coord(cp[a] + 1, na, g.periodic);
+            const double2 sm = x[((long long)cm[2] * g.ny + cm[1]) * g.nx + cm[0]];
+            const double2 sp = x[((long long)cp[2] * g.ny + cp[1]) * g.nx + cp[0]];
+            const double fu = (sp.x - s.x) * g.ih[a], bu = (s.x - sm.x) * g.ih[a];
+            const double fv = (sp.y - s.y) * g.ih[a], bv = (s.y - sm.y) * g.ih[a];
+            gsu += 0.5 * (fu * fu + bu * bu);
+            gsv += 0.5 * (fv * fv + bv * bv);
+        }
+        const double e1 = 0.5 * P.alpha * s.x * (1.0 - s.x) - 0.5 * P.beta * s.y * s.y;
+        const double e2 = P.theta * (entropy(s.x + s.y) + entropy(s.x - s.y));
+        e += e1 + e2 + 0.5 * P.gamma * (gsu + gsv);
+        m += s.x;
+        vmax = red_combine(vmax, fabs(s.y), RED_MAX);
+    }
+    double v[3] = {e, m, vmax};
+    const int ops[3] = {RED_SUM, RED_SUM, RED_MAX};
+    reduce_finish<3>(v, ops, partials, counter, result);
+}
+
+__global__ void trial_kernel(long long n, const double2 *__restrict__ x, const double2 *__restrict__ s, double lam,
+                             double2 *__restrict__ y, double *partials, unsigned int *counter, double *result)
+{
+    double gmin = INFINITY;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double2 a = x[i], d = s[i];
+        double2 r;
+        r.x = a.x + lam * d.x;
+        r.y = a.y + lam * d.y;
+        y[i] = r;
+        gmin = red_combine(gmin, cell_gap(r.x, r.y), RED_MIN);
+    }
+    double v[1] = {gmin};
+    const int ops[1] = {RED_MIN};
+    reduce_finish<1>(v, ops, partials, counter, result);
+}
+
+// _feasible_step_cap (newton.py:75-99): min over bounds of (value - lo)/-slope and (hi - value)/slope
+__global__ void feasible_cap_kernel(long long n, const double2 *__restrict__ x, const double2 *__restrict__ s,
+                                    double margin, double *partials, unsigned int *counter, double *result)
+{
+    double cap = INFINITY;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double2 a = x[i], d = s[i];
+        const double vals[4] = {a.x, a.x + a.y, a.x - a.y, a.y};
+        const double slopes[4] = {d.x, d.x + d.y, d.x - d.y, d.y};
+        const double lo[4] = {margin, margin, margin, -0.5 + margin};
+        const double hi[4] = {1.0 - margin, 1.0 - margin, 1.0 - margin, 0.5 - margin};
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            if (slopes[b] < 0.0) cap = red_combine(cap, (vals[b] - lo[b]) / -slopes[b], RED_MIN);
+            if (slopes[b] > 0.0) cap = red_combine(cap, (hi[b] - vals[b]) / slopes[b], RED_MIN);
+        }
+    }
+    double v[1] = {cap};
+    const int ops[1] = {RED_MIN};
+    reduce_finish<1>(v, ops, partials, counter, result);
+}
+
+__global__ void rms_diff_kernel(long long n, const double *__restrict__ a, const double *__restrict__ b,
+                                double *partials, unsigned int *counter, double *result)
+{
+    double acc = 0.0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double d = a[i] - b[i];
+        acc += d * d;
+    }
+    double v[1] = {acc};
+    const int ops[1] = {RED_SUM};
+    reduce_finish<1>(v, ops, partials, counter, result);
+}
+
+int red_grid(long long n)
+{
+    long long b = (n + kRedThreads * 4 - 1) / (kRedThreads * 4);
+    if (b < 1) b = 1;
+    if (b > kRedBlocks) b = kRedBlocks;
+    return (int)b;
+}
+
+template <typename K>
+acch_status set_smem(K kernel, size_t bytes)
+{
+    static_assert(sizeof(K) > 0, "");
+    ACCH_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    return ACCH_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+
+int stencil_offsets(int dim, int (*off)[3])
+{
+    int n = 0;
+    const int zr = dim == 3 ? 2 : 0;
+    for (int dz = -zr; dz <= zr; ++dz)
+        for (int dy = -2; dy <= 2; ++dy)
+            for (int dx = -2; dx <= 2; ++dx) {
+                if (abs(dx) + abs(dy) + abs(dz) > 2) continue;
+                if (off) {
+                    off[n][0] = dx;
+                    off[n][1] = dy;
+                    off[n][2] = dz;
+                }
+                ++n;
+            }
+    return n;
+}
+
+acch_status launch_residual(acch_ctx *ctx, const double *x_old, double dt, const double *x, double *F)
+{
+    const GridDev &g = ctx->g;
+    const dim3 block(RTX, RTY);
+    if (g.dim == 3) {
+        using L = ResidualSmem<3, RTX, RTY>;
+        static bool configured = false;
+        if (!configured) {
+            acch_status st = set_smem(residual_kernel<3, RTX, RTY>, L::bytes);
+            if (st != ACCH_OK) return st;
+            configured = true;
+        }
+        const dim3 grid((g.nx + RTX - 1) / RTX, (g.ny + RTY - 1) / RTY, (g.nz + ZCHUNK - 1) / ZCHUNK);
+        residual_kernel<3, RTX, RTY><<<grid, block, L::bytes, ctx->stream>>>(
+            g, ctx->p, dt, (const double2 *)x_old, (const double2 *)x, (double2 *)F, ctx->d_partials,
+            ctx->d_counter, ctx->d_result);
+    } else {
+        using L = ResidualSmem<2, RTX, RTY>;
+        const dim3 grid((g.nx + RTX - 1) / RTX, (g.ny + RTY - 1) / RTY, 1);
+        residual_kernel<2, RTX, RTY><<<grid, block, L::bytes, ctx->stream>>>(
+            g, ctx->p, dt, (const double2 *)x_old, (const double2 *)x, (double2 *)F, ctx->d_partials,
+            ctx->d_counter, ctx->d_result);
+    }
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_jacobian_prepare(acch_ctx *ctx, const double *x_old, double dt, const double *x, double *coef)
+{
+    (void)dt;
+    const long long n = ctx->g.n;
+    jac_prepare_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->g, ctx->p, (const double2 *)x_old,
+                                                                          (const double2 *)x, coef);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
+{
+    const GridDev &g = ctx->g;
+    const dim3 block(MTX, MTY);
+    if (g.dim == 3) {
+        using L = MatvecSmem<3, MTX, MTY>;
+        static bool configured = false;
+        if (!configured) {
+            acch_status st = set_smem(matvec_kernel<3, MTX, MTY>, L::bytes);
+            if (st != ACCH_OK) return st;
+            configured = true;
+        }
+        const dim3 grid((g.nx + MTX - 1) / MTX, (g.ny + MTY - 1) / MTY, (g.nz + ZCHUNK - 1) / ZCHUNK);
+        matvec_kernel<3, MTX, MTY><<<grid, block, L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
+                                                                         (double2 *)y);
+    } else {
+        using L = MatvecSmem<2, MTX, MTY>;
+        const dim3 grid((g.nx + MTX - 1) / MTX, (g.ny + MTY - 1) / MTY, 1);
+        matvec_kernel<2, MTX, MTY><<<grid, block, L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
+                                                                         (double2 *)y);
+    }
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_jacobian_blocks(acch_ctx *ctx, const double *coef, double dt, double *out)
+{
+    const int noff = stencil_offsets(ctx->g.dim, nullptr);
+    const long long n = ctx->g.n;
+    if (ctx->g.dim == 3)
+        jac_blocks_kernel<3><<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(ctx->g, ctx->p, dt, coef, out, noff);
+    else
+        jac_blocks_kernel<2><<<(unsigned)((n + 127) / 128), 128, 0, ctx->stream>>>(ctx->g, ctx->p, dt, coef, out, noff);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_chord(acch_ctx *ctx, const double *a, const double *b, long long n, int force_exact, double *val,
+                         double *der)
+{
+    if (n <= 0) return ACCH_OK;
+    chord_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->p, a, b, n, force_exact, val, der);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_gap(acch_ctx *ctx, const double *x)
+{
+    const long long n = ctx->g.n;
+    gap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, ctx->d_partials, ctx->d_counter,
+                                                            ctx->d_result);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_diagnostics(acch_ctx *ctx, const double *x)
+{
+    diagnostics_kernel<<<red_grid(ctx->g.n), kRedThreads, 0, ctx->stream>>>(ctx->g, ctx->p, (const double2 *)x,
+                                                                           ctx->d_partials, ctx->d_counter,
+                                                                           ctx->d_result);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_trial(acch_ctx *ctx, const double *x, const double *s, double lam, double *y)
+{
+    const long long n = ctx->g.n;
+    trial_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, (const double2 *)s, lam,
+                                                              (double2 *)y, ctx->d_partials, ctx->d_counter,
+                                                              ctx->d_result);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_feasible_cap(acch_ctx *ctx, const double *x, const double *s, double margin)
+{
+    const long long n = ctx->g.n;
+    feasible_cap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, (const double2 *)s, margin,
+                                                                     ctx->d_partials, ctx->d_counter, ctx->d_result);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+acch_status launch_rms_diff(acch_ctx *ctx, const double *a, const double *b, long long n)
+{
+    rms_diff_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, a, b, ctx->d_partials, ctx->d_counter,
+                                                                 ctx->d_result);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+

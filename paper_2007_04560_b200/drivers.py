@@ -1,0 +1,233 @@
+"""Run configuration and the accepted-step time loop (the hot path's caller:
+the reference's acch/cli/config.py:23-120 dataclasses and
+acch/cli/drivers.py:26-184 ``build_initial_state`` / ``simulate``).
+
+INI parsing, file output and the experiment drivers are out of scope; the
+dataclasses keep the reference's field names and defaults so a RunConfig
+built for the reference maps over field by field."""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+
+from .exceptions import ConfigError, SolverStallError
+from .grid import Grid
+from .linalg import SchwarzPreconditioner, SchwarzVariant, SubdomainSolverSpec, partition
+from .newton import NewtonConfig, newton_solve
+from .physics import Params, State, diagnostics
+from .scheme import StepProblem
+from .timestep import StepController
+
+COMPLETED = "completed"
+STALLED = "stalled"
+
+
+@dataclass(frozen=True)
+class InitialSpec:
+    kind: str = "random_uniform"
+    center_u: float = 0.55
+    amplitude: float = 0.05
+    seed: int = 1234
+
+    def __post_init__(self):
+        if self.kind not in ("trigonometric", "random_uniform"):
+            raise ConfigError(f"unknown initial condition {self.kind!r}")
+        if self.kind == "random_uniform":
+            lo_u, hi_u = self.center_u - self.amplitude, self.center_u + self.amplitude
+            if not (0.0 < lo_u - self.amplitude and hi_u + self.amplitude < 1.0):
+                raise ConfigError("random initial condition can produce inadmissible states")
+
+
+@dataclass(frozen=True)
+class TimeSpec:
+    horizon: float
+    mode: str = "adaptive"
+    dt: float = 1e-4
+    dt_min: float = 1e-4
+    dt_max: float = 10.0
+    eta: float | None = None
+
+
+@dataclass(frozen=True)
+class SolverSpec:
+    preconditioner: SchwarzVariant = SchwarzVariant.LEFT_RAS
+    overlap: int = 1
+    subdomain_solver: SubdomainSolverSpec = SubdomainSolverSpec("ilu", 0)
+    reuse: bool = True
+    subdomains: int = 0
+    refreeze_every: int = 1
+    rel_tol: float = 1e-6
+    abs_tol: float = 1e-13
+    lin_rel_tol: float = 1e-8
+    lin_abs_tol: float = 1e-14
+    max_newton: int = 50
+    gmres_restart: int = 30
+    max_linear_iterations: int = 500
+    orthogonalization: str = "cgs2"
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    grid: Grid
+    params: Params
+    initial: InitialSpec
+    time: TimeSpec
+    solver: SolverSpec = SolverSpec()
+
+    @property
+    def eta(self) -> float:
+        if self.time.eta is not None:
+            return self.time.eta
+        return 1e4 if self.grid.dim == 2 else 1e2
+
+    def make_controller(self) -> StepController:
+        if self.time.mode == "fixed":
+            return StepController(self.time.dt, self.time.dt, self.eta, fixed_dt=self.time.dt)
+        return StepController(self.time.dt_min, self.time.dt_max, self.eta)
+
+    def make_newton_config(self) -> NewtonConfig:
+        s = self.solver
+        return NewtonConfig(rel_tol=s.rel_tol, abs_tol=s.abs_tol, lin_rel_tol=s.lin_rel_tol,
+                            lin_abs_tol=s.lin_abs_tol, max_iterations=s.max_newton, gmres_restart=s.gmres_restart,
+                            max_linear_iterations=s.max_linear_iterations, reuse_factorization=s.reuse,
+                            refactor_on_entry=s.refreeze_every <= 1, orthogonalization=s.orthogonalization)
+
+    def with_solver(self, **kw) -> "RunConfig":
+        return replace(self, solver=replace(self.solver, **kw))
+
+    def with_time(self, **kw) -> "RunConfig":
+        return replace(self, time=replace(self.time, **kw))
+
+
+def initial_fields(config: RunConfig):
+    """Host fields of the configured initial condition (drivers.py:26-46):
+    one seeded generator, u drawn before v, reversed-axis shape, so the
+    inputs are bitwise those of the reference."""
+    grid = config.grid
+    spec = config.initial
+    if spec.kind == "trigonometric":
+        if grid.dim != 2:
+            raise ConfigError("trigonometric initial condition is 2D only")
+        x, y = grid.center_mesh()
+        sx = np.sin(2.0 * np.pi * x) ** 2
+        cy = np.cos(2.0 * np.pi * y) ** 2
+        return 0.4 * (sx + cy) + 0.1, 0.4 * (sx - cy)
+    rng = np.random.default_rng(spec.seed)
+    u = spec.center_u + rng.uniform(-spec.amplitude, spec.amplitude, grid.array_shape)
+    v = rng.uniform(-spec.amplitude, spec.amplitude, grid.array_shape)
+    return u, v
+
+
+def build_initial_state(config: RunConfig, device=None) -> State:
+    u, v = initial_fields(config)
+    return State.from_interior(config.grid, u, v, device=device)
+
+
+@dataclass
+class HistoryRow:
+    step: int
+    time: float
+    dt: float
+    energy: float
+    mass_u: float
+    max_abs_v: float
+    newton: int
+    gmres: int
+    wall_s: float
+
+
+@dataclass
+class SimulationResult:
+    status: str
+    history: list
+    final_state: State
+    controller: StepController
+    factorizations: int = 0
+    events: list = field(default_factory=list)
+
+    @property
+    def completed(self) -> bool:
+        return self.status == COMPLETED
+
+
+def simulate(config: RunConfig, threads: int = 1, max_steps: int | None = None, state: State | None = None,
+             device=None, diagnostics_every: int = 1) -> SimulationResult:
+    """Advance from t = 0 to the horizon (drivers.py:76-184): predict dt,
+    solve (retrying with the controller's smaller dt on divergence and a
+    fresh factorisation), record energy / mass / max|v| per accepted step.
+    ``events`` lists (step, dt, reason) for every divergence."""
+    grid = config.grid
+    if state is None:
+        state = build_initial_state(config, device)
+    controller = config.make_controller()
+    n_sub = config.solver.subdomains or threads
+    decomposition = partition(grid, n_sub, config.solver.overlap)
+    newton_cfg = config.make_newton_config()
+    precond = SchwarzPreconditioner(decomposition, config.solver.preconditioner, config.solver.subdomain_solver)
+    history = []
+    events = []
+
+    def row(step, t, dt, st, newton, gm, wall):
+        if diagnostics_every and (step % diagnostics_every == 0):
+            e, m, v = diagnostics(st, config.params)
+        else:
+            e = m = v = float("nan")
+        history.append(HistoryRow(step, t, dt, e, m, v, newton, gm, wall))
+
+    row(0, 0.0, 0.0, state, 0, 0, 0.0)
+    status = COMPLETED
+    factorizations = 0
+    t = 0.0
+    step = 0
+    dt_prev = None
+    x_now = state.vector
+    x_prev = None
+    since = 0
+    refreeze_every = max(1, config.solver.refreeze_every)
+    horizon = config.time.horizon
+    while t < horizon * (1.0 - 1e-12):
+        if max_steps is not None and step >= max_steps:
+            break
+        step += 1
+        if step == 1 or x_prev is None:
+            dt = controller.initial_dt()
+        else:
+            dt = controller.predict_dt(x_now, x_prev, dt_prev)
+        if since >= refreeze_every:
+            precond.invalidate()
+            since = 0
+        wall0 = time.perf_counter()
+        newton_count = gmres_count = 0
+        try:
+            while True:
+                prob = StepProblem.create(grid, config.params, state, dt)
+                new_state, report = newton_solve(prob, state, newton_cfg, precond)
+                newton_count += report.newton_iterations
+                gmres_count += report.gmres_iterations
+                factorizations += report.factorizations
+                if report.converged:
+                    break
+                events.append((step, dt, report.reason))
+                dt = controller.on_divergence(dt)
+                precond.invalidate()
+                since = 0
+        except SolverStallError:
+            status = STALLED
+            break
+        since += 1
+        controller.note_success()
+        wall = time.perf_counter() - wall0
+        t += dt
+        x_prev = x_now
+        x_now = new_state.vector
+        dt_prev = dt
+        state = new_state
+        row(step, t, dt, state, newton_count, gmres_count, wall)
+    return SimulationResult(status, history, state, controller, factorizations, events)
+
+
+__all__ = ["InitialSpec", "TimeSpec", "SolverSpec", "RunConfig", "initial_fields", "build_initial_state",
+           "HistoryRow", "SimulationResult", "simulate", "COMPLETED", "STALLED"]

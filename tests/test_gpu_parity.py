@@ -1,0 +1,271 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden vectors and the CPU oracle on the same seeded inputs.
+
+Tolerances (north_star): fp64 residual relative error <= 1e-12; fields
+after N steps <= 1e-8 relative L2; identical accepted dt sequence (1e-10
+relative), identical Newton counts and retry events; mass conserved and the
+discrete energy monotone."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+from paper_2007_04560_b200.exceptions import InadmissibleStateError  # noqa: E402
+from paper_2007_04560_b200.grid import BoundaryCondition, Grid  # noqa: E402
+from paper_2007_04560_b200.linalg import (SchwarzPreconditioner, SchwarzVariant,  # noqa: E402
+                                          SubdomainSolverSpec, gmres, partition)
+from paper_2007_04560_b200.newton import NewtonConfig, newton_solve  # noqa: E402
+from paper_2007_04560_b200.physics import (Params, State, entropy_chord,  # noqa: E402
+                                           entropy_chord_with_deriv, is_admissible, diagnostics)
+from paper_2007_04560_b200.scheme import (StepProblem, assemble_jacobian,  # noqa: E402
+                                          residual_vector)
+
+PARAMS = Params(4.0, 2.0, 0.005, 0.1, 0.001)
+STENCIL = ["2d_neu", "2d_per", "2d_per4", "3d_neu", "3d_per", "2d_per_big", "3d_neu_big"]
+DEV = "cuda:0"
+
+
+def grid_of(z):
+    counts = tuple(int(c) for c in z["counts"])
+    bc = BoundaryCondition.PERIODIC if bool(z["periodic"]) else BoundaryCondition.NEUMANN
+    return Grid(counts, tuple(1.0 for _ in counts), bc)
+
+
+def st(grid, u, v):
+    return State.from_interior(grid, u, v, device=DEV)
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+# --------------------------------------------------------------------------- physics
+
+def test_chord_battery():
+    z = golden("chord.npz")
+    a = torch.tensor(z["a"], device=DEV)
+    b = torch.tensor(z["b"], device=DEV)
+    val, der = entropy_chord_with_deriv(a, b, 10)
+    np.testing.assert_allclose(host(val), z["val"], rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(host(der), z["der"], rtol=1e-12, atol=1e-13)
+    assert np.array_equal(host(entropy_chord(a, b)), host(val))
+
+
+def test_chord_known_answers():
+    assert entropy_chord(0.6, 0.4) == 0.0
+    assert abs(entropy_chord(0.7, 0.5) - 0.41141439252525923) <= 1e-12
+
+
+# --------------------------------------------------------------------------- scheme
+
+@pytest.mark.parametrize("tag", STENCIL)
+def test_residual_matches_reference(tag):
+    z = golden(f"stencil_{tag}.npz")
+    g = grid_of(z)
+    prob = StepProblem.create(g, PARAMS, st(g, z["uo"], z["vo"]), float(z["dt"]))
+    F = host(residual_vector(prob, st(g, z["un"], z["vn"])))
+    assert np.max(np.abs(F - z["F"])) <= 1e-12 * np.max(np.abs(z["F"]))
+    F0 = host(residual_vector(prob, st(g, z["uo"], z["vo"])))
+    assert np.max(np.abs(F0 - z["F0"])) <= 1e-12 * np.max(np.abs(z["F0"]))
+
+
+@pytest.mark.parametrize("tag", STENCIL)
+def test_jacobian_matvec_matches_reference(tag):
+    z = golden(f"stencil_{tag}.npz")
+    g = grid_of(z)
+    prob = StepProblem.create(g, PARAMS, st(g, z["uo"], z["vo"]), float(z["dt"]))
+    J = assemble_jacobian(prob, st(g, z["un"], z["vn"]))
+    y = host(J.matvec(torch.tensor(z["w"], device=DEV)))
+    assert np.max(np.abs(y - z["Jw"])) <= 1e-12 * np.max(np.abs(z["Jw"]))
+
+
+@pytest.mark.parametrize("tag", ["2d_neu", "2d_per", "2d_per4", "3d_neu", "3d_per"])
+def test_jacobian_blocks_match_reference_bsr(tag):
+    from scipy import sparse
+    z = golden(f"stencil_{tag}.npz")
+    g = grid_of(z)
+    prob = StepProblem.create(g, PARAMS, st(g, z["uo"], z["vo"]), float(z["dt"]))
+    J = assemble_jacobian(prob, st(g, z["un"], z["vn"]))
+    got = J.to_bsr().toarray()
+    ref = sparse.bsr_matrix((z["J_blocks"], z["J_indices"], z["J_indptr"]),
+                            shape=(2 * g.n_cells, 2 * g.n_cells)).toarray()
+    assert np.max(np.abs(got - ref)) <= 1e-12 * np.max(np.abs(ref))
+    # same structural skeleton (scheme.py:166-188)
+    ip = J.to_bsr()
+    ip.sort_indices()
+    assert ip.indices.size == z["J_indices"].size
+
+
+@pytest.mark.parametrize("tag", STENCIL)
+def test_energy_and_gap_match_reference(tag):
+    z = golden(f"stencil_{tag}.npz")
+    g = grid_of(z)
+    e, _, _ = diagnostics(st(g, z["un"], z["vn"]), PARAMS)
+    assert abs(e - float(z["energy_new"])) <= 1e-13 * abs(float(z["energy_new"]))
+    from paper_2007_04560_b200.physics import state_gap
+    assert state_gap(st(g, z["un"], z["vn"])) == float(z["gap"])
+
+
+def test_residual_rejects_inadmissible():
+    g = Grid((6, 6), (1.0, 1.0), BoundaryCondition.NEUMANN)
+    u = np.full((6, 6), 0.5)
+    v = np.zeros((6, 6))
+    prob = StepProblem.create(g, PARAMS, st(g, u, v), 1e-3)
+    u2 = u.copy()
+    u2[0, 0] = 1.0 - 1e-14
+    with pytest.raises(InadmissibleStateError):
+        residual_vector(prob, st(g, u2, v))
+    u2[0, 0] = np.nan
+    assert not is_admissible(st(g, u2, v))
+
+
+@pytest.mark.parametrize("bc", [BoundaryCondition.PERIODIC, BoundaryCondition.NEUMANN])
+def test_uniform_state_is_a_fixed_point(bc):
+    g = Grid((12, 10, 6), (1.0, 1.0, 1.0), bc)
+    s = st(g, np.full(g.array_shape, 0.37), np.full(g.array_shape, 0.05))
+    prob = StepProblem.create(g, PARAMS, s, 1e-2)
+    F = host(residual_vector(prob, s))
+    assert np.all(F == 0.0)
+
+
+# --------------------------------------------------------------------------- linalg
+
+def _schwarz_setup(tag):
+    z = golden(f"schwarz_{tag}.npz")
+    g = grid_of(z)
+    prob = StepProblem.create(g, PARAMS, st(g, z["uo"], z["vo"]), float(z["dt"]))
+    J = assemble_jacobian(prob, st(g, z["un"], z["vn"]))
+    return z, g, J
+
+
+@pytest.mark.parametrize("tag", ["2d_neu", "2d_per", "3d_per", "3d_neu"])
+@pytest.mark.parametrize("variant", ["asm", "ras-left", "ras-right"])
+@pytest.mark.parametrize("solver", ["ilu0", "ilu1", "ilu2", "lu"])
+def test_schwarz_apply_matches_reference(tag, variant, solver):
+    z, g, J = _schwarz_setup(tag)
+    pre = SchwarzPreconditioner(partition(g, int(z["nsub"]), int(z["overlap"])), SchwarzVariant(variant),
+                                SubdomainSolverSpec.from_string(solver))
+    assert pre.update(J) is True
+    assert pre.update(J, reuse=True) is False
+    out = host(pre.apply(torch.tensor(z["r"], device=DEV)))
+    ref = z[f"{variant}_{solver}"]
+    assert np.max(np.abs(out - ref)) <= 1e-10 * np.max(np.abs(ref))
+    # bitwise reproducible
+    assert np.array_equal(out, host(pre.apply(torch.tensor(z["r"], device=DEV))))
+
+
+def test_apply_before_update_raises():
+    g = Grid((8, 8), (1.0, 1.0), BoundaryCondition.PERIODIC)
+    pre = SchwarzPreconditioner(partition(g, 2, 1), SchwarzVariant.LEFT_RAS, SubdomainSolverSpec("ilu", 0))
+    with pytest.raises(RuntimeError):
+        pre.apply(torch.zeros(128, dtype=torch.float64, device=DEV))
+
+
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+def test_gmres_matches_reference(ortho):
+    z = golden("gmres.npz")
+    g = Grid((16, 12), (1.0, 1.0), BoundaryCondition.PERIODIC)
+    prob = StepProblem.create(g, PARAMS, st(g, z["uo"], z["vo"]), 1e-3)
+    J = assemble_jacobian(prob, st(g, z["un"], z["vn"]))
+    pre = SchwarzPreconditioner(partition(g, 4, 1), SchwarzVariant.LEFT_RAS, SubdomainSolverSpec("ilu", 0))
+    pre.update(J)
+    b = torch.tensor(z["b"], device=DEV)
+    res = gmres(J, b, pre, 1e-8, 1e-14, 30, 500, ortho=ortho)
+    assert res.converged == bool(z["conv"]) and res.iterations == int(z["its"])
+    assert np.linalg.norm(host(res.x) - z["x"]) <= 1e-9 * np.linalg.norm(z["x"])
+    r5 = gmres(J.matvec, b, pre, 1e-10, 1e-14, 5, 500, ortho=ortho)
+    assert r5.iterations == int(z["its5"]) and r5.converged == bool(z["conv5"])
+    assert np.linalg.norm(host(r5.x) - z["x5"]) <= 1e-9 * np.linalg.norm(z["x5"])
+    rn = gmres(J, b, None, 1e-8, 1e-14, 30, 60, ortho=ortho)
+    assert rn.iterations == int(z["itsn"]) and rn.converged == bool(z["convn"])
+    assert np.linalg.norm(host(rn.x) - z["xn"]) <= 1e-8 * np.linalg.norm(z["xn"])
+
+
+# --------------------------------------------------------------------------- newton
+
+NEWTON = {
+    "a": ((12, 12), False, 1e-3, 4, 1, "ilu0", {}),
+    "b": ((8, 8), False, 0.01, 2, 1, "lu", dict(reuse_factorization=False)),
+    "c": ((8, 8), False, 1.0, 2, 1, "lu", dict(reuse_factorization=False)),
+    "d": ((8, 8), False, 1e-2, 2, 1, "ilu0", dict(max_linear_iterations=1, gmres_restart=1)),
+    "e": ((10, 8, 6), True, 1e-3, 4, 1, "ilu0", {}),
+}
+
+
+@pytest.mark.parametrize("tag", sorted(NEWTON))
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+def test_newton_matches_reference(tag, ortho):
+    z = golden("newton.npz")
+    counts, periodic, dt, nsub, ov, solver, kw = NEWTON[tag]
+    bc = BoundaryCondition.PERIODIC if periodic else BoundaryCondition.NEUMANN
+    g = Grid(counts, tuple(1.0 for _ in counts), bc)
+    s0 = st(g, z[f"{tag}_u"], z[f"{tag}_v"])
+    prob = StepProblem.create(g, PARAMS, s0, dt)
+    pre = SchwarzPreconditioner(partition(g, nsub, ov), SchwarzVariant.LEFT_RAS,
+                                SubdomainSolverSpec.from_string(solver))
+    trace = []
+    sol, rep = newton_solve(prob, s0, NewtonConfig(orthogonalization=ortho, **kw), pre, trace=trace)
+    conv, nit, git, fac = (int(t) for t in z[f"{tag}_report"])
+    assert rep.converged == bool(conv)
+    assert rep.newton_iterations == nit
+    assert abs(rep.gmres_iterations - git) <= 1
+    assert rep.factorizations == fac
+    assert (rep.reason or "") == str(z[f"{tag}_reason"])
+    ref = z[f"{tag}_x"]
+    assert np.linalg.norm(host(sol.vector) - ref) <= 1e-8 * np.linalg.norm(ref)
+    assert is_admissible(sol)
+
+
+# --------------------------------------------------------------------------- simulate
+
+def _run_sim(tag, ortho="cgs2"):
+    from paper_2007_04560_b200.drivers import InitialSpec, RunConfig, SolverSpec, TimeSpec, simulate
+    z = golden(f"sim_{tag}.npz")
+    g = grid_of(z)
+    center, amp, dt, horizon, nsub, eta, max_steps = (float(t) for t in z["meta"])
+    cfg = RunConfig(g, PARAMS, InitialSpec("random_uniform", center, amp, 1234),
+                    TimeSpec(horizon=horizon, mode=str(z["mode"]), dt=dt, dt_min=1e-4, dt_max=10.0,
+                             eta=None if eta < 0 else eta),
+                    SolverSpec(preconditioner=SchwarzVariant(str(z["variant"])),
+                               subdomain_solver=SubdomainSolverSpec.from_string(str(z["solver"])),
+                               subdomains=int(nsub), orthogonalization=ortho))
+    res = simulate(cfg, max_steps=None if max_steps < 0 else int(max_steps), device=DEV)
+    return z, g, res
+
+
+def _check_sim(z, g, res):
+    ref = z["rows"]
+    assert res.status == str(z["status"])
+    got = np.array([[r.step, r.time, r.dt, r.energy, r.mass_u, r.max_abs_v, r.newton, r.gmres]
+                    for r in res.history])
+    assert got.shape == ref.shape
+    np.testing.assert_allclose(got[:, 2], ref[:, 2], rtol=1e-10)   # accepted dt sequence
+    np.testing.assert_allclose(got[:, 3], ref[:, 3], rtol=1e-10)   # energy
+    np.testing.assert_allclose(got[:, 4], ref[:, 4], rtol=1e-12)   # mass
+    np.testing.assert_array_equal(got[:, 6], ref[:, 6])            # Newton iterations
+    assert np.all(np.abs(got[:, 7] - ref[:, 7]) <= 2)              # GMRES iterations
+    assert res.controller.divergence_count == int(z["divergences"])
+    u, v = res.final_state.to_numpy()
+    err = np.sqrt(np.sum((u - z["u"]) ** 2 + (v - z["v"]) ** 2) / np.sum(z["u"] ** 2 + z["v"] ** 2))
+    assert err <= 1e-8
+    # energy monotone and mass conserved (SPEC acceptance criteria)
+    e = got[:, 3]
+    assert np.all(np.diff(e) <= 1e-8 * np.maximum(1.0, np.abs(e[1:])))
+    assert np.max(np.abs(got[:, 4] - got[0, 4])) <= 1e-12
+
+
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+def test_simulate_config1_matches_reference(ortho):
+    _check_sim(*_run_sim("c1", ortho))
+
+
+def test_simulate_adaptive_2d_with_retries_matches_reference():
+    _check_sim(*_run_sim("c2small"))
+
+
+def test_simulate_adaptive_3d_neumann_with_retries_matches_reference():
+    _check_sim(*_run_sim("c3small"))
