@@ -242,8 +242,10 @@ __global__ void jac_prepare_kernel(GridDev g, ParamsDev P, const double2 *__rest
 
 template <int DIM, int TX, int TY>
 struct MatvecSmem {
-    static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2, R = ring_depth(DIM);
-    static constexpr size_t bytes = sizeof(double2) * R * HX * HY + 4 * sizeof(double) * R * GX * GY;
+    // w needs planes k-1..k+2 at once (lap w_v at k, lap w_u at k+1): 4-slot ring
+    static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2, R = ring_depth(DIM),
+                         RW = DIM == 3 ? 4 : 1;
+    static constexpr size_t bytes = sizeof(double2) * RW * HX * HY + 4 * sizeof(double) * R * GX * GY;
 };
 
 template <int DIM, int TX, int TY>
@@ -252,10 +254,10 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
               const double2 *__restrict__ w_g, double2 *__restrict__ yout)
 {
     using L = MatvecSmem<DIM, TX, TY>;
-    constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, NT = TX * TY;
+    constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, RW = L::RW, NT = TX * TY;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *sw = reinterpret_cast<double2 *>(smem_raw);
-    double *sdG = reinterpret_cast<double *>(sw + R * HX * HY);
+    double *sdG = reinterpret_cast<double *>(sw + RW * HX * HY);
     double *sEt = sdG + R * GX * GY;
     double *sCb = sEt + R * GX * GY;
     double *sGu = sCb + R * GX * GY;
@@ -278,8 +280,9 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
     const double hg = 0.5 * P.gamma;
     const bool per = g.periodic != 0;
 
+    auto wslot = [&](int kk) { return (DIM == 3) ? ((kk % RW) + RW) % RW : 0; };
     auto load_plane = [&](int kk) {
-        const int slot = (DIM == 3) ? ((kk % 3) + 3) % 3 : 0;
+        const int slot = wslot(kk);
         const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
         for (int i = tid; i < HX * HY; i += NT) {
             const int hx = i % HX, hy = i / HX;
@@ -291,8 +294,7 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
 
     auto compute_dg = [&](int kk) {
         const int s0 = (DIM == 3) ? ((kk % 3) + 3) % 3 : 0;
-        const int sm = (DIM == 3) ? (((kk - 1) % 3) + 3) % 3 : 0;
-        const int sp = (DIM == 3) ? (((kk + 1) % 3) + 3) % 3 : 0;
+        const int w0s = wslot(kk), wms = wslot(kk - 1), wps = wslot(kk + 1);
         const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
         for (int i = tid; i < GX * GY; i += NT) {
             const int gx = i % GX, gy = i / GX;
@@ -300,10 +302,10 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
             const int ey = wrap_coord(y0 + gy - 1, ny, g.periodic);
             const long long c = ((long long)gz * ny + ey) * nx + ex;
             const int h = (gy + 1) * HX + (gx + 1);
-            const double2 w0 = sw[s0 * HX * HY + h];
-            double lap = (sw[s0 * HX * HY + h + 1].x - 2.0 * w0.x + sw[s0 * HX * HY + h - 1].x) * ihx;
-            lap += (sw[s0 * HX * HY + h + HX].x - 2.0 * w0.x + sw[s0 * HX * HY + h - HX].x) * ihy;
-            if (DIM == 3) lap += (sw[sp * HX * HY + h].x - 2.0 * w0.x + sw[sm * HX * HY + h].x) * ihz;
+            const double2 w0 = sw[w0s * HX * HY + h];
+            double lap = (sw[w0s * HX * HY + h + 1].x - 2.0 * w0.x + sw[w0s * HX * HY + h - 1].x) * ihx;
+            lap += (sw[w0s * HX * HY + h + HX].x - 2.0 * w0.x + sw[w0s * HX * HY + h - HX].x) * ihy;
+            if (DIM == 3) lap += (sw[wps * HX * HY + h].x - 2.0 * w0.x + sw[wms * HX * HY + h].x) * ihz;
             const int o = s0 * GX * GY + i;
             sdG[o] = (-0.5 * P.alpha + __ldg(cS + c)) * w0.x + __ldg(cD + c) * w0.y - hg * lap;
             sEt[o] = 0.5 * (__ldg(cU + c) * w0.x + __ldg(cV + c) * w0.y);
@@ -362,10 +364,11 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
             if (DIM == 3) face(sp * GX * GY + gc, ihz, per || k > 0, per || k < nz - 1, sm * GX * GY + gc);
 
             const int h = (ty + 2) * HX + (tx + 2);
-            const double2 w0 = sw[s0 * HX * HY + h];
-            double lapv = (sw[s0 * HX * HY + h + 1].y - 2.0 * w0.y + sw[s0 * HX * HY + h - 1].y) * ihx;
-            lapv += (sw[s0 * HX * HY + h + HX].y - 2.0 * w0.y + sw[s0 * HX * HY + h - HX].y) * ihy;
-            if (DIM == 3) lapv += (sw[sp * HX * HY + h].y - 2.0 * w0.y + sw[sm * HX * HY + h].y) * ihz;
+            const int w0s = wslot(k), wms = wslot(k - 1), wps = wslot(k + 1);
+            const double2 w0 = sw[w0s * HX * HY + h];
+            double lapv = (sw[w0s * HX * HY + h + 1].y - 2.0 * w0.y + sw[w0s * HX * HY + h - 1].y) * ihx;
+            lapv += (sw[w0s * HX * HY + h + HX].y - 2.0 * w0.y + sw[w0s * HX * HY + h - HX].y) * ihy;
+            if (DIM == 3) lapv += (sw[wps * HX * HY + h].y - 2.0 * w0.y + sw[wms * HX * HY + h].y) * ihz;
             const long long c = ((long long)k * ny + y) * nx + x;
             const double S = __ldg(cS + c), D = __ldg(cD + c), Gv = __ldg(cGv + c);
             double2 out;

@@ -153,22 +153,76 @@ class SimulationResult:
         return self.status == COMPLETED
 
 
+class Stepper:
+    """The body of the reference's time loop (drivers.py:118-167), one
+    accepted step per ``advance()`` call: predict dt, solve with retries
+    (controller shrink + fresh factorisation on divergence), update the
+    two-level history the predictor needs.  Raises SolverStallError when the
+    controller gives up."""
+
+    def __init__(self, config: RunConfig, state: State, threads: int = 1):
+        self.config = config
+        self.grid = config.grid
+        self.state = state
+        self.controller = config.make_controller()
+        n_sub = config.solver.subdomains or threads
+        self.decomposition = partition(self.grid, n_sub, config.solver.overlap)
+        self.newton_cfg = config.make_newton_config()
+        self.precond = SchwarzPreconditioner(self.decomposition, config.solver.preconditioner,
+                                             config.solver.subdomain_solver)
+        self.t = 0.0
+        self.step = 0
+        self.dt_prev = None
+        self.x_now = state.vector
+        self.x_prev = None
+        self.since = 0
+        self.refreeze_every = max(1, config.solver.refreeze_every)
+        self.factorizations = 0
+        self.events = []
+
+    def advance(self):
+        """One accepted step; returns (dt, newton iterations, gmres iterations)."""
+        self.step += 1
+        ctl = self.controller
+        if self.step == 1 or self.x_prev is None:
+            dt = ctl.initial_dt()
+        else:
+            dt = ctl.predict_dt(self.x_now, self.x_prev, self.dt_prev)
+        if self.since >= self.refreeze_every:
+            self.precond.invalidate()
+            self.since = 0
+        newton_count = gmres_count = 0
+        while True:
+            prob = StepProblem.create(self.grid, self.config.params, self.state, dt)
+            new_state, report = newton_solve(prob, self.state, self.newton_cfg, self.precond)
+            newton_count += report.newton_iterations
+            gmres_count += report.gmres_iterations
+            self.factorizations += report.factorizations
+            if report.converged:
+                break
+            self.events.append((self.step, dt, report.reason))
+            dt = ctl.on_divergence(dt)
+            self.precond.invalidate()
+            self.since = 0
+        self.since += 1
+        ctl.note_success()
+        self.t += dt
+        self.x_prev = self.x_now
+        self.x_now = new_state.vector
+        self.dt_prev = dt
+        self.state = new_state
+        return dt, newton_count, gmres_count
+
+
 def simulate(config: RunConfig, threads: int = 1, max_steps: int | None = None, state: State | None = None,
              device=None, diagnostics_every: int = 1) -> SimulationResult:
-    """Advance from t = 0 to the horizon (drivers.py:76-184): predict dt,
-    solve (retrying with the controller's smaller dt on divergence and a
-    fresh factorisation), record energy / mass / max|v| per accepted step.
-    ``events`` lists (step, dt, reason) for every divergence."""
-    grid = config.grid
+    """Advance from t = 0 to the horizon (drivers.py:76-184) and record
+    energy / mass / max|v| per accepted step.  ``events`` lists
+    (step, dt, reason) for every divergence."""
     if state is None:
         state = build_initial_state(config, device)
-    controller = config.make_controller()
-    n_sub = config.solver.subdomains or threads
-    decomposition = partition(grid, n_sub, config.solver.overlap)
-    newton_cfg = config.make_newton_config()
-    precond = SchwarzPreconditioner(decomposition, config.solver.preconditioner, config.solver.subdomain_solver)
+    stepper = Stepper(config, state, threads)
     history = []
-    events = []
 
     def row(step, t, dt, st, newton, gm, wall):
         if diagnostics_every and (step % diagnostics_every == 0):
@@ -179,55 +233,20 @@ def simulate(config: RunConfig, threads: int = 1, max_steps: int | None = None, 
 
     row(0, 0.0, 0.0, state, 0, 0, 0.0)
     status = COMPLETED
-    factorizations = 0
-    t = 0.0
-    step = 0
-    dt_prev = None
-    x_now = state.vector
-    x_prev = None
-    since = 0
-    refreeze_every = max(1, config.solver.refreeze_every)
     horizon = config.time.horizon
-    while t < horizon * (1.0 - 1e-12):
-        if max_steps is not None and step >= max_steps:
+    while stepper.t < horizon * (1.0 - 1e-12):
+        if max_steps is not None and stepper.step >= max_steps:
             break
-        step += 1
-        if step == 1 or x_prev is None:
-            dt = controller.initial_dt()
-        else:
-            dt = controller.predict_dt(x_now, x_prev, dt_prev)
-        if since >= refreeze_every:
-            precond.invalidate()
-            since = 0
         wall0 = time.perf_counter()
-        newton_count = gmres_count = 0
         try:
-            while True:
-                prob = StepProblem.create(grid, config.params, state, dt)
-                new_state, report = newton_solve(prob, state, newton_cfg, precond)
-                newton_count += report.newton_iterations
-                gmres_count += report.gmres_iterations
-                factorizations += report.factorizations
-                if report.converged:
-                    break
-                events.append((step, dt, report.reason))
-                dt = controller.on_divergence(dt)
-                precond.invalidate()
-                since = 0
+            dt, nn, ng = stepper.advance()
         except SolverStallError:
             status = STALLED
             break
-        since += 1
-        controller.note_success()
-        wall = time.perf_counter() - wall0
-        t += dt
-        x_prev = x_now
-        x_now = new_state.vector
-        dt_prev = dt
-        state = new_state
-        row(step, t, dt, state, newton_count, gmres_count, wall)
-    return SimulationResult(status, history, state, controller, factorizations, events)
+        row(stepper.step, stepper.t, dt, stepper.state, nn, ng, time.perf_counter() - wall0)
+    return SimulationResult(status, history, stepper.state, stepper.controller, stepper.factorizations,
+                            stepper.events)
 
 
 __all__ = ["InitialSpec", "TimeSpec", "SolverSpec", "RunConfig", "initial_fields", "build_initial_state",
-           "HistoryRow", "SimulationResult", "simulate", "COMPLETED", "STALLED"]
+           "HistoryRow", "SimulationResult", "Stepper", "simulate", "COMPLETED", "STALLED"]
