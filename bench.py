@@ -1,0 +1,406 @@
+#!/usr/bin/env python
+"""Benchmark: adaptive NKS time steps of the AC/CH step on a synthetic
+256^3 periodic grid (BASELINE.json configs[3]) through the library's public
+API, plus the Jacobian-matvec and residual microbenchmarks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Prints ONE JSON line (rank 0).  `value` = accepted time steps per second over
+exactly K timed steps after W warm-up steps (inputs resident in HBM); `e2e`
+repeats K steps through the public API with the state staged from pinned host
+memory and read back every step; `roofline` is for the kernel category with
+the largest share of the timed region (algorithmic bytes / measured time,
+from CUDA events recorded around every launch on the launching stream);
+`cpu_baseline` times the CPU oracle (a port of the reference algorithm) on a
+bounded sample on this host.  Every vector is 268 MB (> 126 MB L2), so no L2
+flush is needed between iterations.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return dict(PEAKS_FALLBACK)
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=256, help="cells per axis (BASELINE configs[3]: 256)")
+    ap.add_argument("--dim", type=int, default=3)
+    ap.add_argument("--box", type=int, default=8, help="RAS box edge in cells")
+    ap.add_argument("--solver", default="ilu0")
+    ap.add_argument("--variant", default="ras-left")
+    ap.add_argument("--restart", type=int, default=30)
+    ap.add_argument("--ortho", default="cgs2", choices=["cgs2", "mgs"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--verbose", action="store_true")
+    return ap.parse_args()
+
+
+def log(args, *a):
+    if args.verbose:
+        print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# configuration
+# ---------------------------------------------------------------------------
+
+def make_config(args):
+    from paper_2007_04560_b200.drivers import InitialSpec, RunConfig, SolverSpec, TimeSpec
+    from paper_2007_04560_b200.grid import BoundaryCondition, Grid
+    from paper_2007_04560_b200.linalg import SchwarzVariant, SubdomainSolverSpec
+    from paper_2007_04560_b200.physics import Params
+    n = args.n
+    counts = (n,) * args.dim
+    grid = Grid(counts, (1.0,) * args.dim, BoundaryCondition.PERIODIC)
+    nsub = (n // args.box) ** args.dim
+    cfg = RunConfig(grid, Params(4.0, 2.0, 0.005, 0.1, 0.001),
+                    InitialSpec("random_uniform", 0.5, 0.01, 1234),
+                    TimeSpec(horizon=10.0, mode="adaptive", dt_min=1e-4, dt_max=10.0),
+                    SolverSpec(preconditioner=SchwarzVariant(args.variant), overlap=1,
+                               subdomain_solver=SubdomainSolverSpec.from_string(args.solver), subdomains=nsub,
+                               gmres_restart=args.restart, orthogonalization=args.ortho))
+    return cfg, nsub
+
+
+def workload_name(args):
+    return (f"AC/CH {args.dim}D {args.n}^{args.dim} periodic fp64, adaptive dt (eta=1e2), NKS: Newton + "
+            f"GMRES({args.restart}) + {args.variant} {args.box}^{args.dim}-cell boxes overlap 1 {args.solver}")
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle (a port of the reference algorithm) on this host
+# ---------------------------------------------------------------------------
+
+def cpu_sample(args, threads=1, budget_s=30.0):
+    """One adaptive NKS step sequence of the oracle on a reduced grid with the
+    same solver settings, reported as steps/s scaled to the full grid by the
+    cell-count ratio (optimistic for the CPU: iteration counts grow with N)."""
+    import numpy as np
+    from oracle import acch_oracle as O
+    ns = 24 if args.dim == 3 else 128
+    while ns % args.box:
+        ns += 1
+    m = O.Mesh((ns,) * args.dim, (1.0,) * args.dim, True)
+    u, v = O.initial_fields(m, 0.5, 0.01, 1234)
+    ctl = O.Controller(1e-4, 10.0, 1e2 if args.dim == 3 else 1e4)
+    t0 = time.perf_counter()
+    status, rows, x, ev = O.simulate(m, O.Coeffs(), u, v, ctl, 10.0, (ns // args.box) ** args.dim, 1,
+                                     args.variant, args.solver,
+                                     newton_cfg=O.NewtonSettings(gmres_restart=args.restart), max_steps=1,
+                                     threads=threads)
+    t = time.perf_counter() - t0
+    steps = len(rows) - 1
+    scale = (ns ** args.dim) / float(args.n ** args.dim)
+    return {"value": steps / t * scale, "unit": "time steps/s", "cores": threads, "kind": "port",
+            "sample": (f"oracle (numpy + C ILU port of acch) first adaptive step on {ns}^{args.dim} "
+                       f"(same solver settings), {t:.1f} s/step, scaled to {args.n}^{args.dim} by the cell ratio "
+                       f"{scale:.3g}")}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        r = cpu_sample(args, threads=threads)
+        if i >= args.warmup:
+            vals.append(r["value"])
+    value = sum(vals) / len(vals)
+    line = {"metric": "NKS time steps/s (fp64, 256^3 adaptive)", "value": value, "unit": "time steps/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args)},
+            "cpu_baseline": {"value": value, "unit": "time steps/s", "cores": threads, "kind": "port",
+                             "sample": r["sample"]},
+            "e2e": {"value": value, "unit": "time steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def microbench_stencils(args, stepper, peaks, reps=20):
+    """Standalone residual and Jacobian-matvec launches at the current state
+    (U' = U^n + 1e-4 N(0,1): the chords take the series branch)."""
+    import torch
+    from paper_2007_04560_b200.physics import State
+    from paper_2007_04560_b200.scheme import StepProblem, assemble_jacobian
+    grid = stepper.grid
+    n2 = 2 * grid.n_cells
+    prob = StepProblem.create(grid, stepper.config.params, stepper.state, 1e-4)
+    gen = torch.Generator(device=stepper.state.device).manual_seed(1234)
+    pert = stepper.state.vector + 1e-4 * torch.randn(n2, dtype=torch.float64, device=stepper.state.device,
+                                                     generator=gen)
+    new = State(grid, pert)
+    J = assemble_jacobian(prob, new)
+    w = torch.randn(n2, dtype=torch.float64, device=pert.device, generator=gen)
+    y = torch.empty_like(w)
+    F = torch.empty_like(w)
+    out = {}
+    for name, fn, nbytes in (("matvec", lambda: J.matvec_into(w, y), 88.0 * grid.n_cells),
+                             ("residual", lambda: prob.residual_into(pert, F), 48.0 * grid.n_cells)):
+        for _ in range(3):
+            fn()
+        ts = []
+        for _ in range(reps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn() if name == "matvec" else _residual_async(prob, pert, F)
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        ts.sort()
+        t = ts[len(ts) // 2] * 1e-3
+        gbs = nbytes / t / 1e9
+        out[name] = {"ms": t * 1e3, "gdof_s": n2 / t / 1e9, "gb_s": gbs, "frac": gbs / peaks["hbm_gbs"],
+                     "alg_bytes": nbytes}
+    return out
+
+
+def _residual_async(prob, x, F):
+    # the public residual synchronises to return ||F|| and the gap; for the
+    # launch-time microbenchmark call the kernel without the readback
+    from paper_2007_04560_b200 import _native as nat
+    import ctypes
+    nat.check(nat.lib().acch_residual(prob.ctx.bind(), nat.ptr(prob.old.x), prob.dt, nat.ptr(x), nat.ptr(F),
+                                      None, None), "residual")
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2007_04560_b200 import _native as nat
+    from paper_2007_04560_b200.drivers import Stepper, build_initial_state
+    from paper_2007_04560_b200.physics import State
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = load_peaks()
+    cfg, nsub = make_config(args)
+    grid = cfg.grid
+    t_setup = time.perf_counter()
+    state = build_initial_state(cfg, device=dev)
+    stepper = Stepper(cfg, state)
+    ctx = nat.context_for(grid, cfg.params, dev)
+    log(args, f"setup {time.perf_counter() - t_setup:.1f}s")
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for i in range(args.warmup):
+        t0 = time.perf_counter()
+        dt, nn, ng = stepper.advance()
+        torch.cuda.synchronize()
+        log(args, f"warmup step {stepper.step}: dt={dt:.4g} newton={nn} gmres={ng} "
+                  f"retries={len(stepper.events)} {time.perf_counter() - t0:.2f}s")
+
+    ctx.profile(True)
+    ctx.profile_read()
+    launches0 = nat.total_launches()
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    newton_total = gmres_total = 0
+    ev_before = len(stepper.events)
+    dts = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        dt, nn, ng = stepper.advance()
+        newton_total += nn
+        gmres_total += ng
+        dts.append(dt)
+        log(args, f"timed step {stepper.step}: dt={dt:.4g} newton={nn} gmres={ng} "
+                  f"retries={len(stepper.events)} {time.perf_counter() - t0:.2f}s")
+    e1.record()
+    barrier()
+    elapsed = e0.elapsed_time(e1) * 1e-3
+    clk = clocks.stop()
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    launches = nat.total_launches() - launches0
+    if world > 1:
+        t = torch.tensor([elapsed], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    retries = len(stepper.events) - ev_before
+
+    # e2e: the same K-step job through the public API with host-staged state
+    e2e = None
+    n2 = 2 * grid.n_cells
+    if not args.no_e2e:
+        host = torch.empty((grid.n_cells, 2), dtype=torch.float64, pin_memory=True)
+        host.copy_(stepper.state.x)
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(args.steps):
+            dev_state = State(grid, host.to(dev, non_blocking=True))
+            stepper.state = dev_state
+            stepper.x_now = dev_state.vector
+            stepper.advance()
+            host.copy_(stepper.state.x, non_blocking=True)
+            torch.cuda.synchronize()
+        barrier()
+        t_e2e = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([t_e2e], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            t_e2e = float(t.item())
+        e2e = {"value": world * args.steps / t_e2e, "unit": "time steps/s", "h2d_bytes_per_step": 8 * n2,
+               "d2h_bytes_per_step": 8 * n2}
+
+    micro = microbench_stencils(args, stepper, peaks)
+
+    total_ms = sum(v[0] for v in prof.values())
+    cats = {}
+    for k, (ms, cnt, nb) in prof.items():
+        if cnt == 0:
+            continue
+        gbs = nb / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        cats[k] = {"ms": round(ms, 3), "share": round(ms / (elapsed * 1e3), 4), "launches": int(cnt),
+                   "alg_bytes_per_launch": nb / cnt, "gb_s": round(gbs, 1),
+                   "frac": round(gbs / peaks["hbm_gbs"], 4)}
+    dom = max(cats, key=lambda k: cats[k]["ms"]) if cats else "matvec"
+    d = cats.get(dom, {})
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": d.get("gb_s"), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": d.get("frac"), "traffic": None,
+                "avg_launch_ms": (d["ms"] / d["launches"]) if d else None,
+                "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "peak_source": peaks["source"]}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_sample(args, threads=1)
+        except Exception as e:  # the baseline must not break the GPU line
+            cpu = {"error": repr(e)}
+
+    if rank == 0:
+        value = world * args.steps / elapsed
+        line = {
+            "metric": "NKS time steps/s (fp64, 256^3 adaptive); Jacobian-matvec GDOF/s; % of HBM roofline",
+            "value": value, "unit": "time steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": elapsed * 1e3 / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(args), "grid": [args.n] * args.dim, "bc": "periodic",
+                       "ic": "u0=0.5+0.01U(-1,1), v0=0.01U(-1,1), seed 1234", "subdomains": nsub,
+                       "parallelism": "1 GPU" if world == 1 else f"{world} replicas (no slab decomposition yet)",
+                       "l2": "every vector 268 MB > 126 MB L2 (no flush needed)",
+                       "steps_timed": f"accepted steps {stepper.step - args.steps - (args.steps if e2e else 0) + 1}.."},
+            "solver_stats": {"newton": newton_total, "gmres": gmres_total, "retries": retries,
+                             "dt": [round(x, 6) for x in dts]},
+            "roofline": roofline,
+            "matvec": micro["matvec"], "residual": micro["residual"],
+            "kernels": cats,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -82,7 +82,8 @@ acch_status acch_diagnostics(acch_ctx *ctx, const double *x, double *energy,
 /* residual_vector(StepProblem(old=x_old, dt), new=x) (scheme.py:343-354).
  * Writes F (2N).  Returns ACCH_ERR_INADMISSIBLE (F undefined) when the
  * admissibility gap of x is below 1e-12 (check_admissible, scheme.py:250).
- * gap and norm2 (= ||F||_2^2, deterministic) may be NULL. */
+ * gap and norm2 (= ||F||_2^2, deterministic) may be NULL; when both are NULL
+ * the call is asynchronous and skips the admissibility check (raw launch). */
 acch_status acch_residual(acch_ctx *ctx, const double *x_old, double dt, const double *x,
                           double *F, double *gap, double *norm2);
 
@@ -150,6 +151,16 @@ acch_status acch_gmres(acch_ctx *ctx, const double *coef, double dt, acch_precon
 /* Count of kernels this library has launched on ctx since creation (for the
  * bench's gpu_launches field). */
 int64_t acch_launch_count(acch_ctx *ctx);
+
+/* Optional per-category CUDA-event kernel timing (bench / profiling only).
+ * Categories, in order: residual, jacobian_prepare, matvec, precond_factor,
+ * precond_apply, precond_gather, krylov_dot, krylov_update, krylov_vector,
+ * state_reductions.  acch_profile_read synchronises, returns the milliseconds,
+ * launch counts and algorithmic DRAM bytes (the bytes each kernel must move
+ * at minimum) accumulated since the last read (n <= 10), and resets. */
+acch_status acch_profile_enable(acch_ctx *ctx, int32_t on);
+acch_status acch_profile_read(acch_ctx *ctx, double *ms, int64_t *counts, double *alg_bytes,
+                              int32_t n);
 
 #ifdef __cplusplus
 }

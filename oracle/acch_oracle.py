@@ -717,7 +717,8 @@ class SchwarzOracle:
     """ASM / left-RAS / right-RAS with ILU(k) or LU subdomain solves
     (linalg.py:320-396)."""
 
-    def __init__(self, boxes: Boxes, variant="ras-left", solver="ilu0"):
+    def __init__(self, boxes: Boxes, variant="ras-left", solver="ilu0", threads=1):
+        self.threads = max(1, int(threads))
         self.boxes = boxes
         self.variant = variant
         self.solver = solver
@@ -734,26 +735,37 @@ class SchwarzOracle:
         if reuse and self.factors is not None:
             return False
         ip, ix, bv = blocks_csr
-        facs = []
-        for cells in self.boxes.extended:
+
+        def one(cells):
             sip, six, sbv = restrict_blocks(ip, ix, bv, cells)
             if self.solver == "lu":
-                facs.append(LuOracle(sip, six, sbv))
-            else:
-                facs.append(IluOracle(sip, six, sbv, int(self.solver[3:]), cells))
-        self.factors = facs
+                return LuOracle(sip, six, sbv)
+            return IluOracle(sip, six, sbv, int(self.solver[3:]), cells)
+        self.factors = self._map(one, self.boxes.extended)
         self.factorization_count += 1
         return True
 
+    def _map(self, fn, items):
+        """Ordered map; threads only change wall time (parallel.py:12-40)."""
+        if self.threads == 1:
+            return [fn(i) for i in items]
+        from concurrent.futures import ThreadPoolExecutor
+        if not hasattr(self, "_pool"):
+            self._pool = ThreadPoolExecutor(self.threads)
+        return list(self._pool.map(fn, items))
+
     def apply(self, r):
         out = np.zeros_like(r)
-        for k, f in enumerate(self.factors):
+
+        def solve(k):
             if self.variant == "ras-right":
                 rk = np.zeros(len(self.ext_dofs[k]))
                 rk[self.own_pos[k]] = r[self.own_dofs[k]]
             else:
                 rk = r[self.ext_dofs[k]]
-            yk = f.solve(rk)
+            return self.factors[k].solve(rk)
+        parts = self._map(solve, range(len(self.factors)))
+        for k, yk in enumerate(parts):
             if self.variant == "ras-left":
                 out[self.own_dofs[k]] = yk[self.own_pos[k]]
             else:
@@ -1009,12 +1021,12 @@ def diagnostics(mesh, co, u, v):
 
 def simulate(mesh, co, u0, v0, controller: Controller, horizon, nsub, overlap=1,
              variant="ras-left", solver="ilu0", newton_cfg=NewtonSettings(),
-             max_steps=None, refreeze_every=1):
+             max_steps=None, refreeze_every=1, threads=1):
     """Accepted-step loop with retries on divergence (drivers.py:76-184).
     Returns (status, rows, final x, events) where events lists
     (step, dt_tried, reason) for every divergence."""
     boxes = decompose(mesh, nsub, overlap)
-    pre = SchwarzOracle(boxes, variant, solver)
+    pre = SchwarzOracle(boxes, variant, solver, threads)
     u, v = u0.copy(), v0.copy()
     rows = [Row(0, 0.0, 0.0, *diagnostics(mesh, co, u, v), 0, 0)]
     events = []

@@ -74,7 +74,12 @@ SIGNATURES = {
     "acch_precond_info": (_I32, [_P, _PI64, _PI64, _PI64]),
     "acch_gmres": (_I32, [_P, _P, _D, _P, _P, _P, _D, _D, _I32, _I32, _I32, _PI32, _PI32, _PD]),
     "acch_launch_count": (_I64, [_P]),
+    "acch_profile_enable": (_I32, [_P, _I32]),
+    "acch_profile_read": (_I32, [_P, _PD, _PI64, _PD, _I32]),
 }
+
+PROFILE_CATEGORIES = ("residual", "jacobian_prepare", "matvec", "precond_factor", "precond_apply",
+                      "precond_gather", "krylov_dot", "krylov_update", "krylov_vector", "state_reductions")
 
 _lib = None
 _lock = threading.Lock()
@@ -179,6 +184,19 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self._lib.acch_launch_count(self.handle))
+
+    def profile(self, on: bool = True):
+        check(self._lib.acch_profile_enable(self.handle, int(bool(on))), "profile_enable")
+
+    def profile_read(self) -> dict:
+        """{category: (milliseconds, launches, algorithmic bytes)} since the last read."""
+        n = len(PROFILE_CATEGORIES)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        nb = (ctypes.c_double * n)()
+        self.bind()
+        check(self._lib.acch_profile_read(self.handle, ms, cnt, nb, n), "profile_read")
+        return {k: (ms[i], cnt[i], nb[i]) for i, k in enumerate(PROFILE_CATEGORIES)}
 
     def __del__(self):
         h = getattr(self, "handle", None)

@@ -39,6 +39,23 @@ enum { CO_S = 0, CO_D, CO_CBAR, CO_GU, CO_CU, CO_CV, CO_GV, CO_NFIELDS };
 // Host-side context
 // ---------------------------------------------------------------------------
 
+// kernel categories for the optional CUDA-event profile (acch_profile_*)
+enum ProfCat {
+    PC_RESIDUAL = 0, PC_JPREP, PC_MATVEC, PC_FACTOR, PC_APPLY, PC_GATHER, PC_KDOT, PC_KUPDATE, PC_KVEC,
+    PC_REDUCE, PC_COUNT
+};
+
+struct ProfState {
+    bool on = false;
+    std::vector<cudaEvent_t> pool;
+    std::vector<int> cat;
+    std::vector<cudaEvent_t> ev0, ev1;
+    std::vector<double> nbytes;
+    double ms[PC_COUNT] = {0};
+    long long cnt[PC_COUNT] = {0};
+    double bytes[PC_COUNT] = {0};
+};
+
 struct acch_ctx {
     GridDev g;
     ParamsDev p;
@@ -56,6 +73,18 @@ struct acch_ctx {
     double *d_work = nullptr;         // 3 * 2N: z (precond out), r, t
     double *d_h = nullptr;            // small device array for Hessenberg column
     long long launches = 0;
+    ProfState prof;
+};
+
+// Records a CUDA event pair around the launches in its scope when profiling is on.
+struct ProfScope {
+    acch_ctx *ctx;
+    int cat;
+    double bytes;
+    cudaEvent_t e1 = nullptr;
+    // bytes: algorithmic DRAM bytes the launches in scope must move
+    ProfScope(acch_ctx *c, int category, double alg_bytes);
+    ~ProfScope();
 };
 
 constexpr int kRedBlocks = 296;   // 2 x 148 SMs; fixed -> deterministic reductions

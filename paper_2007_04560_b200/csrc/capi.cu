@@ -16,6 +16,37 @@ acch_status acch_cuda_fail(cudaError_t e, const char *where)
     return ACCH_ERR_CUDA;
 }
 
+static cudaEvent_t prof_event(acch_ctx *ctx)
+{
+    auto &p = ctx->prof;
+    if (!p.pool.empty()) {
+        cudaEvent_t e = p.pool.back();
+        p.pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+ProfScope::ProfScope(acch_ctx *c, int category, double alg_bytes) : ctx(c), cat(category), bytes(alg_bytes)
+{
+    if (!ctx->prof.on) return;
+    cudaEvent_t e0 = prof_event(ctx);
+    e1 = prof_event(ctx);
+    cudaEventRecord(e0, ctx->stream);
+    ctx->prof.ev0.push_back(e0);
+}
+
+ProfScope::~ProfScope()
+{
+    if (!e1) return;
+    cudaEventRecord(e1, ctx->stream);
+    ctx->prof.ev1.push_back(e1);
+    ctx->prof.cat.push_back(cat);
+    ctx->prof.nbytes.push_back(bytes);
+}
+
 acch_status acch_fetch_results(acch_ctx *ctx, int count)
 {
     ACCH_CUDA(cudaMemcpyAsync(ctx->h_result, ctx->d_result, sizeof(double) * count, cudaMemcpyDeviceToHost, ctx->stream));
@@ -159,6 +190,42 @@ acch_status acch_set_stream(acch_ctx *ctx, void *cuda_stream)
 
 int64_t acch_launch_count(acch_ctx *ctx) { return ctx ? ctx->launches : 0; }
 
+acch_status acch_profile_enable(acch_ctx *ctx, int32_t on)
+{
+    CHECK_CTX(ctx);
+    ctx->prof.on = on != 0;
+    return ACCH_OK;
+}
+
+acch_status acch_profile_read(acch_ctx *ctx, double *ms, int64_t *counts, double *bytes, int32_t n)
+{
+    CHECK_CTX(ctx);
+    ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
+    auto &p = ctx->prof;
+    for (size_t i = 0; i < p.cat.size(); ++i) {
+        float t = 0.f;
+        cudaEventElapsedTime(&t, p.ev0[i], p.ev1[i]);
+        p.ms[p.cat[i]] += t;
+        p.cnt[p.cat[i]] += 1;
+        p.bytes[p.cat[i]] += p.nbytes[i];
+        p.pool.push_back(p.ev0[i]);
+        p.pool.push_back(p.ev1[i]);
+    }
+    p.cat.clear();
+    p.nbytes.clear();
+    p.ev0.clear();
+    p.ev1.clear();
+    for (int i = 0; i < n && i < PC_COUNT; ++i) {
+        if (ms) ms[i] = p.ms[i];
+        if (counts) counts[i] = p.cnt[i];
+        if (bytes) bytes[i] = p.bytes[i];
+        p.bytes[i] = 0.0;
+        p.ms[i] = 0.0;
+        p.cnt[i] = 0;
+    }
+    return ACCH_OK;
+}
+
 int32_t acch_stencil_offsets(int32_t dim, int32_t *offsets_xyz)
 {
     int off[25][3];
@@ -209,6 +276,7 @@ acch_status acch_residual(acch_ctx *ctx, const double *x_old, double dt, const d
         return ACCH_ERR_INVALID_ARG;
     }
     TRY(launch_residual(ctx, x_old, dt, x, F));
+    if (!gap && !norm2) return ACCH_OK;   // asynchronous form: no readback, no admissibility check
     TRY(acch_fetch_results(ctx, 2));
     const double gp = isnan(ctx->h_result[1]) ? -INFINITY : ctx->h_result[1];
     if (gap) *gap = gp;

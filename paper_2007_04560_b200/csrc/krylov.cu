@@ -139,6 +139,7 @@ int rgrid(long long n)
 static acch_status mdot_to(acch_ctx *ctx, const double *V, long long ld, int m, const double *w, long long n,
                            double *out)
 {
+    ProfScope prof_scope(ctx, PC_KDOT, 8.0 * (m + 1) * n);
     const int G = rgrid(n);
 #define MDOT_CASE(NS)                                                                                            \
     mdot_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, w, n, ctx->d_partials, ctx->d_counter, out); \
@@ -157,6 +158,7 @@ static acch_status mdot_to(acch_ctx *ctx, const double *V, long long ld, int m, 
 static acch_status mupdate_to(acch_ctx *ctx, const double *V, long long ld, int m, const double *h, double *w,
                               long long n, double *out)
 {
+    ProfScope prof_scope(ctx, PC_KUPDATE, 8.0 * (m + 2) * n);
     const int G = rgrid(n);
 #define MUP_CASE(NS) \
     mupdate_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter, out);
@@ -172,6 +174,7 @@ static acch_status mupdate_to(acch_ctx *ctx, const double *V, long long ld, int 
 
 static acch_status combine(acch_ctx *ctx, const double *V, long long ld, int m, const double *y, double *t, long long n)
 {
+    ProfScope prof_scope(ctx, PC_KVEC, 8.0 * (m + 1) * n);
     const int G = vgrid(n);
     if (m <= 8) combine_kernel<8><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, y, t, n);
     else if (m <= 16) combine_kernel<16><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, y, t, n);
@@ -183,6 +186,7 @@ static acch_status combine(acch_ctx *ctx, const double *V, long long ld, int m, 
 
 acch_status launch_dot(acch_ctx *ctx, const double *a, const double *b, long long n)
 {
+    ProfScope prof_scope(ctx, PC_KDOT, 16.0 * n);
     dot_kernel<<<rgrid(n), kRedThreads, 0, ctx->stream>>>(a, b, n, ctx->d_partials, ctx->d_counter, ctx->d_result);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
@@ -190,6 +194,7 @@ acch_status launch_dot(acch_ctx *ctx, const double *a, const double *b, long lon
 
 static acch_status dot_to(acch_ctx *ctx, const double *a, const double *b, long long n, double *out)
 {
+    ProfScope prof_scope(ctx, PC_KDOT, 16.0 * n);
     dot_kernel<<<rgrid(n), kRedThreads, 0, ctx->stream>>>(a, b, n, ctx->d_partials, ctx->d_counter, out);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
@@ -197,6 +202,7 @@ static acch_status dot_to(acch_ctx *ctx, const double *a, const double *b, long 
 
 acch_status launch_axpby(acch_ctx *ctx, double a, const double *x, double b, double *y, long long n)
 {
+    ProfScope prof_scope(ctx, PC_KVEC, 24.0 * n);
     axpby_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(a, x, b, y, n);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
@@ -204,6 +210,7 @@ acch_status launch_axpby(acch_ctx *ctx, double a, const double *x, double b, dou
 
 static acch_status scale_by(acch_ctx *ctx, double a, const double *x, double *y, long long n)
 {
+    ProfScope prof_scope(ctx, PC_KVEC, 16.0 * n);
     scale_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(a, x, y, n);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
@@ -309,8 +316,11 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                 TRY(dot_to(ctx, w, w, n, dh + 40));
                 for (int i = 0; i <= j; ++i) {
                     TRY(dot_to(ctx, col(i), w, n, dh + i));
-                    axpy_dev_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(dh + i, col(i), w, n);
-                    ACCH_LAUNCHED(ctx);
+                    {
+                        ProfScope ps(ctx, PC_KUPDATE, 24.0 * n);
+                        axpy_dev_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(dh + i, col(i), w, n);
+                        ACCH_LAUNCHED(ctx);
+                    }
                 }
                 TRY(dot_to(ctx, w, w, n, dh + 41));
                 TRY(fetch(ctx, tmp, dh, 42));
@@ -320,8 +330,11 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                 if (norm_after < 0.5 * norm_before) {
                     for (int i = 0; i <= j; ++i) {
                         TRY(dot_to(ctx, col(i), w, n, dh + i));
-                        axpy_dev_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(dh + i, col(i), w, n);
-                        ACCH_LAUNCHED(ctx);
+                        {
+                            ProfScope ps(ctx, PC_KUPDATE, 24.0 * n);
+                            axpy_dev_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(dh + i, col(i), w, n);
+                            ACCH_LAUNCHED(ctx);
+                        }
                     }
                     TRY(dot_to(ctx, w, w, n, dh + 41));
                     TRY(fetch(ctx, tmp, dh, 42));

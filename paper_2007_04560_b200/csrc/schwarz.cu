@@ -670,6 +670,7 @@ extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef,
     if (reuse && pc->have_factors) return ACCH_OK;
     acch_ctx *ctx = pc->ctx;
     ACCH_CUDA(cudaMemsetAsync(pc->d_bad, 0x7f, sizeof(int) * pc->nsub, ctx->stream));
+    ProfScope prof_scope(ctx, PC_FACTOR, 32.0 * pc->total_blocks + 56.0 * pc->total_ext);
     if (pc->dim == 3)
         factor_kernel<3><<<(unsigned)pc->nsub, kFactorThreads, 0, ctx->stream>>>(
             ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals,
@@ -718,6 +719,7 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     acch_ctx *ctx = pc->ctx;
     const unsigned nb = (unsigned)pc->nsub;
     const size_t sm = pc->apply_smem;
+    ProfScope prof_scope(ctx, PC_APPLY, 32.0 * pc->total_blocks + 16.0 * pc->total_ext + 16.0 * ctx->g.n);
 #define APPLY(V) \
     apply_kernel<V><<<nb, kApplyThreads, sm, ctx->stream>>>(ctx->g, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, \
         pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->use_smem)

@@ -553,6 +553,7 @@ int stencil_offsets(int dim, int (*off)[3])
 
 acch_status launch_residual(acch_ctx *ctx, const double *x_old, double dt, const double *x, double *F)
 {
+    ProfScope prof_scope(ctx, PC_RESIDUAL, 48.0 * ctx->g.n);
     const GridDev &g = ctx->g;
     const dim3 block(RTX, RTY);
     if (g.dim == 3) {
@@ -580,6 +581,7 @@ acch_status launch_residual(acch_ctx *ctx, const double *x_old, double dt, const
 
 acch_status launch_jacobian_prepare(acch_ctx *ctx, const double *x_old, double dt, const double *x, double *coef)
 {
+    ProfScope prof_scope(ctx, PC_JPREP, 88.0 * ctx->g.n);
     (void)dt;
     const long long n = ctx->g.n;
     jac_prepare_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->g, ctx->p, (const double2 *)x_old,
@@ -590,6 +592,7 @@ acch_status launch_jacobian_prepare(acch_ctx *ctx, const double *x_old, double d
 
 acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
+    ProfScope prof_scope(ctx, PC_MATVEC, 88.0 * ctx->g.n);
     const GridDev &g = ctx->g;
     const dim3 block(MTX, MTY);
     if (g.dim == 3) {
@@ -615,6 +618,7 @@ acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const do
 
 acch_status launch_jacobian_blocks(acch_ctx *ctx, const double *coef, double dt, double *out)
 {
+    ProfScope prof_scope(ctx, PC_JPREP, (56.0 + 32.0 * stencil_offsets(ctx->g.dim, nullptr)) * ctx->g.n);
     const int noff = stencil_offsets(ctx->g.dim, nullptr);
     const long long n = ctx->g.n;
     if (ctx->g.dim == 3)
@@ -628,6 +632,7 @@ acch_status launch_jacobian_blocks(acch_ctx *ctx, const double *coef, double dt,
 acch_status launch_chord(acch_ctx *ctx, const double *a, const double *b, long long n, int force_exact, double *val,
                          double *der)
 {
+    ProfScope prof_scope(ctx, PC_REDUCE, 24.0 * n);
     if (n <= 0) return ACCH_OK;
     chord_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(ctx->p, a, b, n, force_exact, val, der);
     ACCH_LAUNCHED(ctx);
@@ -636,6 +641,7 @@ acch_status launch_chord(acch_ctx *ctx, const double *a, const double *b, long l
 
 acch_status launch_gap(acch_ctx *ctx, const double *x)
 {
+    ProfScope prof_scope(ctx, PC_REDUCE, 16.0 * ctx->g.n);
     const long long n = ctx->g.n;
     gap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, ctx->d_partials, ctx->d_counter,
                                                             ctx->d_result);
@@ -645,6 +651,7 @@ acch_status launch_gap(acch_ctx *ctx, const double *x)
 
 acch_status launch_diagnostics(acch_ctx *ctx, const double *x)
 {
+    ProfScope prof_scope(ctx, PC_REDUCE, 16.0 * ctx->g.n);
     diagnostics_kernel<<<red_grid(ctx->g.n), kRedThreads, 0, ctx->stream>>>(ctx->g, ctx->p, (const double2 *)x,
                                                                            ctx->d_partials, ctx->d_counter,
                                                                            ctx->d_result);
@@ -654,6 +661,7 @@ acch_status launch_diagnostics(acch_ctx *ctx, const double *x)
 
 acch_status launch_trial(acch_ctx *ctx, const double *x, const double *s, double lam, double *y)
 {
+    ProfScope prof_scope(ctx, PC_REDUCE, 48.0 * ctx->g.n);
     const long long n = ctx->g.n;
     trial_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, (const double2 *)s, lam,
                                                               (double2 *)y, ctx->d_partials, ctx->d_counter,
@@ -664,6 +672,7 @@ acch_status launch_trial(acch_ctx *ctx, const double *x, const double *s, double
 
 acch_status launch_feasible_cap(acch_ctx *ctx, const double *x, const double *s, double margin)
 {
+    ProfScope prof_scope(ctx, PC_REDUCE, 32.0 * ctx->g.n);
     const long long n = ctx->g.n;
     feasible_cap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, (const double2 *)s, margin,
                                                                      ctx->d_partials, ctx->d_counter, ctx->d_result);
@@ -673,6 +682,7 @@ acch_status launch_feasible_cap(acch_ctx *ctx, const double *x, const double *s,
 
 acch_status launch_rms_diff(acch_ctx *ctx, const double *a, const double *b, long long n)
 {
+    ProfScope prof_scope(ctx, PC_REDUCE, 16.0 * n);
     rms_diff_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, a, b, ctx->d_partials, ctx->d_counter,
                                                                  ctx->d_result);
     ACCH_LAUNCHED(ctx);
