@@ -21,35 +21,34 @@
 
 namespace {
 
+// All vector kernels stream double2 (16 B) per thread; n (= 2N) is even.
+constexpr int kVecBlocks = 148 * 8;   // fixed grid: 8 CTAs of 256 threads per SM, deterministic reductions
+
 template <int NS>
 __global__ void __launch_bounds__(kRedThreads)
 mdot_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ w, long long n,
             double *partials, unsigned int *counter, double *result)
 {
+    // result[s] = <V_s, w> (s < m), result[NS-1] = <w, w>
     double acc[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const double wi = w[i];
+    const long long n2 = n >> 1;
+    const double2 *__restrict__ w2 = reinterpret_cast<const double2 *>(w);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        const double2 wi = w2[i];
 #pragma unroll
         for (int s = 0; s < NS - 1; ++s)
-            if (s < m) acc[s] += V[s * ld + i] * wi;
-        acc[NS - 1] += wi * wi;
+            if (s < m) {
+                const double2 v = reinterpret_cast<const double2 *>(V + s * ld)[i];
+                acc[s] += v.x * wi.x + v.y * wi.y;
+            }
+        acc[NS - 1] += wi.x * wi.x + wi.y * wi.y;
     }
     int ops[NS];
 #pragma unroll
     for (int s = 0; s < NS; ++s) ops[s] = RED_SUM;
-    double v[NS];
-#pragma unroll
-    for (int s = 0; s < NS; ++s) v[s] = acc[s];
-    // slot NS-1 holds ||w||^2; move_slot_kernel relocates it to slot m
-    reduce_finish<NS>(v, ops, partials, counter, result);
-}
-
-// after mdot: result[NS-1] holds <w,w>; fix-up kernel moves it to result[m]
-__global__ void move_slot_kernel(double *result, int from, int to)
-{
-    if (threadIdx.x == 0 && blockIdx.x == 0) result[to] = result[from];
+    reduce_finish<NS>(acc, ops, partials, counter, result);
 }
 
 template <int NS>
@@ -61,13 +60,19 @@ mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *
     if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[threadIdx.x] : 0.0;
     __syncthreads();
     double acc = 0.0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        double wi = w[i];
+    const long long n2 = n >> 1;
+    double2 *__restrict__ w2 = reinterpret_cast<double2 *>(w);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        double2 wi = w2[i];
 #pragma unroll
         for (int s = 0; s < NS; ++s)
-            if (s < m) wi -= sh[s] * V[s * ld + i];
-        w[i] = wi;
-        acc += wi * wi;
+            if (s < m) {
+                const double2 v = reinterpret_cast<const double2 *>(V + s * ld)[i];
+                wi.x -= sh[s] * v.x;
+                wi.y -= sh[s] * v.y;
+            }
+        w2[i] = wi;
+        acc += wi.x * wi.x + wi.y * wi.y;
     }
     double v[1] = {acc};
     const int ops[1] = {RED_SUM};
@@ -81,12 +86,17 @@ __global__ void combine_kernel(const double *__restrict__ V, long long ld, int m
     __shared__ double sy[NS];
     if (threadIdx.x < NS) sy[threadIdx.x] = threadIdx.x < m ? y[threadIdx.x] : 0.0;
     __syncthreads();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        double acc = 0.0;
+    const long long n2 = n >> 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
         for (int s = 0; s < NS; ++s)
-            if (s < m) acc += sy[s] * V[s * ld + i];
-        t[i] = acc;
+            if (s < m) {
+                const double2 v = reinterpret_cast<const double2 *>(V + s * ld)[i];
+                acc.x += sy[s] * v.x;
+                acc.y += sy[s] * v.y;
+            }
+        reinterpret_cast<double2 *>(t)[i] = acc;
     }
 }
 
@@ -94,8 +104,12 @@ __global__ void dot_kernel(const double *__restrict__ a, const double *__restric
                            unsigned int *counter, double *result)
 {
     double acc = 0.0;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-        acc += a[i] * b[i];
+    const long long n2 = n >> 1;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        const double2 x = reinterpret_cast<const double2 *>(a)[i], y = reinterpret_cast<const double2 *>(b)[i];
+        acc += x.x * y.x + x.y * y.y;
+    }
+    if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) acc += a[n - 1] * b[n - 1];
     double v[1] = {acc};
     const int ops[1] = {RED_SUM};
     reduce_finish<1>(v, ops, partials, counter, result);
@@ -124,27 +138,22 @@ __global__ void scale_kernel(double a, const double *__restrict__ x, double *__r
 
 int vgrid(long long n)
 {
-    long long b = (n + kRedThreads * 4 - 1) / (kRedThreads * 4);
-    return (int)std::max<long long>(1, std::min<long long>(b, 4 * 148));
+    long long b = (n + kRedThreads * 2 - 1) / (kRedThreads * 2);
+    return (int)std::max<long long>(1, std::min<long long>(b, kVecBlocks));
 }
-int rgrid(long long n)
-{
-    long long b = (n + kRedThreads * 4 - 1) / (kRedThreads * 4);
-    return (int)std::max<long long>(1, std::min<long long>(b, kRedBlocks));
-}
+int rgrid(long long n) { return vgrid(n); }
 
 }  // namespace
 
-// results[0..m-1] = <V_q, w>, results[m] = <w, w>, written to `out` (device)
+// out[0..m-1] = <V_q, w>, out[*ns - 1] = <w, w> (device)
 static acch_status mdot_to(acch_ctx *ctx, const double *V, long long ld, int m, const double *w, long long n,
-                           double *out)
+                           double *out, int *ns)
 {
     ProfScope prof_scope(ctx, PC_KDOT, 8.0 * (m + 1) * n);
     const int G = rgrid(n);
 #define MDOT_CASE(NS)                                                                                            \
     mdot_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, w, n, ctx->d_partials, ctx->d_counter, out); \
-    move_slot_kernel<<<1, 32, 0, ctx->stream>>>(out, NS - 1, m);                                               \
-    ctx->launches += 1;
+    *ns = NS;
     if (m + 1 <= 4) { MDOT_CASE(4) }
     else if (m + 1 <= 8) { MDOT_CASE(8) }
     else if (m + 1 <= 16) { MDOT_CASE(16) }
@@ -299,14 +308,15 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
             TRY(launch_matvec(ctx, coef, dt, zj, w));
             double norm_before, norm_after;
             if (ortho == 1) {
-                TRY(mdot_to(ctx, V, n, j + 1, w, n, dh));
+                int ns = 0;
+                TRY(mdot_to(ctx, V, n, j + 1, w, n, dh, &ns));
                 TRY(mupdate_to(ctx, V, n, j + 1, dh, w, n, dh + 40));
                 TRY(fetch(ctx, tmp, dh, 41));
                 for (int i = 0; i <= j; ++i) h(i, j) = tmp[i];
-                norm_before = sqrt(tmp[j + 1]);
+                norm_before = sqrt(tmp[ns - 1]);
                 norm_after = sqrt(tmp[40]);
                 if (norm_after < 0.5 * norm_before) {
-                    TRY(mdot_to(ctx, V, n, j + 1, w, n, dh));
+                    TRY(mdot_to(ctx, V, n, j + 1, w, n, dh, &ns));
                     TRY(mupdate_to(ctx, V, n, j + 1, dh, w, n, dh + 40));
                     TRY(fetch(ctx, tmp, dh, 41));
                     for (int i = 0; i <= j; ++i) h(i, j) += tmp[i];

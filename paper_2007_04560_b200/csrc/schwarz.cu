@@ -24,6 +24,8 @@
 //     per-subdomain buffer that gather_kernel sums per cell in subdomain
 //     order -- the reference's fixed combination order, linalg.py:389-396).
 #include <limits.h>
+#include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -42,24 +44,35 @@ constexpr int kFactorThreads = 128;
 constexpr int kApplyThreads = 128;
 
 struct ClassDev {
-    int nloc, nnzb, nlev, nlevb;
+    int nloc, nnzb, nlev, nlevb, ell_total, max_fwidth, max_bwidth;
     int len[3];
     const int *rel[3];
     const int *rowptr, *col, *diag;
-    const int *jmap;        // nloc * noff
-    const int *upd_ptr;     // nnzb + 1
-    const int2 *upd;        // (src, dst)
+    const int *pos;         // CSR entry -> slot in the per-subdomain level-major value array
+    const int *jmap;        // nloc * noff -> slot (or -1)
+    const int *upd_ptr;     // nnzb + 1 (indexed by CSR entry)
+    const int2 *upd;        // (src slot, dst slot)
     const int *lev_ptr, *lev_rows, *levb_ptr, *levb_rows;
+    // level-major ("ELL per level") solve layout: slot(level, t, q) = base[level] + t * m + q
+    const int *f_base, *f_len, *b_base, *b_len;   // f_len/b_len indexed like lev_rows/levb_rows
+    const int *ecol;        // local column of every slot (-1 = padding)
     const unsigned char *owned;
+    const int *f_jptr, *f_joff, *b_jptr, *b_joff;   // per-level jagged-diagonal offsets
+    // compact copies for staging into shared memory by the warp solver
+    const unsigned short *f_rows16, *b_rows16;
+    const unsigned short *f_len8, *b_len8;   // row lengths (slots) in level order
 };
 
 struct ClassHost {
     std::array<std::vector<int>, 3> rel;
     int own_len[3];
-    std::vector<int> rowptr, col, diag, jmap, upd_ptr, lev_ptr, lev_rows, levb_ptr, levb_rows;
+    std::vector<int> rowptr, col, diag, pos, jmap, upd_ptr, lev_ptr, lev_rows, levb_ptr, levb_rows;
+    std::vector<int> f_base, f_len, b_base, b_len, ecol, f_jptr, f_joff, b_jptr, b_joff;
+    std::vector<unsigned short> f_rows16, b_rows16;
+    std::vector<unsigned short> f_len8, b_len8;
     std::vector<int2> upd;
     std::vector<unsigned char> owned;
-    int nloc = 0, nnzb = 0;
+    int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
     void *dev_mem = nullptr;
     ClassDev dev;
 };
@@ -96,7 +109,7 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
     const int4 o = sub_origin[s];
     double4 *A = vals + sub_off[s];
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int t = tid; t < C.nnzb; t += nt) A[t] = make_double4(0.0, 0.0, 0.0, 0.0);
+    for (int t = tid; t < C.ell_total; t += nt) A[t] = make_double4(0.0, 0.0, 0.0, 0.0);
     __syncthreads();
     for (int l = tid; l < C.nloc; l += nt) {
         int gx, gy, gz;
@@ -115,15 +128,17 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
         }
     }
     __syncthreads();
+    // block IKJ elimination, level by level (rows of a level are independent)
     for (int lev = 0; lev < C.nlev; ++lev) {
         for (int q = C.lev_ptr[lev] + tid; q < C.lev_ptr[lev + 1]; q += nt) {
             const int i = C.lev_rows[q];
             const int d = C.diag[i];
             for (int t = C.rowptr[i]; t < d; ++t) {
                 const int k = C.col[t];
-                const double4 ak = A[t], dk = A[C.diag[k]];
+                const int pt = C.pos[t];
+                const double4 ak = A[pt], dk = A[C.pos[C.diag[k]]];
                 const Blk L = mul({ak.x, ak.y, ak.z, ak.w}, {dk.x, dk.y, dk.z, dk.w});
-                A[t] = make_double4(L.a, L.b, L.c, L.d);
+                A[pt] = make_double4(L.a, L.b, L.c, L.d);
                 for (int u = C.upd_ptr[t]; u < C.upd_ptr[t + 1]; ++u) {
                     const int2 sd = C.upd[u];
                     const double4 us = A[sd.x];
@@ -137,7 +152,8 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
                 }
             }
             // diagonal block: scalar pivots as the reference's factor_inplace sees them
-            const double4 D = A[d];
+            const int pd = C.pos[d];
+            const double4 D = A[pd];
             const double p0 = D.x;
             const double p1 = D.w - (D.z / D.x) * D.y;
             int bad = -1;
@@ -145,74 +161,345 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
             else if (fabs(p1) < 1e-300) bad = 2 * i + 1;
             if (bad >= 0) atomicMin(bad_row + s, bad);
             const double det = D.x * D.w - D.y * D.z;
-            A[d] = make_double4(D.w / det, -D.y / det, -D.z / det, D.x / det);
+            A[pd] = make_double4(D.w / det, -D.y / det, -D.z / det, D.x / det);
         }
         __syncthreads();
     }
 }
 
-template <int VARIANT>   // 0 asm, 1 ras-left, 2 ras-right
-__global__ void __launch_bounds__(kApplyThreads)
+// Level-scheduled forward (unit-L) and backward (U with inverted diagonal)
+// sweeps of one subdomain.  TPS threads cooperate on a subdomain: 32 (one
+// warp, __syncwarp between levels) for boxes whose levels are narrow, or the
+// whole CTA.  Factor slots are level-major, so the q-th row of a level reads
+// slot base + t*m + q: consecutive lanes touch consecutive 32-byte blocks.
+template <int TPS>
+__device__ __forceinline__ void level_sync()
+{
+    if (TPS == 32) __syncwarp();
+    else __syncthreads();
+}
+
+// Bulk L2 prefetch (TMA engine, no registers or shared memory): the warp
+// solver asks for the factor slots of the level D ahead while it works on the
+// current one, so its own loads hit L2 instead of waiting on HBM.
+__device__ __forceinline__ void prefetch_l2(const void *p, unsigned bytes)
+{
+    if (bytes >= 16) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes & ~15u) : "memory");
+}
+
+// one 256-bit read-only load (LDG.256, sm_100) per 2x2 factor block
+__device__ __forceinline__ double4 ldg4(const double4 *p)
+{
+    double4 v;
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+__device__ __forceinline__ void blk_sub(double2 &acc, const double4 &a, const double2 &y)
+{
+    acc.x -= a.x * y.x + a.y * y.y;
+    acc.y -= a.z * y.x + a.w * y.y;
+}
+
+template <int VARIANT, int TPS, int MAXW = 12>   // VARIANT: 0 asm, 1 ras-left, 2 ras-right
+__global__ void __launch_bounds__(128, 3)
 apply_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
              const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
              const long long *__restrict__ sub_ext_off, const double4 *__restrict__ vals,
-             const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out, int use_smem)
+             const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out, int use_smem,
+             int max_nloc, long long nsub)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int s = blockIdx.x;
+    const int group = threadIdx.x / TPS;               // subdomain slot within the CTA
+    const int lane = threadIdx.x % TPS;
+    const long long s = (long long)blockIdx.x * (blockDim.x / TPS) + group;
+    if (s >= nsub) return;                             // whole group exits together
     const ClassDev C = classes[sub_class[s]];
     const int4 o = sub_origin[s];
-    const double4 *A = vals + sub_off[s];
-    double2 *y = use_smem ? reinterpret_cast<double2 *>(smem_raw) : ext_out + sub_ext_off[s];
-    const int tid = threadIdx.x, nt = blockDim.x;
+    const double4 *__restrict__ A = vals + sub_off[s];
+    double2 *y = use_smem ? reinterpret_cast<double2 *>(smem_raw) + (size_t)group * max_nloc
+                          : ext_out + sub_ext_off[s];
     const long long nx = g.nx, ny = g.ny;
-    for (int l = tid; l < C.nloc; l += nt) {
+    for (int l = lane; l < C.nloc; l += TPS) {
         int gx, gy, gz;
         local_to_global(g, C, o, l, gx, gy, gz);
         double2 v = r[(gz * ny + gy) * nx + gx];
         if (VARIANT == 2 && !C.owned[l]) v = make_double2(0.0, 0.0);
         y[l] = v;
     }
-    __syncthreads();
+    level_sync<TPS>();
+    // Each row's slots are fetched up front (MAXW loads in flight per lane), so a
+    // level costs one global round trip; the y reads are shared-memory hits.
     for (int lev = 0; lev < C.nlev; ++lev) {
-        for (int q = C.lev_ptr[lev] + tid; q < C.lev_ptr[lev + 1]; q += nt) {
-            const int i = C.lev_rows[q];
+        const int r0 = C.lev_ptr[lev], m = C.lev_ptr[lev + 1] - r0, base = C.f_base[lev];
+        const int *joff = C.f_joff + C.f_jptr[lev];
+        for (int q = lane; q < m; q += TPS) {
+            const int i = C.lev_rows[r0 + q];
+            const int len = C.f_len[r0 + q];
             double2 acc = y[i];
-            for (int t = C.rowptr[i]; t < C.diag[i]; ++t) {
-                const double4 a = A[t];
-                const double2 yk = y[C.col[t]];
-                acc.x -= a.x * yk.x + a.y * yk.y;
-                acc.y -= a.z * yk.x + a.w * yk.y;
+            if (len <= MAXW) {
+                double4 a[MAXW];
+                int c[MAXW];
+#pragma unroll
+                for (int t = 0; t < MAXW; ++t) {
+                    if (t < len) {
+                        a[t] = ldg4(A + base + joff[t] + q);
+                        c[t] = __ldg(C.ecol + base + joff[t] + q);
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < MAXW; ++t)
+                    if (t < len) blk_sub(acc, a[t], y[c[t]]);
+            } else {
+                for (int t = 0; t < len; ++t) {
+                    const int e = base + joff[t] + q;
+                    blk_sub(acc, ldg4(A + e), y[__ldg(C.ecol + e)]);
+                }
             }
             y[i] = acc;
         }
-        __syncthreads();
+        level_sync<TPS>();
     }
     for (int lev = 0; lev < C.nlevb; ++lev) {
-        for (int q = C.levb_ptr[lev] + tid; q < C.levb_ptr[lev + 1]; q += nt) {
-            const int i = C.levb_rows[q];
+        const int r0 = C.levb_ptr[lev], m = C.levb_ptr[lev + 1] - r0, base = C.b_base[lev];
+        const int *joff = C.b_joff + C.b_jptr[lev];
+        for (int q = lane; q < m; q += TPS) {
+            const int i = C.levb_rows[r0 + q];
+            const int len = C.b_len[r0 + q];     // slot 0: inverted diagonal block
             double2 acc = y[i];
-            const int d = C.diag[i];
-            for (int t = d + 1; t < C.rowptr[i + 1]; ++t) {
-                const double4 a = A[t];
-                const double2 xk = y[C.col[t]];
-                acc.x -= a.x * xk.x + a.y * xk.y;
-                acc.y -= a.z * xk.x + a.w * xk.y;
+            const double4 di = ldg4(A + base + joff[0] + q);
+            if (len <= MAXW + 1) {
+                double4 a[MAXW];
+                int c[MAXW];
+#pragma unroll
+                for (int t = 0; t < MAXW; ++t) {
+                    if (t + 1 < len) {
+                        a[t] = ldg4(A + base + joff[t + 1] + q);
+                        c[t] = __ldg(C.ecol + base + joff[t + 1] + q);
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < MAXW; ++t)
+                    if (t + 1 < len) blk_sub(acc, a[t], y[c[t]]);
+            } else {
+                for (int t = 1; t < len; ++t) {
+                    const int e = base + joff[t] + q;
+                    blk_sub(acc, ldg4(A + e), y[__ldg(C.ecol + e)]);
+                }
             }
-            const double4 di = A[d];
             y[i] = make_double2(di.x * acc.x + di.y * acc.y, di.z * acc.x + di.w * acc.y);
         }
-        __syncthreads();
+        level_sync<TPS>();
     }
     if (VARIANT == 1) {
-        for (int l = tid; l < C.nloc; l += nt) {
+        for (int l = lane; l < C.nloc; l += TPS) {
             if (!C.owned[l]) continue;
             int gx, gy, gz;
             local_to_global(g, C, o, l, gx, gy, gz);
             z[(gz * ny + gy) * nx + gx] = y[l];
         }
     } else if (use_smem) {
-        for (int l = tid; l < C.nloc; l += nt) ext_out[sub_ext_off[s] + l] = y[l];
+        for (int l = lane; l < C.nloc; l += TPS) ext_out[sub_ext_off[s] + l] = y[l];
+    }
+}
+
+// Warp-per-subdomain solver (boxes with <= 32767 cells and levels <= 64 wide).
+// Shared memory per subdomain: y (double2 per cell) plus the class's level
+// metadata (row lists as uint16, row lengths as uint8, level starts/bases), so
+// a level costs one global round trip: the factor slots (level-major, lane q
+// reads slot base + t*m + q) and their column ids, all issued up front.
+struct WarpSmem {
+    int max_nloc, max_nlev, max_nlevb;
+    __host__ __device__ size_t y_bytes() const { return sizeof(double2) * (size_t)max_nloc; }
+    __host__ __device__ size_t bytes() const
+    {
+        size_t b = y_bytes();
+        b += sizeof(int) * (size_t)(2 * max_nlev + 1 + 2 * max_nlevb + 1);
+        b += sizeof(unsigned short) * 4 * (size_t)max_nloc;
+        return (b + 15) / 16 * 16;
+    }
+};
+
+template <int VARIANT, int MAXW = 12, int PREFETCH_DEPTH = 4>
+__global__ void __launch_bounds__(32, 8)
+apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
+                  const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
+                  const long long *__restrict__ sub_ext_off, const double4 *__restrict__ vals,
+                  const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
+                  WarpSmem L, long long nsub)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x;
+    const long long s = blockIdx.x;
+    if (s >= nsub) return;
+    const ClassDev C = classes[sub_class[s]];
+    const int4 o = sub_origin[s];
+    const double4 *__restrict__ A = vals + sub_off[s];
+    double2 *y = reinterpret_cast<double2 *>(smem_raw);
+    int *f_ptr = reinterpret_cast<int *>(smem_raw + L.y_bytes());
+    int *f_bs = f_ptr + (C.nlev + 1);
+    int *b_ptr = f_bs + C.nlev;
+    int *b_bs = b_ptr + (C.nlevb + 1);
+    unsigned short *f_rows = reinterpret_cast<unsigned short *>(b_bs + C.nlevb);
+    unsigned short *b_rows = f_rows + C.nloc;
+    unsigned short *f_len = b_rows + C.nloc;
+    unsigned short *b_len = f_len + C.nloc;
+    for (int i = lane; i <= C.nlev; i += 32) f_ptr[i] = C.lev_ptr[i];
+    for (int i = lane; i < C.nlev; i += 32) f_bs[i] = C.f_base[i];
+    for (int i = lane; i <= C.nlevb; i += 32) b_ptr[i] = C.levb_ptr[i];
+    for (int i = lane; i < C.nlevb; i += 32) b_bs[i] = C.b_base[i];
+    for (int i = lane; i < C.nloc; i += 32) {
+        f_rows[i] = C.f_rows16[i];
+        b_rows[i] = C.b_rows16[i];
+        f_len[i] = C.f_len8[i];
+        b_len[i] = C.b_len8[i];
+    }
+    // slot range of "global level" k: forward levels 0..nlev-1 then backward 0..nlevb-1
+    // (reads the shared-memory copies of the level bases: no global round trip)
+    auto level_range = [&](int k, int &lo, int &hi) {
+        if (k < C.nlev) {
+            lo = f_bs[k];
+            hi = k + 1 < C.nlev ? f_bs[k + 1] : (C.nlevb > 0 ? b_bs[0] : C.ell_total);
+        } else {
+            const int kb = k - C.nlev;
+            lo = b_bs[kb];
+            hi = kb + 1 < C.nlevb ? b_bs[kb + 1] : C.ell_total;
+        }
+    };
+    __syncwarp();
+    const int nlev_all = C.nlev + C.nlevb;
+    auto prefetch_level = [&](int k) {
+        if (k >= nlev_all) return;
+        int lo, hi;
+        level_range(k, lo, hi);
+        prefetch_l2(A + lo, (unsigned)(hi - lo) * 32u);
+    };
+    if (lane < PREFETCH_DEPTH) prefetch_level(lane);
+    const long long nx = g.nx, ny = g.ny;
+    for (int l = lane; l < C.nloc; l += 32) {
+        int gx, gy, gz;
+        local_to_global(g, C, o, l, gx, gy, gz);
+        double2 v = r[(gz * ny + gy) * nx + gx];
+        if (VARIANT == 2 && !C.owned[l]) v = make_double2(0.0, 0.0);
+        y[l] = v;
+    }
+    __syncwarp();
+    // Levels are at most 64 rows wide here.  Lane q owns rows q and q + 32 of
+    // a level; the jagged-diagonal offsets come from ballots (rows sorted by
+    // length).  The first MAXW slots of a row are loaded up front (one global
+    // round trip per level); longer rows (wrapped boxes, fill-in) finish in a
+    // tail loop.  Rows of a level are independent, so results are written
+    // after all of the level's loads.
+    for (int lev = 0; lev < C.nlev; ++lev) {
+        if (lane == 0) prefetch_level(lev + PREFETCH_DEPTH);
+        const int r0 = f_ptr[lev], m = f_ptr[lev + 1] - r0, base = f_bs[lev];
+        const int len0 = lane < m ? f_len[r0 + lane] : 0;
+        const int len1 = lane + 32 < m ? f_len[r0 + lane + 32] : 0;
+        const int i0 = lane < m ? f_rows[r0 + lane] : 0;
+        const int i1 = lane + 32 < m ? f_rows[r0 + lane + 32] : 0;
+        int offs[MAXW];
+        double4 a[MAXW];
+        int c[MAXW];
+        int off = 0;
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t) {
+            offs[t] = off;
+            if (t < len0) {
+                a[t] = ldg4(A + base + off + lane);
+                c[t] = __ldg(C.ecol + base + off + lane);
+            }
+            off += __popc(__ballot_sync(0xffffffffu, len0 > t)) + __popc(__ballot_sync(0xffffffffu, len1 > t));
+        }
+        double2 acc0 = y[i0], acc1 = y[i1];
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t)
+            if (t < len0) blk_sub(acc0, a[t], y[c[t]]);
+        if (len1 > 0) {
+#pragma unroll
+            for (int t = 0; t < MAXW; ++t)
+                if (t < len1) {
+                    a[t] = ldg4(A + base + offs[t] + lane + 32);
+                    c[t] = __ldg(C.ecol + base + offs[t] + lane + 32);
+                }
+#pragma unroll
+            for (int t = 0; t < MAXW; ++t)
+                if (t < len1) blk_sub(acc1, a[t], y[c[t]]);
+        }
+        for (int t = MAXW;; ++t) {
+            const unsigned b0 = __ballot_sync(0xffffffffu, len0 > t), b1 = __ballot_sync(0xffffffffu, len1 > t);
+            if (!(b0 | b1)) break;
+            if (t < len0) blk_sub(acc0, ldg4(A + base + off + lane), y[__ldg(C.ecol + base + off + lane)]);
+            if (t < len1) blk_sub(acc1, ldg4(A + base + off + lane + 32), y[__ldg(C.ecol + base + off + lane + 32)]);
+            off += __popc(b0) + __popc(b1);
+        }
+        if (lane < m) y[i0] = acc0;
+        if (lane + 32 < m) y[i1] = acc1;
+        __syncwarp();
+    }
+    for (int lev = 0; lev < C.nlevb; ++lev) {
+        if (lane == 0) prefetch_level(C.nlev + lev + PREFETCH_DEPTH);
+        const int r0 = b_ptr[lev], m = b_ptr[lev + 1] - r0, base = b_bs[lev];
+        // slot 0 of every row: the inverted diagonal block; U slots follow
+        const int len0 = lane < m ? b_len[r0 + lane] - 1 : 0;
+        const int len1 = lane + 32 < m ? b_len[r0 + lane + 32] - 1 : 0;
+        const int i0 = lane < m ? b_rows[r0 + lane] : 0;
+        const int i1 = lane + 32 < m ? b_rows[r0 + lane + 32] : 0;
+        int offs[MAXW];
+        double4 a[MAXW];
+        int c[MAXW];
+        int off = m;
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t) {
+            offs[t] = off;
+            if (t < len0) {
+                a[t] = ldg4(A + base + off + lane);
+                c[t] = __ldg(C.ecol + base + off + lane);
+            }
+            off += __popc(__ballot_sync(0xffffffffu, len0 > t)) + __popc(__ballot_sync(0xffffffffu, len1 > t));
+        }
+        double2 acc0 = y[i0], acc1 = y[i1];
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t)
+            if (t < len0) blk_sub(acc0, a[t], y[c[t]]);
+        if (len1 > 0) {
+#pragma unroll
+            for (int t = 0; t < MAXW; ++t)
+                if (t < len1) {
+                    a[t] = ldg4(A + base + offs[t] + lane + 32);
+                    c[t] = __ldg(C.ecol + base + offs[t] + lane + 32);
+                }
+#pragma unroll
+            for (int t = 0; t < MAXW; ++t)
+                if (t < len1) blk_sub(acc1, a[t], y[c[t]]);
+        }
+        for (int t = MAXW;; ++t) {
+            const unsigned b0 = __ballot_sync(0xffffffffu, len0 > t), b1 = __ballot_sync(0xffffffffu, len1 > t);
+            if (!(b0 | b1)) break;
+            if (t < len0) blk_sub(acc0, ldg4(A + base + off + lane), y[__ldg(C.ecol + base + off + lane)]);
+            if (t < len1) blk_sub(acc1, ldg4(A + base + off + lane + 32), y[__ldg(C.ecol + base + off + lane + 32)]);
+            off += __popc(b0) + __popc(b1);
+        }
+        if (lane < m) {
+            const double4 di = ldg4(A + base + lane);
+            y[i0] = make_double2(di.x * acc0.x + di.y * acc0.y, di.z * acc0.x + di.w * acc0.y);
+        }
+        if (lane + 32 < m) {
+            const double4 di = ldg4(A + base + lane + 32);
+            y[i1] = make_double2(di.x * acc1.x + di.y * acc1.y, di.z * acc1.x + di.w * acc1.y);
+        }
+        __syncwarp();
+    }
+    if (VARIANT == 1) {
+        for (int l = lane; l < C.nloc; l += 32) {
+            if (!C.owned[l]) continue;
+            int gx, gy, gz;
+            local_to_global(g, C, o, l, gx, gy, gz);
+            z[(gz * ny + gy) * nx + gx] = y[l];
+        }
+    } else {
+        for (int l = lane; l < C.nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
     }
 }
 
@@ -373,6 +660,61 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
     };
     bucket(lev, nlev, C.lev_ptr, C.lev_rows);
     bucket(levb, nlevb, C.levb_ptr, C.levb_rows);
+    // Jagged-diagonal slot layout per level (see apply_kernel): rows of a
+    // level sorted by decreasing length, slot(t, q) = base + off_t + q with
+    // off_t = sum_{t'<t} m_t' and m_t = #rows longer than t.  No padding, and
+    // lane q of a warp reads slot base + off_t + q: consecutive 32-byte
+    // blocks.  The factorisation addresses the same slots through pos[].
+    C.pos.assign(C.nnzb, -1);
+    int slot = 0;
+    auto layout = [&](std::vector<int> &ptr, std::vector<int> &rows, bool lower, std::vector<int> &base,
+                      std::vector<int> &lens, std::vector<int> &jptr, std::vector<int> &joff, int &maxw) {
+        const int nl = (int)ptr.size() - 1;
+        base.assign(nl, 0);
+        lens.assign(nloc, 0);
+        jptr.assign(nl + 1, 0);
+        joff.clear();
+        maxw = 0;
+        auto rlen = [&](int i) { return lower ? C.diag[i] - C.rowptr[i] : C.rowptr[i + 1] - C.diag[i]; };
+        for (int lv = 0; lv < nl; ++lv) {
+            const int r0 = ptr[lv], m = ptr[lv + 1] - r0;
+            std::stable_sort(rows.begin() + r0, rows.begin() + r0 + m, [&](int a, int b) { return rlen(a) > rlen(b); });
+            const int w = m > 0 ? rlen(rows[r0]) : 0;
+            base[lv] = slot;
+            std::vector<int> off(w + 1, 0);
+            for (int t = 0; t < w; ++t) {
+                int mt = 0;
+                while (mt < m && rlen(rows[r0 + mt]) > t) ++mt;
+                off[t + 1] = off[t] + mt;
+            }
+            for (int q = 0; q < m; ++q) {
+                const int i = rows[r0 + q];
+                const int len = rlen(i);
+                lens[r0 + q] = len;
+                const int first = lower ? C.rowptr[i] : C.diag[i];
+                for (int t = 0; t < len; ++t) C.pos[first + t] = slot + off[t] + q;
+            }
+            joff.insert(joff.end(), off.begin(), off.end());
+            jptr[lv + 1] = (int)joff.size();
+            slot += off[w];
+            maxw = std::max(maxw, m);
+        }
+    };
+    layout(C.lev_ptr, C.lev_rows, true, C.f_base, C.f_len, C.f_jptr, C.f_joff, C.max_fwidth);
+    layout(C.levb_ptr, C.levb_rows, false, C.b_base, C.b_len, C.b_jptr, C.b_joff, C.max_bwidth);
+    C.ell_total = slot;
+    C.f_rows16.assign(C.lev_rows.begin(), C.lev_rows.end());
+    C.b_rows16.assign(C.levb_rows.begin(), C.levb_rows.end());
+    C.f_len8.assign(C.f_len.begin(), C.f_len.end());
+    C.b_len8.assign(C.b_len.begin(), C.b_len.end());
+    C.ecol.assign(slot, -1);
+    for (int t = 0; t < C.nnzb; ++t) C.ecol[C.pos[t]] = C.col[t];
+    for (auto &j : C.jmap)
+        if (j >= 0) j = C.pos[j];
+    for (auto &u : C.upd) {
+        u.x = C.pos[u.x];
+        u.y = C.pos[u.y];
+    }
     C.owned.assign(nloc, 0);
     for (int l = 0; l < nloc; ++l) {
         const int ix[3] = {l % lx, (l / lx) % ly, l / (lx * ly)};
@@ -398,6 +740,13 @@ acch_status upload_class(ClassHost &C)
     const size_t o_lp = add(sizeof(int) * C.lev_ptr.size()), o_lr = add(sizeof(int) * C.lev_rows.size());
     const size_t o_bp = add(sizeof(int) * C.levb_ptr.size()), o_br = add(sizeof(int) * C.levb_rows.size());
     const size_t o_ow = add(C.owned.size());
+    const size_t o_ps = add(sizeof(int) * C.pos.size()), o_fb = add(sizeof(int) * C.f_base.size());
+    const size_t o_fl = add(sizeof(int) * C.f_len.size()), o_bb = add(sizeof(int) * C.b_base.size());
+    const size_t o_bl = add(sizeof(int) * C.b_len.size()), o_ec = add(sizeof(int) * C.ecol.size());
+    const size_t o_fr16 = add(2 * C.f_rows16.size()), o_br16 = add(2 * C.b_rows16.size());
+    const size_t o_fl8 = add(2 * C.f_len8.size()), o_bl8 = add(2 * C.b_len8.size());
+    const size_t o_fjp = add(sizeof(int) * C.f_jptr.size()), o_fjo = add(sizeof(int) * std::max<size_t>(1, C.f_joff.size()));
+    const size_t o_bjp = add(sizeof(int) * C.b_jptr.size()), o_bjo = add(sizeof(int) * std::max<size_t>(1, C.b_joff.size()));
     ACCH_CUDA(cudaMalloc(&C.dev_mem, total));
     std::vector<unsigned char> h(total, 0);
     auto put = [&](size_t o, const void *src, size_t bytes) { if (bytes) memcpy(h.data() + o, src, bytes); };
@@ -413,6 +762,20 @@ acch_status upload_class(ClassHost &C)
     put(o_bp, C.levb_ptr.data(), sizeof(int) * C.levb_ptr.size());
     put(o_br, C.levb_rows.data(), sizeof(int) * C.levb_rows.size());
     put(o_ow, C.owned.data(), C.owned.size());
+    put(o_ps, C.pos.data(), sizeof(int) * C.pos.size());
+    put(o_fb, C.f_base.data(), sizeof(int) * C.f_base.size());
+    put(o_fl, C.f_len.data(), sizeof(int) * C.f_len.size());
+    put(o_bb, C.b_base.data(), sizeof(int) * C.b_base.size());
+    put(o_bl, C.b_len.data(), sizeof(int) * C.b_len.size());
+    put(o_ec, C.ecol.data(), sizeof(int) * C.ecol.size());
+    put(o_fr16, C.f_rows16.data(), 2 * C.f_rows16.size());
+    put(o_br16, C.b_rows16.data(), 2 * C.b_rows16.size());
+    put(o_fl8, C.f_len8.data(), 2 * C.f_len8.size());
+    put(o_bl8, C.b_len8.data(), 2 * C.b_len8.size());
+    put(o_fjp, C.f_jptr.data(), sizeof(int) * C.f_jptr.size());
+    put(o_fjo, C.f_joff.data(), sizeof(int) * C.f_joff.size());
+    put(o_bjp, C.b_jptr.data(), sizeof(int) * C.b_jptr.size());
+    put(o_bjo, C.b_joff.data(), sizeof(int) * C.b_joff.size());
     ACCH_CUDA(cudaMemcpy(C.dev_mem, h.data(), total, cudaMemcpyHostToDevice));
     unsigned char *b = (unsigned char *)C.dev_mem;
     ClassDev &d = C.dev;
@@ -435,6 +798,23 @@ acch_status upload_class(ClassHost &C)
     d.levb_ptr = (const int *)(b + o_bp);
     d.levb_rows = (const int *)(b + o_br);
     d.owned = (const unsigned char *)(b + o_ow);
+    d.pos = (const int *)(b + o_ps);
+    d.f_base = (const int *)(b + o_fb);
+    d.f_len = (const int *)(b + o_fl);
+    d.b_base = (const int *)(b + o_bb);
+    d.b_len = (const int *)(b + o_bl);
+    d.ecol = (const int *)(b + o_ec);
+    d.f_rows16 = (const unsigned short *)(b + o_fr16);
+    d.b_rows16 = (const unsigned short *)(b + o_br16);
+    d.f_len8 = (const unsigned short *)(b + o_fl8);
+    d.b_len8 = (const unsigned short *)(b + o_bl8);
+    d.f_jptr = (const int *)(b + o_fjp);
+    d.f_joff = (const int *)(b + o_fjo);
+    d.b_jptr = (const int *)(b + o_bjp);
+    d.b_joff = (const int *)(b + o_bjo);
+    d.ell_total = C.ell_total;
+    d.max_fwidth = C.max_fwidth;
+    d.max_bwidth = C.max_bwidth;
     return ACCH_OK;
 }
 
@@ -453,7 +833,7 @@ struct acch_precond {
     int4 *d_sub_origin = nullptr;
     long long *d_sub_off = nullptr, *d_sub_ext_off = nullptr;
     double4 *d_vals = nullptr;
-    long long total_blocks = 0, total_ext = 0;
+    long long total_blocks = 0, total_ext = 0, total_nnzb = 0;
     int *d_bad = nullptr;
     double2 *d_ext_out = nullptr;
     long long *d_cell_ptr = nullptr, *d_cell_src = nullptr;
@@ -461,6 +841,11 @@ struct acch_precond {
     long long factorizations = 0;
     size_t apply_smem = 0;
     int use_smem = 1;
+    int tps = 32;          // threads per subdomain in the solves
+    int max_nloc = 0;
+    int warp_mode = 0;     // apply_warp_kernel usable
+    int pf_depth = 8;      // levels prefetched ahead into L2 (ACCH_PREFETCH_DEPTH overrides)
+    WarpSmem wl{0, 0, 0};
 };
 
 static void free_precond(acch_precond *pc)
@@ -555,13 +940,41 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         const ClassHost &C = pc->classes[pc->sub_class[s]];
         pc->sub_off.push_back(vo);
         pc->sub_ext_off.push_back(eo);
-        vo += C.nnzb;
+        vo += C.ell_total;
         eo += C.nloc;
+        pc->total_nnzb += C.nnzb;
         max_nloc = std::max(max_nloc, C.nloc);
     }
+    int max_width = 0;
+    for (const auto &C : pc->classes) max_width = std::max(max_width, std::max(C.max_fwidth, C.max_bwidth));
     pc->total_blocks = vo;
     pc->total_ext = eo;
-    pc->apply_smem = sizeof(double2) * (size_t)max_nloc;
+    pc->max_nloc = max_nloc;
+    pc->tps = max_width <= 64 ? 32 : 128;
+    {
+        int mnl = 0, mnb = 0;
+        for (const auto &C : pc->classes) {
+            mnl = std::max(mnl, (int)C.lev_ptr.size() - 1);
+            mnb = std::max(mnb, (int)C.levb_ptr.size() - 1);
+        }
+        pc->wl = WarpSmem{max_nloc, mnl, mnb};
+        int max_len = 0;
+        for (const auto &C : pc->classes) {
+            for (int v : C.f_len) max_len = std::max(max_len, v);
+            for (int v : C.b_len) max_len = std::max(max_len, v - 1);
+        }
+        pc->warp_mode = (max_width <= 64 && max_nloc <= 65535 && pc->wl.bytes() <= 200 * 1024) ? 1 : 0;
+        if (const char *e = getenv("ACCH_PREFETCH_DEPTH")) pc->pf_depth = atoi(e);
+        if (const char *e = getenv("ACCH_SCHWARZ_BLOCK_SOLVER"))   // testing: force the CTA-wide solver
+            if (atoi(e)) pc->warp_mode = 0, pc->tps = 128;
+        if (getenv("ACCH_DEBUG"))
+            fprintf(stderr, "[acch] precond: %lld subdomains, %zu classes, max_nloc %d, max level width %d, "
+                            "max row %d, warp smem %zu B -> %s solver\n",
+                    (long long)n_sub, pc->classes.size(), max_nloc, max_width, max_len, pc->wl.bytes(),
+                    pc->warp_mode ? "warp" : "CTA");
+    }
+    const int groups = 128 / pc->tps;
+    pc->apply_smem = sizeof(double2) * (size_t)max_nloc * groups;
     pc->use_smem = pc->apply_smem <= 200 * 1024 ? 1 : 0;
     if (!pc->use_smem) pc->apply_smem = 0;
 
@@ -632,9 +1045,30 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaMemcpy(pc->d_cell_src, src.data(), sizeof(long long) * src.size(), cudaMemcpyHostToDevice));
     }
     if (pc->use_smem && pc->apply_smem > 48 * 1024) {
-        PC_CUDA(cudaFuncSetAttribute(apply_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc->apply_smem));
-        PC_CUDA(cudaFuncSetAttribute(apply_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc->apply_smem));
-        PC_CUDA(cudaFuncSetAttribute(apply_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pc->apply_smem));
+        const int b = (int)pc->apply_smem;
+        const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<0, 32>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<1, 32>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 32>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<0, 128>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<1, 128>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 128>, attr, b));
+    }
+    if (pc->warp_mode && pc->wl.bytes() > 48 * 1024) {
+        const int b = (int)pc->wl.bytes();
+        const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 4>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 4>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 8>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 8>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 8>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 16>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16>, attr, b));
+    }
+    if (pc->warp_mode && !pc->d_ext_out && variant == 1) {
+        // ext_out is not needed by the warp kernel for left-RAS
     }
 #undef PC_CUDA
     *out = pc;
@@ -670,7 +1104,7 @@ extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef,
     if (reuse && pc->have_factors) return ACCH_OK;
     acch_ctx *ctx = pc->ctx;
     ACCH_CUDA(cudaMemsetAsync(pc->d_bad, 0x7f, sizeof(int) * pc->nsub, ctx->stream));
-    ProfScope prof_scope(ctx, PC_FACTOR, 32.0 * pc->total_blocks + 56.0 * pc->total_ext);
+    ProfScope prof_scope(ctx, PC_FACTOR, 32.0 * pc->total_nnzb + 56.0 * pc->total_ext);
     if (pc->dim == 3)
         factor_kernel<3><<<(unsigned)pc->nsub, kFactorThreads, 0, ctx->stream>>>(
             ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals,
@@ -717,16 +1151,40 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         return ACCH_ERR_NO_FACTOR;
     }
     acch_ctx *ctx = pc->ctx;
-    const unsigned nb = (unsigned)pc->nsub;
+    const int groups = 128 / pc->tps;
+    const unsigned nb = (unsigned)((pc->nsub + groups - 1) / groups);
     const size_t sm = pc->apply_smem;
-    ProfScope prof_scope(ctx, PC_APPLY, 32.0 * pc->total_blocks + 16.0 * pc->total_ext + 16.0 * ctx->g.n);
-#define APPLY(V) \
-    apply_kernel<V><<<nb, kApplyThreads, sm, ctx->stream>>>(ctx->g, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, \
-        pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->use_smem)
-    if (pc->variant == 1) APPLY(1);
-    else if (pc->variant == 0) APPLY(0);
-    else APPLY(2);
+    ProfScope prof_scope(ctx, PC_APPLY, 32.0 * pc->total_nnzb + 16.0 * pc->total_ext + 16.0 * ctx->g.n);
+#define APPLY(V, T)                                                                                    \
+    apply_kernel<V, T><<<nb, 128, sm, ctx->stream>>>(ctx->g, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, \
+        pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r, (double2 *)z, pc->d_ext_out,      \
+        pc->use_smem, pc->max_nloc, pc->nsub)
+#define WAPPLY_D(V, D)                                                                                        \
+    apply_warp_kernel<V, 12, D><<<(unsigned)pc->nsub, 32, pc->wl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,    \
+        pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
+        (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub)
+#define WAPPLY(V)                                            \
+    do {                                                     \
+        if (pc->pf_depth <= 4) WAPPLY_D(V, 4);               \
+        else if (pc->pf_depth <= 8) WAPPLY_D(V, 8);          \
+        else WAPPLY_D(V, 16);                                \
+    } while (0)
+    if (pc->warp_mode) {
+        if (pc->variant == 1) WAPPLY(1);
+        else if (pc->variant == 0) WAPPLY(0);
+        else WAPPLY(2);
+    } else if (pc->tps == 32) {
+        if (pc->variant == 1) APPLY(1, 32);
+        else if (pc->variant == 0) APPLY(0, 32);
+        else APPLY(2, 32);
+    } else {
+        if (pc->variant == 1) APPLY(1, 128);
+        else if (pc->variant == 0) APPLY(0, 128);
+        else APPLY(2, 128);
+    }
 #undef APPLY
+#undef WAPPLY
+#undef WAPPLY_D
     ACCH_LAUNCHED(ctx);
     if (pc->variant != 1) {
         const long long n = ctx->g.n;

@@ -285,3 +285,31 @@ def test_simulate_adaptive_2d_with_retries_matches_reference():
 
 def test_simulate_adaptive_3d_neumann_with_retries_matches_reference():
     _check_sim(*_run_sim("c3small"))
+
+
+@pytest.mark.parametrize("block_solver", ["0", "1"])
+@pytest.mark.parametrize("solver", ["ilu0", "ilu1"])
+def test_schwarz_wide_boxes_match_oracle(block_solver, solver, monkeypatch):
+    """Boxes whose levels are wider than a warp (and the CTA-wide solver
+    forced on small boxes) against the oracle's scalar ILU on kron(P, 1)."""
+    from oracle import acch_oracle as O
+    monkeypatch.setenv("ACCH_SCHWARZ_BLOCK_SOLVER", block_solver)
+    rng = np.random.default_rng(77)
+    counts = (16, 14, 12)
+    g = Grid(counts, (1.0, 1.0, 1.0), BoundaryCondition.NEUMANN)
+    uo, vo = 0.5 + rng.uniform(-0.1, 0.1, g.array_shape), rng.uniform(-0.1, 0.1, g.array_shape)
+    un, vn = uo + rng.uniform(-0.01, 0.01, g.array_shape), vo + rng.uniform(-0.01, 0.01, g.array_shape)
+    prob = StepProblem.create(g, PARAMS, st(g, uo, vo), 1e-3)
+    J = assemble_jacobian(prob, st(g, un, vn))
+    r = rng.standard_normal(2 * g.n_cells)
+    m = O.Mesh(counts, (1.0, 1.0, 1.0), False)
+    Jo = O.Step(m, O.Coeffs(), uo, vo, 1e-3).jacobian(O.pack(un, vn)).assemble()
+    for nsub in (1, 2):
+        pre = SchwarzPreconditioner(partition(g, nsub, 1), SchwarzVariant.LEFT_RAS,
+                                    SubdomainSolverSpec.from_string(solver))
+        pre.update(J)
+        out = host(pre.apply(torch.tensor(r, device=DEV)))
+        po = O.SchwarzOracle(O.decompose(m, nsub, 1), "ras-left", solver)
+        po.update(Jo)
+        ref = po.apply(r)
+        assert np.max(np.abs(out - ref)) <= 1e-10 * np.max(np.abs(ref))
