@@ -151,30 +151,46 @@ def workload_name(args):
 # CPU baseline: the oracle (a port of the reference algorithm) on this host
 # ---------------------------------------------------------------------------
 
-def cpu_sample(args, threads=1, budget_s=30.0):
-    """One adaptive NKS step sequence of the oracle on a reduced grid with the
-    same solver settings, reported as steps/s scaled to the full grid by the
-    cell-count ratio (optimistic for the CPU: iteration counts grow with N)."""
+# Per-step work of the timed region of the 256^3 GPU run (steps 4-7 after the
+# 3 warm-up steps; profiles/r01_bench_*.json): used by the reference arm,
+# which runs without a GPU and cannot measure them itself.
+REF_STEP_COUNTS = {"gmres_per_step": 922.0, "factorizations_per_step": 1.25, "newton_per_step": 2.25}
+
+
+def cpu_sample(args, threads=1, counts=None):
+    """CPU oracle (numpy + C ILU port of the reference, tests only) timed on
+    this host on a bounded sample of the same workload: the per-cell cost of
+    one GMRES iteration (matvec + left-RAS ILU(0) apply + MGS) and of one
+    Jacobian assembly + subdomain factorisation, measured on a 32^3 periodic
+    grid with the same 8^3 boxes, scaled to the full grid and to the GMRES
+    iterations and factorisations per step of the GPU run."""
     import numpy as np
     from oracle import acch_oracle as O
-    ns = 24 if args.dim == 3 else 128
-    while ns % args.box:
-        ns += 1
+    counts = counts or REF_STEP_COUNTS
+    ns = 32 if args.dim == 3 else 256
     m = O.Mesh((ns,) * args.dim, (1.0,) * args.dim, True)
     u, v = O.initial_fields(m, 0.5, 0.01, 1234)
-    ctl = O.Controller(1e-4, 10.0, 1e2 if args.dim == 3 else 1e4)
+    st = O.Step(m, O.Coeffs(), u, v, 2e-3)
+    rng = np.random.default_rng(1234)
+    x = O.pack(u, v) + 1e-4 * rng.standard_normal(2 * m.n_cells)
+    pre = O.SchwarzOracle(O.decompose(m, (ns // args.box) ** args.dim, 1), args.variant, args.solver, threads)
     t0 = time.perf_counter()
-    status, rows, x, ev = O.simulate(m, O.Coeffs(), u, v, ctl, 10.0, (ns // args.box) ** args.dim, 1,
-                                     args.variant, args.solver,
-                                     newton_cfg=O.NewtonSettings(gmres_restart=args.restart), max_steps=1,
-                                     threads=threads)
-    t = time.perf_counter() - t0
-    steps = len(rows) - 1
-    scale = (ns ** args.dim) / float(args.n ** args.dim)
-    return {"value": steps / t * scale, "unit": "time steps/s", "cores": threads, "kind": "port",
-            "sample": (f"oracle (numpy + C ILU port of acch) first adaptive step on {ns}^{args.dim} "
-                       f"(same solver settings), {t:.1f} s/step, scaled to {args.n}^{args.dim} by the cell ratio "
-                       f"{scale:.3g}")}
+    J = st.jacobian(x)
+    pre.update(J.assemble())
+    t_fact = time.perf_counter() - t0
+    b = -st.residual(x)
+    its = 30
+    t0 = time.perf_counter()
+    res = O.gmres(J.matvec, b, pre.apply, 1e-30, 1e-300, its, its)   # exactly `its` Arnoldi steps
+    t_gm = (time.perf_counter() - t0) / max(res.iterations, 1)
+    scale = float(args.n ** args.dim) / m.n_cells
+    t_step = scale * (counts["gmres_per_step"] * t_gm + counts["factorizations_per_step"] * t_fact)
+    return {"value": 1.0 / t_step, "unit": "time steps/s", "cores": threads, "kind": "port",
+            "sample": (f"oracle (numpy + C ILU port of acch) on {ns}^{args.dim} periodic, {args.box}^{args.dim} boxes: "
+                       f"{t_gm * 1e3:.1f} ms per GMRES iteration, {t_fact:.2f} s per assembly+factorisation; "
+                       f"scaled by the cell ratio {scale:.0f} and per-step counts {counts['gmres_per_step']:.0f} "
+                       f"GMRES + {counts['factorizations_per_step']:.2f} factorisations "
+                       f"(CPU step estimate {t_step:.0f} s)")}
 
 
 def run_reference(args):
@@ -183,9 +199,9 @@ def run_reference(args):
         return
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     vals = []
-    for i in range(args.warmup + args.steps):
+    for i in range(min(args.warmup, 1) + args.steps):
         r = cpu_sample(args, threads=threads)
-        if i >= args.warmup:
+        if i >= min(args.warmup, 1):
             vals.append(r["value"])
     value = sum(vals) / len(vals)
     line = {"metric": "NKS time steps/s (fp64, 256^3 adaptive)", "value": value, "unit": "time steps/s",
@@ -363,7 +379,11 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            cpu = cpu_sample(args, threads=1)
+            steps_done = max(args.steps, 1)
+            cpu = cpu_sample(args, threads=1, counts={
+                "gmres_per_step": gmres_total / steps_done,
+                "factorizations_per_step": max(prof.get("precond_factor", (0, 0, 0))[1], 1) / steps_done,
+                "newton_per_step": newton_total / steps_done})
         except Exception as e:  # the baseline must not break the GPU line
             cpu = {"error": repr(e)}
 

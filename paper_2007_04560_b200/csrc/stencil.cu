@@ -41,6 +41,42 @@ struct ResidualSmem {
     static constexpr size_t bytes = 2 * xbytes + 3 * gbytes;
 };
 
+__device__ __forceinline__ int mod3(int k) { return ((k % 3) + 3) % 3; }
+
+// cp.async (LDGSTS) 16-byte global -> shared copies, grouped per plane
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Chord for the residual's hot loop: same branch predicates as
+// entropy_chord (physics.py:193-200, bitwise-identical choices), with the
+// two logs of ln z - ln(1-z) merged into one log of z/(1-z), reciprocals
+// shared between the log argument and the series ratios, and FMA Horner.
+// Agrees with the reference formula to a few ulps of the O(1) terms.
+__device__ __forceinline__ double chord_fast(double a, double b, const ParamsDev &P)
+{
+    const double zeta = 0.5 * (a + b);
+    const double sigma = 0.5 * (a - b);
+    const double w = 1.0 - zeta;
+    if (sigma == 0.0) return log(zeta / w);
+    if (fabs(sigma) <= 0.4 * fmin(zeta, w)) {
+        const double iz = 1.0 / zeta, iw = 1.0 / w;
+        const double rz = sigma * iz, rw = sigma * iw;
+        const double tz = rz * rz, tw = rw * rw;
+        double pz = P.c1[P.order - 1], pw = P.c1[P.order - 1];
+        for (int s = P.order - 2; s >= 0; --s) {
+            pz = fma(pz, tz, P.c1[s]);
+            pw = fma(pw, tw, P.c1[s]);
+        }
+        return log(zeta * iw) - pz * tz + pw * tw;
+    }
+    return (entropy(a) - entropy(b)) / (a - b);
+}
+
 template <int DIM, int TX, int TY>
 __global__ void __launch_bounds__(TX *TY)
 residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ xo_g,
@@ -63,32 +99,33 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
     const int ze = (DIM == 3) ? min(zb + ZCHUNK, nz) : 1;
     const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
 
+    // plane kk of both states (tile + 2 halo) into ring slot kk mod 3, asynchronously
     auto load_plane = [&](int kk) {
-        const int slot = (DIM == 3) ? ((kk % 3) + 3) % 3 : 0;
+        const int slot = (DIM == 3) ? mod3(kk) : 0;
         const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
         for (int i = tid; i < HX * HY; i += NT) {
             const int hx = i % HX, hy = i / HX;
             const int gx = wrap_coord(x0 + hx - 2, nx, g.periodic);
             const int gy = wrap_coord(y0 + hy - 2, ny, g.periodic);
             const long long c = ((long long)gz * ny + gy) * nx + gx;
-            sxn[slot * HX * HY + i] = __ldg(xn_g + c);
-            sxo[slot * HX * HY + i] = __ldg(xo_g + c);
+            cp_async16(sxn + slot * HX * HY + i, xn_g + c);
+            cp_async16(sxo + slot * HX * HY + i, xo_g + c);
         }
+        cp_async_commit();
     };
 
     // G_u, G_v (scheme.py:270-287) and cbar (scheme.py:223-232) on tile + 1 halo of plane kk
     auto compute_g = [&](int kk) {
-        const int s0 = (DIM == 3) ? ((kk % 3) + 3) % 3 : 0;
-        const int sm = (DIM == 3) ? (((kk - 1) % 3) + 3) % 3 : 0;
-        const int sp = (DIM == 3) ? (((kk + 1) % 3) + 3) % 3 : 0;
+        const int s0 = (DIM == 3) ? mod3(kk) : 0;
+        const int sm = (DIM == 3) ? mod3(kk - 1) : 0;
+        const int sp = (DIM == 3) ? mod3(kk + 1) : 0;
         for (int i = tid; i < GX * GY; i += NT) {
             const int gx = i % GX, gy = i / GX;
             const int c = (gy + 1) * HX + (gx + 1);
-            const double2 n0 = sxn[s0 * HX * HY + c], o0 = sxo[s0 * HX * HY + c];
-            const double2 nxm = sxn[s0 * HX * HY + c - 1], nxp = sxn[s0 * HX * HY + c + 1];
-            const double2 nym = sxn[s0 * HX * HY + c - HX], nyp = sxn[s0 * HX * HY + c + HX];
-            const double2 oxm = sxo[s0 * HX * HY + c - 1], oxp = sxo[s0 * HX * HY + c + 1];
-            const double2 oym = sxo[s0 * HX * HY + c - HX], oyp = sxo[s0 * HX * HY + c + HX];
+            const double2 *n = sxn + s0 * HX * HY, *o = sxo + s0 * HX * HY;
+            const double2 n0 = n[c], o0 = o[c];
+            const double2 nxm = n[c - 1], nxp = n[c + 1], nym = n[c - HX], nyp = n[c + HX];
+            const double2 oxm = o[c - 1], oxp = o[c + 1], oym = o[c - HX], oyp = o[c + HX];
             // Laplacian, axes summed x, y, z (grid.py:263-271)
             double lun = (nxp.x - 2.0 * n0.x + nxm.x) * ihx;
             double lvn = (nxp.y - 2.0 * n0.y + nxm.y) * ihx;
@@ -106,17 +143,12 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
                 luo += (ozp.x - 2.0 * o0.x + ozm.x) * ihz;
                 lvo += (ozp.y - 2.0 * o0.y + ozm.y) * ihz;
             }
-            double phi, psi, dummy;
-            entropy_chord<false>(n0.x + n0.y, o0.x + o0.y, P, 0, phi, dummy);
-            entropy_chord<false>(n0.x - n0.y, o0.x - o0.y, P, 0, psi, dummy);
-            const double gu = -0.5 * P.alpha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) -
-                              0.5 * P.gamma * (lun + luo);
-            const double gv = -0.5 * P.beta * (n0.y + o0.y) + P.theta * (phi - psi) -
-                              0.5 * P.gamma * (lvn + lvo);
-            const int o = s0 * GX * GY + i;
-            sGu[o] = gu;
-            sGv[o] = gv;
-            sCb[o] = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
+            const double phi = chord_fast(n0.x + n0.y, o0.x + o0.y, P);
+            const double psi = chord_fast(n0.x - n0.y, o0.x - o0.y, P);
+            const int idx = s0 * GX * GY + i;
+            sGu[idx] = -0.5 * P.alpha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) - 0.5 * P.gamma * (lun + luo);
+            sGv[idx] = -0.5 * P.beta * (n0.y + o0.y) + P.theta * (phi - psi) - 0.5 * P.gamma * (lvn + lvo);
+            sCb[idx] = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
         }
     };
 
@@ -124,69 +156,75 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
     const int x = x0 + tx, y = y0 + ty;
     const bool active = x < nx && y < ny;
     const bool per = g.periodic != 0;
+    const int gc = (ty + 1) * GX + (tx + 1);
+    const int xc = (ty + 2) * HX + (tx + 2);
 
-    if (DIM == 3) {
+    auto output = [&](int k, const double2 &n0, const double2 &o0) {
+        const int s0 = (DIM == 3) ? mod3(k) : 0;
+        const int sm = (DIM == 3) ? mod3(k - 1) : 0;
+        const int sp = (DIM == 3) ? mod3(k + 1) : 0;
+        const double *Gu = sGu + s0 * GX * GY, *Cb = sCb + s0 * GX * GY;
+        const double G0 = Gu[gc], C0 = Cb[gc];
+        // div(cbar grad G_u), flux form (grid.py:274-298); a Neumann wall face
+        // carries no flux (mirrored ghost: g[ghost] - g[cell] == 0).
+        double div = 0.0;
+        {
+            const bool lo = per || x > 0, hi = per || x < nx - 1;
+            const double fp = hi ? 0.5 * (C0 + Cb[gc + 1]) * (Gu[gc + 1] - G0) : 0.0;
+            const double fm = lo ? 0.5 * (C0 + Cb[gc - 1]) * (G0 - Gu[gc - 1]) : 0.0;
+            div += (fp - fm) * ihx;
+        }
+        {
+            const bool lo = per || y > 0, hi = per || y < ny - 1;
+            const double fp = hi ? 0.5 * (C0 + Cb[gc + GX]) * (Gu[gc + GX] - G0) : 0.0;
+            const double fm = lo ? 0.5 * (C0 + Cb[gc - GX]) * (G0 - Gu[gc - GX]) : 0.0;
+            div += (fp - fm) * ihy;
+        }
+        if (DIM == 3) {
+            const bool lo = per || k > 0, hi = per || k < nz - 1;
+            const double fp = hi ? 0.5 * (C0 + sCb[sp * GX * GY + gc]) * (sGu[sp * GX * GY + gc] - G0) : 0.0;
+            const double fm = lo ? 0.5 * (C0 + sCb[sm * GX * GY + gc]) * (G0 - sGu[sm * GX * GY + gc]) : 0.0;
+            div += (fp - fm) * ihz;
+        }
+        double2 f;
+        f.x = (n0.x - o0.x) / dt - div;
+        f.y = (n0.y - o0.y) / dt + (C0 / P.rho) * sGv[s0 * GX * GY + gc];
+        F[((long long)k * ny + y) * nx + x] = f;
+        acc_norm += f.x * f.x + f.y * f.y;
+        acc_gap = red_combine(acc_gap, cell_gap(n0.x, n0.y), RED_MIN);
+    };
+
+    if (DIM == 2) {
+        load_plane(0);
+        cp_async_wait_all();
+        __syncthreads();
+        compute_g(0);
+        __syncthreads();
+        if (active) output(0, sxn[xc], sxo[xc]);
+    } else {
+        // pipeline: x ring {k, k+1, k+2}, x(k+3) in flight; G ring {k-1, k, k+1}
         load_plane(zb - 2);
         load_plane(zb - 1);
         load_plane(zb);
+        cp_async_wait_all();
         __syncthreads();
         compute_g(zb - 1);
         __syncthreads();
         load_plane(zb + 1);
+        cp_async_wait_all();
         __syncthreads();
         compute_g(zb);
-    } else {
-        load_plane(0);
         __syncthreads();
-        compute_g(0);
-    }
-    __syncthreads();
-
-    for (int k = zb; k < ze; ++k) {
-        if (DIM == 3) {
-            load_plane(k + 2);
+        load_plane(zb + 2);
+        for (int k = zb; k < ze; ++k) {
+            cp_async_wait_all();
             __syncthreads();
+            const double2 n0 = sxn[mod3(k) * HX * HY + xc], o0 = sxo[mod3(k) * HX * HY + xc];
             compute_g(k + 1);
             __syncthreads();
+            if (k + 3 <= ze + 1) load_plane(k + 3);
+            if (active) output(k, n0, o0);
         }
-        if (active) {
-            const int s0 = (DIM == 3) ? k % 3 : 0;
-            const int sm = (DIM == 3) ? (k + 2) % 3 : 0;
-            const int sp = (DIM == 3) ? (k + 1) % 3 : 0;
-            const int gc = (ty + 1) * GX + (tx + 1);
-            const double G0 = sGu[s0 * GX * GY + gc], C0 = sCb[s0 * GX * GY + gc];
-            // div(cbar grad G_u), flux form (grid.py:274-298); a Neumann wall face
-            // carries no flux (mirrored ghost: g[ghost] - g[cell] == 0).
-            double div = 0.0;
-            {
-                const bool lo = per || x > 0, hi = per || x < nx - 1;
-                const double fp = hi ? 0.5 * (C0 + sCb[s0 * GX * GY + gc + 1]) * (sGu[s0 * GX * GY + gc + 1] - G0) : 0.0;
-                const double fm = lo ? 0.5 * (C0 + sCb[s0 * GX * GY + gc - 1]) * (G0 - sGu[s0 * GX * GY + gc - 1]) : 0.0;
-                div += (fp - fm) * ihx;
-            }
-            {
-                const bool lo = per || y > 0, hi = per || y < ny - 1;
-                const double fp = hi ? 0.5 * (C0 + sCb[s0 * GX * GY + gc + GX]) * (sGu[s0 * GX * GY + gc + GX] - G0) : 0.0;
-                const double fm = lo ? 0.5 * (C0 + sCb[s0 * GX * GY + gc - GX]) * (G0 - sGu[s0 * GX * GY + gc - GX]) : 0.0;
-                div += (fp - fm) * ihy;
-            }
-            if (DIM == 3) {
-                const bool lo = per || k > 0, hi = per || k < nz - 1;
-                const double fp = hi ? 0.5 * (C0 + sCb[sp * GX * GY + gc]) * (sGu[sp * GX * GY + gc] - G0) : 0.0;
-                const double fm = lo ? 0.5 * (C0 + sCb[sm * GX * GY + gc]) * (G0 - sGu[sm * GX * GY + gc]) : 0.0;
-                div += (fp - fm) * ihz;
-            }
-            const int xc = (ty + 2) * HX + (tx + 2);
-            const double2 n0 = sxn[s0 * HX * HY + xc], o0 = sxo[s0 * HX * HY + xc];
-            double2 f;
-            f.x = (n0.x - o0.x) / dt - div;
-            f.y = (n0.y - o0.y) / dt + (C0 / P.rho) * sGv[s0 * GX * GY + gc];
-            F[((long long)k * ny + y) * nx + x] = f;
-            acc_norm += f.x * f.x + f.y * f.y;
-            acc_gap = fmin(acc_gap, cell_gap(n0.x, n0.y));
-            if (isnan(n0.x) || isnan(n0.y)) acc_gap = NAN;
-        }
-        if (DIM == 3) __syncthreads();
     }
     double v[2] = {acc_norm, acc_gap};
     const int ops[2] = {RED_SUM, RED_MIN};
@@ -242,10 +280,8 @@ __global__ void jac_prepare_kernel(GridDev g, ParamsDev P, const double2 *__rest
 
 template <int DIM, int TX, int TY>
 struct MatvecSmem {
-    // w needs planes k-1..k+2 at once (lap w_v at k, lap w_u at k+1): 4-slot ring
-    static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2, R = ring_depth(DIM),
-                         RW = DIM == 3 ? 4 : 1;
-    static constexpr size_t bytes = sizeof(double2) * RW * HX * HY + 4 * sizeof(double) * R * GX * GY;
+    static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2, R = ring_depth(DIM);
+    static constexpr size_t bytes = sizeof(double2) * R * HX * HY + 4 * sizeof(double) * R * GX * GY;
 };
 
 template <int DIM, int TX, int TY>
@@ -254,10 +290,11 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
               const double2 *__restrict__ w_g, double2 *__restrict__ yout)
 {
     using L = MatvecSmem<DIM, TX, TY>;
-    constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, RW = L::RW, NT = TX * TY;
+    constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, NT = TX * TY;
+    constexpr int NJ = (GX * GY + NT - 1) / NT;   // tile+1-halo cells per thread
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *sw = reinterpret_cast<double2 *>(smem_raw);
-    double *sdG = reinterpret_cast<double *>(sw + RW * HX * HY);
+    double *sdG = reinterpret_cast<double *>(sw + R * HX * HY);
     double *sEt = sdG + R * GX * GY;
     double *sCb = sEt + R * GX * GY;
     double *sGu = sCb + R * GX * GY;
@@ -280,103 +317,148 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
     const double hg = 0.5 * P.gamma;
     const bool per = g.periodic != 0;
 
-    auto wslot = [&](int kk) { return (DIM == 3) ? ((kk % RW) + RW) % RW : 0; };
     auto load_plane = [&](int kk) {
-        const int slot = wslot(kk);
+        const int slot = (DIM == 3) ? mod3(kk) : 0;
         const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
         for (int i = tid; i < HX * HY; i += NT) {
             const int hx = i % HX, hy = i / HX;
             const int gx = wrap_coord(x0 + hx - 2, nx, g.periodic);
             const int gy = wrap_coord(y0 + hy - 2, ny, g.periodic);
-            sw[slot * HX * HY + i] = __ldg(w_g + ((long long)gz * ny + gy) * nx + gx);
+            cp_async16(sw + slot * HX * HY + i, w_g + ((long long)gz * ny + gy) * nx + gx);
+        }
+        cp_async_commit();
+    };
+
+    // coefficient planes for this thread's tile+1-halo cells, fetched one
+    // plane ahead into registers (latency hidden behind a whole plane)
+    double pS[NJ], pD[NJ], pU[NJ], pV[NJ], pC[NJ], pG[NJ];
+    auto prefetch_coef = [&](int kk) {
+        const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int i = tid + j * NT;
+            if (i < GX * GY) {
+                const int ex = wrap_coord(x0 + i % GX - 1, nx, g.periodic);
+                const int ey = wrap_coord(y0 + i / GX - 1, ny, g.periodic);
+                const long long c = ((long long)gz * ny + ey) * nx + ex;
+                pS[j] = __ldg(cS + c);
+                pD[j] = __ldg(cD + c);
+                pU[j] = __ldg(cU + c);
+                pV[j] = __ldg(cV + c);
+                pC[j] = __ldg(cC + c);
+                pG[j] = __ldg(cG + c);
+            }
         }
     };
 
+    // dG_u and eta on tile + 1 halo of plane kk (coefficients already in registers)
     auto compute_dg = [&](int kk) {
-        const int s0 = (DIM == 3) ? ((kk % 3) + 3) % 3 : 0;
-        const int w0s = wslot(kk), wms = wslot(kk - 1), wps = wslot(kk + 1);
-        const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
-        for (int i = tid; i < GX * GY; i += NT) {
-            const int gx = i % GX, gy = i / GX;
-            const int ex = wrap_coord(x0 + gx - 1, nx, g.periodic);
-            const int ey = wrap_coord(y0 + gy - 1, ny, g.periodic);
-            const long long c = ((long long)gz * ny + ey) * nx + ex;
-            const int h = (gy + 1) * HX + (gx + 1);
-            const double2 w0 = sw[w0s * HX * HY + h];
-            double lap = (sw[w0s * HX * HY + h + 1].x - 2.0 * w0.x + sw[w0s * HX * HY + h - 1].x) * ihx;
-            lap += (sw[w0s * HX * HY + h + HX].x - 2.0 * w0.x + sw[w0s * HX * HY + h - HX].x) * ihy;
-            if (DIM == 3) lap += (sw[wps * HX * HY + h].x - 2.0 * w0.x + sw[wms * HX * HY + h].x) * ihz;
-            const int o = s0 * GX * GY + i;
-            sdG[o] = (-0.5 * P.alpha + __ldg(cS + c)) * w0.x + __ldg(cD + c) * w0.y - hg * lap;
-            sEt[o] = 0.5 * (__ldg(cU + c) * w0.x + __ldg(cV + c) * w0.y);
-            sCb[o] = __ldg(cC + c);
-            sGu[o] = __ldg(cG + c);
+        const int s0 = (DIM == 3) ? mod3(kk) : 0;
+        const int sm = (DIM == 3) ? mod3(kk - 1) : 0;
+        const int sp = (DIM == 3) ? mod3(kk + 1) : 0;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) {
+            const int i = tid + j * NT;
+            if (i < GX * GY) {
+                const int h = (i / GX + 1) * HX + (i % GX + 1);
+                const double2 *w = sw + s0 * HX * HY;
+                const double2 w0 = w[h];
+                double lap = (w[h + 1].x - 2.0 * w0.x + w[h - 1].x) * ihx;
+                lap += (w[h + HX].x - 2.0 * w0.x + w[h - HX].x) * ihy;
+                if (DIM == 3) lap += (sw[sp * HX * HY + h].x - 2.0 * w0.x + sw[sm * HX * HY + h].x) * ihz;
+                const int o = s0 * GX * GY + i;
+                sdG[o] = (-0.5 * P.alpha + pS[j]) * w0.x + pD[j] * w0.y - hg * lap;
+                sEt[o] = 0.5 * (pU[j] * w0.x + pV[j] * w0.y);
+                sCb[o] = pC[j];
+                sGu[o] = pG[j];
+            }
         }
     };
 
     const int x = x0 + tx, y = y0 + ty;
     const bool active = x < nx && y < ny;
+    const int gc = (ty + 1) * GX + (tx + 1);
+    const int hc = (ty + 2) * HX + (tx + 2);
 
-    if (DIM == 3) {
+    // xy part of lap(w_v) at the thread's own cell of plane k (read before the
+    // ring slot of plane k is recycled for plane k + 3)
+    auto lapv_xy = [&](int k) {
+        const double2 *w = sw + ((DIM == 3) ? mod3(k) : 0) * HX * HY;
+        const double c = w[hc].y;
+        return (w[hc + 1].y - 2.0 * c + w[hc - 1].y) * ihx + (w[hc + HX].y - 2.0 * c + w[hc - HX].y) * ihy;
+    };
+
+    // y at plane k: w(k) centre, xy lap(w_v), w_v(k -/+ 1) centres passed in
+    auto output = [&](int k, const double2 &w0, double lxy, double wvm, double wvp) {
+        const int s0 = (DIM == 3) ? mod3(k) : 0;
+        const int sm = (DIM == 3) ? mod3(k - 1) : 0;
+        const int sp = (DIM == 3) ? mod3(k + 1) : 0;
+        const int b0 = s0 * GX * GY + gc;
+        const double dG0 = sdG[b0], E0 = sEt[b0], C0 = sCb[b0], G0 = sGu[b0];
+        double d1 = 0.0, d2 = 0.0;
+        auto face = [&](int bn, double ih, bool lo_ok, bool hi_ok, int bm) {
+            if (hi_ok) {
+                d1 += 0.5 * (C0 + sCb[bn]) * (sdG[bn] - dG0) * ih;
+                d2 += 0.5 * (E0 + sEt[bn]) * (sGu[bn] - G0) * ih;
+            }
+            if (lo_ok) {
+                d1 -= 0.5 * (C0 + sCb[bm]) * (dG0 - sdG[bm]) * ih;
+                d2 -= 0.5 * (E0 + sEt[bm]) * (G0 - sGu[bm]) * ih;
+            }
+        };
+        face(b0 + 1, ihx, per || x > 0, per || x < nx - 1, b0 - 1);
+        face(b0 + GX, ihy, per || y > 0, per || y < ny - 1, b0 - GX);
+        if (DIM == 3) face(sp * GX * GY + gc, ihz, per || k > 0, per || k < nz - 1, sm * GX * GY + gc);
+        double lapv = lxy;
+        if (DIM == 3) lapv += (wvp - 2.0 * w0.y + wvm) * ihz;
+        const long long c = ((long long)k * ny + y) * nx + x;
+        const double S = __ldg(cS + c), D = __ldg(cD + c), Gv = __ldg(cGv + c);
+        double2 out;
+        out.x = w0.x / dt - d1 - d2;
+        out.y = w0.y / dt + (C0 / P.rho) * (D * w0.x + (-0.5 * P.beta + S) * w0.y - hg * lapv) + (Gv / P.rho) * E0;
+        yout[c] = out;
+    };
+
+    if (DIM == 2) {
+        prefetch_coef(0);
+        load_plane(0);
+        cp_async_wait_all();
+        __syncthreads();
+        compute_dg(0);
+        __syncthreads();
+        if (active) output(0, sw[hc], lapv_xy(0), 0.0, 0.0);
+    } else {
+        // pipeline: w ring {k, k+1, k+2} with w(k+3) in flight; dG ring {k-1, k, k+1}
+        prefetch_coef(zb - 1);
         load_plane(zb - 2);
         load_plane(zb - 1);
         load_plane(zb);
+        cp_async_wait_all();
         __syncthreads();
         compute_dg(zb - 1);
+        prefetch_coef(zb);
         __syncthreads();
         load_plane(zb + 1);
+        cp_async_wait_all();
         __syncthreads();
         compute_dg(zb);
-    } else {
-        load_plane(0);
+        prefetch_coef(zb + 1);
+        double wvm = sw[mod3(zb - 1) * HX * HY + hc].y;
         __syncthreads();
-        compute_dg(0);
-    }
-    __syncthreads();
-
-    for (int k = zb; k < ze; ++k) {
-        if (DIM == 3) {
-            load_plane(k + 2);
+        load_plane(zb + 2);
+        for (int k = zb; k < ze; ++k) {
+            cp_async_wait_all();
             __syncthreads();
+            const double2 w0 = sw[mod3(k) * HX * HY + hc];
+            const double wvp = sw[mod3(k + 1) * HX * HY + hc].y;
+            const double lxy = lapv_xy(k);
             compute_dg(k + 1);
+            if (k + 2 <= ze) prefetch_coef(k + 2);
             __syncthreads();
+            if (k + 3 <= ze + 1) load_plane(k + 3);
+            if (active) output(k, w0, lxy, wvm, wvp);
+            wvm = w0.y;
         }
-        if (active) {
-            const int s0 = (DIM == 3) ? k % 3 : 0;
-            const int sm = (DIM == 3) ? (k + 2) % 3 : 0;
-            const int sp = (DIM == 3) ? (k + 1) % 3 : 0;
-            const int gc = (ty + 1) * GX + (tx + 1);
-            const int b0 = s0 * GX * GY + gc;
-            const double dG0 = sdG[b0], E0 = sEt[b0], C0 = sCb[b0], G0 = sGu[b0];
-            double d1 = 0.0, d2 = 0.0;
-            auto face = [&](int bn, double ih, bool lo_ok, bool hi_ok, int bm) {
-                if (hi_ok) {
-                    d1 += 0.5 * (C0 + sCb[bn]) * (sdG[bn] - dG0) * ih;
-                    d2 += 0.5 * (E0 + sEt[bn]) * (sGu[bn] - G0) * ih;
-                }
-                if (lo_ok) {
-                    d1 -= 0.5 * (C0 + sCb[bm]) * (dG0 - sdG[bm]) * ih;
-                    d2 -= 0.5 * (E0 + sEt[bm]) * (G0 - sGu[bm]) * ih;
-                }
-            };
-            face(b0 + 1, ihx, per || x > 0, per || x < nx - 1, b0 - 1);
-            face(b0 + GX, ihy, per || y > 0, per || y < ny - 1, b0 - GX);
-            if (DIM == 3) face(sp * GX * GY + gc, ihz, per || k > 0, per || k < nz - 1, sm * GX * GY + gc);
-
-            const int h = (ty + 2) * HX + (tx + 2);
-            const int w0s = wslot(k), wms = wslot(k - 1), wps = wslot(k + 1);
-            const double2 w0 = sw[w0s * HX * HY + h];
-            double lapv = (sw[w0s * HX * HY + h + 1].y - 2.0 * w0.y + sw[w0s * HX * HY + h - 1].y) * ihx;
-            lapv += (sw[w0s * HX * HY + h + HX].y - 2.0 * w0.y + sw[w0s * HX * HY + h - HX].y) * ihy;
-            if (DIM == 3) lapv += (sw[wps * HX * HY + h].y - 2.0 * w0.y + sw[wms * HX * HY + h].y) * ihz;
-            const long long c = ((long long)k * ny + y) * nx + x;
-            const double S = __ldg(cS + c), D = __ldg(cD + c), Gv = __ldg(cGv + c);
-            double2 out;
-            out.x = w0.x / dt - d1 - d2;
-            out.y = w0.y / dt + (C0 / P.rho) * (D * w0.x + (-0.5 * P.beta + S) * w0.y - hg * lapv) + (Gv / P.rho) * E0;
-            yout[c] = out;
-        }
-        if (DIM == 3) __syncthreads();
     }
 }
 
