@@ -148,6 +148,36 @@ acch_status acch_gmres(acch_ctx *ctx, const double *coef, double dt, acch_precon
                        int32_t restart, int32_t max_iterations, int32_t ortho,
                        int32_t *iterations, int32_t *converged, double *residual_norm);
 
+/* ---- z-slab decomposition (multi-GPU; one context per rank) ------------ */
+
+/* A 3D context whose grid is this rank's slab of nz interior planes.  With
+ * ghost_planes = 2 every state / solver / coefficient vector passed to the
+ * library stores 2 ghost planes below and above the interior
+ * ((nz + 4) * nx * ny cells, acch_storage_cells); calls refresh the ghost
+ * planes of their inputs through the halo hook before reading them, and
+ * every reduction (norms, dots, gaps, caps, energies) is combined across
+ * ranks through the allreduce hook.  wall_lo / wall_hi mark the slabs that
+ * touch a homogeneous Neumann wall.  Left-RAS only (no reverse scatter). */
+typedef struct {
+    int32_t nranks, rank;
+    int32_t ghost_planes;       /* 0 (whole grid) or 2 */
+    int32_t wall_lo, wall_hi;
+} acch_slab_desc;
+
+/* op: 0 sum, 1 min, 2 max over ranks, in place on n host doubles. */
+typedef int32_t (*acch_allreduce_fn)(void *user, double *values, int32_t n, int32_t op);
+/* Fill the `depth` ghost planes on each side of device vector `vec`
+ * (plane = plane_doubles doubles; zg ghost planes, nz interior planes) from
+ * the neighbouring ranks' interior planes (wrapping for periodic z).  The
+ * library synchronises its stream before the call; the hook must complete
+ * the exchange before returning. */
+typedef int32_t (*acch_halo_fn)(void *user, double *vec, int64_t plane_doubles, int32_t nz, int32_t zg,
+                                int32_t depth);
+
+acch_status acch_ctx_set_slab(acch_ctx *ctx, const acch_slab_desc *slab);
+acch_status acch_set_comm(acch_ctx *ctx, acch_allreduce_fn allreduce, acch_halo_fn halo, void *user);
+int64_t acch_storage_cells(acch_ctx *ctx);
+
 /* Count of kernels this library has launched on ctx since creation (for the
  * bench's gpu_launches field). */
 int64_t acch_launch_count(acch_ctx *ctx);

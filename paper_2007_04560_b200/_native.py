@@ -38,6 +38,16 @@ class ParamsDesc(ctypes.Structure):
                 ("theta", ctypes.c_double), ("rho", ctypes.c_double), ("series_order", ctypes.c_int32)]
 
 
+class SlabDesc(ctypes.Structure):
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("ghost_planes", ctypes.c_int32),
+                ("wall_lo", ctypes.c_int32), ("wall_hi", ctypes.c_int32)]
+
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32,
+                                ctypes.c_int32)
+HALO_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32,
+                           ctypes.c_int32, ctypes.c_int32)
+
 _P = ctypes.c_void_p
 _D = ctypes.c_double
 _I32 = ctypes.c_int32
@@ -75,6 +85,9 @@ SIGNATURES = {
     "acch_gmres": (_I32, [_P, _P, _D, _P, _P, _P, _D, _D, _I32, _I32, _I32, _PI32, _PI32, _PD]),
     "acch_launch_count": (_I64, [_P]),
     "acch_profile_enable": (_I32, [_P, _I32]),
+    "acch_ctx_set_slab": (_I32, [_P, ctypes.POINTER(SlabDesc)]),
+    "acch_set_comm": (_I32, [_P, ALLREDUCE_FN, HALO_FN, _P]),
+    "acch_storage_cells": (_I64, [_P]),
     "acch_profile_read": (_I32, [_P, _PD, _PI64, _PD, _I32]),
 }
 
@@ -174,6 +187,18 @@ class Context:
               "acch_ctx_create")
         self.handle = h
         self._lib = lib()
+        self.comm = None
+        if getattr(grid, "nz_global", 0):
+            # a z-slab of a decomposed grid: ghost planes + cross-rank hooks
+            from .slab import comm_for
+            sd = SlabDesc(grid.nranks, grid.rank, grid.ghost, int(grid.wall_lo), int(grid.wall_hi))
+            check(self._lib.acch_ctx_set_slab(h, ctypes.byref(sd)), "acch_ctx_set_slab")
+            comm = comm_for(grid)
+            if comm is None:
+                raise RuntimeError("no communicator bound to this slab grid (slab.bind_comm)")
+            ar, ha = comm.c_hooks(self.device)
+            check(self._lib.acch_set_comm(h, ar, ha, None), "acch_set_comm")
+            self.comm = comm
 
     def bind(self):
         """Point the context at the current torch stream; returns the handle."""

@@ -18,11 +18,19 @@
 struct GridDev {
     int dim;
     int periodic;
-    int nx, ny, nz;          // nz == 1 in 2D
-    long long n;             // cells
+    int nx, ny, nz;          // nz == 1 in 2D; in slab mode the local interior planes
+    long long n;             // interior cells of this domain
     double ih2[3];           // 1 / h^2 per axis (x, y, z)
     double ih[3];            // 1 / h per axis
     double cell_volume;
+    // z-slab decomposition (multi-GPU).  zg == 0: the whole grid, z wraps or
+    // clamps like x and y.  zg > 0: vectors store zg ghost planes below and
+    // above the nz interior planes (refreshed by the halo hook); z never wraps
+    // locally and only the physical Neumann walls (zwall_lo/hi) clamp.
+    int zg;
+    int zwall_lo, zwall_hi;
+    long long zoff;          // zg * nx * ny: first interior cell in storage
+    long long nstore;        // (nz + 2 zg) * nx * ny stored cells
 };
 
 struct ParamsDev {
@@ -56,6 +64,10 @@ struct ProfState {
     double bytes[PC_COUNT] = {0};
 };
 
+struct acch_ctx;
+typedef int (*acch_allreduce_cb)(void *user, double *values, int n, int op);
+typedef int (*acch_halo_cb)(void *user, double *vec, long long plane_doubles, int nz, int zg, int depth);
+
 struct acch_ctx {
     GridDev g;
     ParamsDev p;
@@ -74,7 +86,17 @@ struct acch_ctx {
     double *d_h = nullptr;            // small device array for Hessenberg column
     long long launches = 0;
     ProfState prof;
+    // slab decomposition: rank topology and the host hooks that move ghost
+    // planes and combine per-rank partial reductions (acch_set_comm)
+    int nranks = 1, rank = 0;
+    acch_allreduce_cb allreduce = nullptr;
+    acch_halo_cb halo = nullptr;
+    void *comm_user = nullptr;
 };
+
+// multi-rank helpers (capi.cu): no-ops for a single domain
+acch_status comm_allreduce(acch_ctx *ctx, double *vals, int n, int op);
+acch_status comm_halo(acch_ctx *ctx, const double *vec, int doubles_per_cell, int depth);
 
 // Records a CUDA event pair around the launches in its scope when profiling is on.
 struct ProfScope {

@@ -54,6 +54,31 @@ acch_status acch_fetch_results(acch_ctx *ctx, int count)
     return ACCH_OK;
 }
 
+acch_status comm_allreduce(acch_ctx *ctx, double *vals, int n, int op)
+{
+    if (ctx->nranks <= 1 || !ctx->allreduce || n <= 0) return ACCH_OK;
+    if (ctx->allreduce(ctx->comm_user, vals, n, op) != 0) {
+        g_last_error = "allreduce hook failed";
+        return ACCH_ERR_CUDA;
+    }
+    return ACCH_OK;
+}
+
+acch_status comm_halo(acch_ctx *ctx, const double *vec, int doubles_per_cell, int depth)
+{
+    if (ctx->g.zg == 0 || !ctx->halo) return ACCH_OK;
+    ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
+    const long long plane = (long long)doubles_per_cell * ctx->g.nx * ctx->g.ny;
+    if (ctx->halo(ctx->comm_user, const_cast<double *>(vec), plane, ctx->g.nz, ctx->g.zg, depth) != 0) {
+        g_last_error = "halo hook failed";
+        return ACCH_ERR_CUDA;
+    }
+    return ACCH_OK;
+}
+
+// gap reductions: NaN (inadmissible) -> -inf before the cross-rank min
+static double gap_value(double g) { return isnan(g) ? -INFINITY : g; }
+
 // launchers defined in stencil.cu without a shared header entry
 acch_status launch_chord(acch_ctx *ctx, const double *a, const double *b, long long n, int force_exact, double *val,
                          double *der);
@@ -139,6 +164,10 @@ acch_status acch_ctx_create(const acch_grid_desc *grid, const acch_params *param
         }
     }
     g.cell_volume = vol;
+    g.zg = 0;
+    g.zwall_lo = g.zwall_hi = g.periodic ? 0 : 1;
+    g.zoff = 0;
+    g.nstore = g.n;
     ParamsDev &p = ctx->p;
     p.alpha = params->alpha;
     p.beta = params->beta;
@@ -189,6 +218,40 @@ acch_status acch_set_stream(acch_ctx *ctx, void *cuda_stream)
 }
 
 int64_t acch_launch_count(acch_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+acch_status acch_ctx_set_slab(acch_ctx *ctx, const acch_slab_desc *slab)
+{
+    CHECK_CTX(ctx);
+    if (!slab || slab->nranks < 1 || slab->rank < 0 || slab->rank >= slab->nranks || slab->ghost_planes < 0 ||
+        slab->ghost_planes > 2 || ctx->g.dim != 3 || ctx->d_krylov) {
+        acch_set_error("acch_ctx_set_slab: invalid slab (3D only, 0..2 ghost planes, before any GMRES call)");
+        return ACCH_ERR_INVALID_ARG;
+    }
+    GridDev &g = ctx->g;
+    ctx->nranks = slab->nranks;
+    ctx->rank = slab->rank;
+    g.zg = slab->ghost_planes;
+    if (g.zg == 0) {
+        g.zwall_lo = g.zwall_hi = g.periodic ? 0 : 1;
+    } else {
+        g.zwall_lo = slab->wall_lo ? 1 : 0;
+        g.zwall_hi = slab->wall_hi ? 1 : 0;
+    }
+    g.zoff = (long long)g.zg * g.nx * g.ny;
+    g.nstore = g.n + 2 * g.zoff;
+    return ACCH_OK;
+}
+
+acch_status acch_set_comm(acch_ctx *ctx, acch_allreduce_fn allreduce, acch_halo_fn halo, void *user)
+{
+    CHECK_CTX(ctx);
+    ctx->allreduce = (acch_allreduce_cb)allreduce;
+    ctx->halo = (acch_halo_cb)halo;
+    ctx->comm_user = user;
+    return ACCH_OK;
+}
+
+int64_t acch_storage_cells(acch_ctx *ctx) { return ctx ? ctx->g.nstore : 0; }
 
 acch_status acch_profile_enable(acch_ctx *ctx, int32_t on)
 {
@@ -252,18 +315,24 @@ acch_status acch_admissibility_gap(acch_ctx *ctx, const double *x, double *gap)
     CHECK_CTX(ctx);
     TRY(launch_gap(ctx, x));
     TRY(acch_fetch_results(ctx, 1));
-    if (gap) *gap = isnan(ctx->h_result[0]) ? -INFINITY : ctx->h_result[0];
+    double v = gap_value(ctx->h_result[0]);
+    TRY(comm_allreduce(ctx, &v, 1, 1));
+    if (gap) *gap = v;
     return ACCH_OK;
 }
 
 acch_status acch_diagnostics(acch_ctx *ctx, const double *x, double *energy, double *mass_u, double *max_abs_v)
 {
     CHECK_CTX(ctx);
+    TRY(comm_halo(ctx, x, 2, 1));
     TRY(launch_diagnostics(ctx, x));
     TRY(acch_fetch_results(ctx, 3));
-    if (energy) *energy = ctx->h_result[0] * ctx->g.cell_volume;
-    if (mass_u) *mass_u = ctx->h_result[1] * ctx->g.cell_volume;
-    if (max_abs_v) *max_abs_v = ctx->h_result[2];
+    double sums[2] = {ctx->h_result[0], ctx->h_result[1]}, vmax = ctx->h_result[2];
+    TRY(comm_allreduce(ctx, sums, 2, 0));
+    TRY(comm_allreduce(ctx, &vmax, 1, 2));
+    if (energy) *energy = sums[0] * ctx->g.cell_volume;
+    if (mass_u) *mass_u = sums[1] * ctx->g.cell_volume;
+    if (max_abs_v) *max_abs_v = vmax;
     return ACCH_OK;
 }
 
@@ -275,12 +344,16 @@ acch_status acch_residual(acch_ctx *ctx, const double *x_old, double dt, const d
         acch_set_error("acch_residual: invalid argument (time step must be positive)");
         return ACCH_ERR_INVALID_ARG;
     }
+    TRY(comm_halo(ctx, x_old, 2, 2));
+    TRY(comm_halo(ctx, x, 2, 2));
     TRY(launch_residual(ctx, x_old, dt, x, F));
     if (!gap && !norm2) return ACCH_OK;   // asynchronous form: no readback, no admissibility check
     TRY(acch_fetch_results(ctx, 2));
-    const double gp = isnan(ctx->h_result[1]) ? -INFINITY : ctx->h_result[1];
+    double nrm = ctx->h_result[0], gp = gap_value(ctx->h_result[1]);
+    TRY(comm_allreduce(ctx, &nrm, 1, 0));
+    TRY(comm_allreduce(ctx, &gp, 1, 1));
     if (gap) *gap = gp;
-    if (norm2) *norm2 = ctx->h_result[0];
+    if (norm2) *norm2 = nrm;
     if (!(gp >= kMargin)) {
         char buf[160];
         snprintf(buf, sizeof buf, "state violates admissibility bounds (gap %.3e < margin %.1e)", gp, kMargin);
@@ -297,7 +370,12 @@ acch_status acch_jacobian_prepare(acch_ctx *ctx, const double *x_old, double dt,
         acch_set_error("acch_jacobian_prepare: invalid argument");
         return ACCH_ERR_INVALID_ARG;
     }
-    return launch_jacobian_prepare(ctx, x_old, dt, x, coef);
+    TRY(comm_halo(ctx, x_old, 2, 1));
+    TRY(comm_halo(ctx, x, 2, 1));
+    TRY(launch_jacobian_prepare(ctx, x_old, dt, x, coef));
+    // the factorisation reads coefficients one plane beyond an overlapping box
+    for (int f = 0; f < CO_NFIELDS; ++f) TRY(comm_halo(ctx, coef + f * ctx->g.nstore, 1, 2));
+    return ACCH_OK;
 }
 
 acch_status acch_jacobian_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
@@ -307,6 +385,7 @@ acch_status acch_jacobian_matvec(acch_ctx *ctx, const double *coef, double dt, c
         acch_set_error("acch_jacobian_matvec: invalid argument");
         return ACCH_ERR_INVALID_ARG;
     }
+    TRY(comm_halo(ctx, w, 2, 2));
     return launch_matvec(ctx, coef, dt, w, y);
 }
 
@@ -323,9 +402,17 @@ acch_status acch_jacobian_blocks(acch_ctx *ctx, const double *coef, double dt, d
 acch_status acch_dot(acch_ctx *ctx, const double *a, const double *b, int64_t n, double *out)
 {
     CHECK_CTX(ctx);
+    // a whole-storage state vector in slab mode: reduce over this rank's interior
+    if (ctx->g.zg && n == 2 * ctx->g.nstore) {
+        a += 2 * ctx->g.zoff;
+        b += 2 * ctx->g.zoff;
+        n = 2 * ctx->g.n;
+    }
     TRY(launch_dot(ctx, a, b, n));
     TRY(acch_fetch_results(ctx, 1));
-    if (out) *out = ctx->h_result[0];
+    double v = ctx->h_result[0];
+    TRY(comm_allreduce(ctx, &v, 1, 0));
+    if (out) *out = v;
     return ACCH_OK;
 }
 
@@ -347,9 +434,16 @@ acch_status acch_rms_diff(acch_ctx *ctx, const double *a, const double *b, int64
         acch_set_error("acch_rms_diff: empty vector");
         return ACCH_ERR_INVALID_ARG;
     }
+    if (ctx->g.zg && n == 2 * ctx->g.nstore) {
+        a += 2 * ctx->g.zoff;
+        b += 2 * ctx->g.zoff;
+        n = 2 * ctx->g.n;
+    }
     TRY(launch_rms_diff(ctx, a, b, n));
     TRY(acch_fetch_results(ctx, 1));
-    if (out) *out = sqrt(ctx->h_result[0] / (double)n);
+    double v[2] = {ctx->h_result[0], (double)n};
+    TRY(comm_allreduce(ctx, v, 2, 0));
+    if (out) *out = sqrt(v[0] / v[1]);
     return ACCH_OK;
 }
 
@@ -358,7 +452,9 @@ acch_status acch_trial(acch_ctx *ctx, const double *x, const double *s, double l
     CHECK_CTX(ctx);
     TRY(launch_trial(ctx, x, s, lam, y));
     TRY(acch_fetch_results(ctx, 1));
-    if (gap) *gap = isnan(ctx->h_result[0]) ? -INFINITY : ctx->h_result[0];
+    double v = gap_value(ctx->h_result[0]);
+    TRY(comm_allreduce(ctx, &v, 1, 1));
+    if (gap) *gap = v;
     return ACCH_OK;
 }
 
@@ -368,7 +464,9 @@ acch_status acch_feasible_cap(acch_ctx *ctx, const double *x, const double *s, d
     CHECK_CTX(ctx);
     TRY(launch_feasible_cap(ctx, x, s, margin));
     TRY(acch_fetch_results(ctx, 1));
-    const double c = ctx->h_result[0];
+    double c = ctx->h_result[0];
+    if (isnan(c)) c = INFINITY;
+    TRY(comm_allreduce(ctx, &c, 1, 1));
     double out;
     if (!isfinite(c)) out = 1.0;   // newton.py:97-98 (no bound is active, or NaN)
     else out = fmin(1.0, fraction * c);

@@ -32,23 +32,24 @@ template <int DIM>
 __device__ __forceinline__ void jac_row_blocks(const GridDev &g, const ParamsDev &P, double dt, const double *__restrict__ coef,
                                int x, int y, int z, double (*blk)[4], int noff)
 {
-    const long long N = g.n;
+    // x, y wrap or clamp; z stays a raw local plane index (it may address a
+    // slab ghost plane) and is mapped to storage by zplane()
+    const long long N = g.nstore;
     const int cc[3] = {x, y, z};
     const int nn[3] = {g.nx, g.ny, g.nz};
     for (int o = 0; o < noff; ++o) blk[o][0] = blk[o][1] = blk[o][2] = blk[o][3] = 0.0;
-    auto cid = [&](const int (&q)[3]) -> long long {
-        return ((long long)q[2] * g.ny + q[1]) * g.nx + q[0];
-    };
+    auto cid = [&](const int (&q)[3]) -> long long { return cell_at(g, q[0], q[1], zplane(g, q[2])); };
     auto offid = [&](int dx, int dy, int dz) { return stencil_offset_id<DIM>(dx, dy, dz); };
-    // neighbour m = c + e_a s is valid when periodic or inside the box
+    // neighbour m = c + e_a s exists (periodic, inside the box, or across a slab boundary)
     auto valid = [&](const int (&q)[3], int a, int s) {
+        if (a == 2) return zstep_ok(g, q[2], s);
         if (g.periodic) return true;
         const int t = q[a] + s;
         return t >= 0 && t < nn[a];
     };
     auto shifted = [&](const int (&q)[3], int a, int s, int (&r)[3]) {
         r[0] = q[0]; r[1] = q[1]; r[2] = q[2];
-        r[a] = wrap_coord(q[a] + s, nn[a], g.periodic);
+        r[a] = a == 2 ? q[a] + s : wrap_coord(q[a] + s, nn[a], g.periodic);
     };
     const long long c0 = cid(cc);
     const double cb0 = coef[CO_CBAR * N + c0], gu0 = coef[CO_GU * N + c0];
@@ -82,8 +83,9 @@ __device__ __forceinline__ void jac_row_blocks(const GridDev &g, const ParamsDev
     const double hg = 0.5 * P.gamma;
     for (int j = 0; j < nm; ++j) {
         int q[3] = {cc[0], cc[1], cc[2]};
-        for (int a = 0; a < 3; ++a)
+        for (int a = 0; a < 2; ++a)
             if (mo[3 * j + a] != 0) q[a] = wrap_coord(cc[a] + mo[3 * j + a], nn[a], g.periodic);
+        q[2] = cc[2] + mo[3 * j + 2];
         const long long cm = cid(q);
         double lsum = 0.0;   // sum of 1/h^2 over valid neighbours of m
         for (int a = 0; a < g.dim; ++a) {

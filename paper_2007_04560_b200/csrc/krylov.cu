@@ -227,7 +227,7 @@ static acch_status scale_by(acch_ctx *ctx, double a, const double *x, double *y,
 
 static acch_status ensure_krylov(acch_ctx *ctx, int restart)
 {
-    const long long nv = 2 * ctx->g.n;
+    const long long nv = 2 * ctx->g.nstore;
     if (ctx->d_krylov && ctx->krylov_cols >= restart + 1) return ACCH_OK;
     if (ctx->d_krylov) cudaFree(ctx->d_krylov);
     if (ctx->d_work) cudaFree(ctx->d_work);
@@ -235,6 +235,10 @@ static acch_status ensure_krylov(acch_ctx *ctx, int restart)
     ctx->d_work = nullptr;
     ACCH_CUDA(cudaMalloc(&ctx->d_krylov, sizeof(double) * nv * (restart + 1)));
     ACCH_CUDA(cudaMalloc(&ctx->d_work, sizeof(double) * nv * 3));
+    // slab ghost planes are rewritten by the halo hook before every read;
+    // start them (and everything else) from zero rather than stale memory
+    ACCH_CUDA(cudaMemsetAsync(ctx->d_krylov, 0, sizeof(double) * nv * (restart + 1), ctx->stream));
+    ACCH_CUDA(cudaMemsetAsync(ctx->d_work, 0, sizeof(double) * nv * 3, ctx->stream));
     ctx->krylov_cols = restart + 1;
     return ACCH_OK;
 }
@@ -262,20 +266,42 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
         return ACCH_ERR_INVALID_ARG;
     }
     TRY(ensure_krylov(ctx, restart));
-    const long long n = 2 * ctx->g.n;
+    // nv: stored vector length (column stride); [off, off + ni): this rank's
+    // interior, the only part that enters dots and norms
+    const long long nv = 2 * ctx->g.nstore, off = 2 * ctx->g.zoff, ni = 2 * ctx->g.n;
+    const bool multi = ctx->nranks > 1;
     double *V = ctx->d_krylov;
-    double *Z = ctx->d_work, *R = ctx->d_work + n, *T = ctx->d_work + 2 * n;
+    double *Z = ctx->d_work, *R = ctx->d_work + nv, *T = ctx->d_work + 2 * nv;
     double *dh = ctx->d_h;      // [0..63] scratch for dots
-    auto col = [&](int j) { return V + (long long)j * n; };
+    auto col = [&](int j) { return V + (long long)j * nv; };
+    auto matvec = [&](const double *in, double *out) -> acch_status {
+        TRY(comm_halo(ctx, in, 2, 2));
+        return launch_matvec(ctx, coef, dt, in, out);
+    };
+    auto precond = [&](const double *in, double *out) -> acch_status {
+        TRY(comm_halo(ctx, in, 2, 1));
+        return precond_apply_impl(pc, in, out);
+    };
+    // fetch `count` dot results, combine across ranks, and (when a kernel
+    // reads them next) put the combined values back on the device
+    auto reduce_dots = [&](double *host, double *dev, int count, bool to_device) -> acch_status {
+        TRY(fetch(ctx, host, dev, count));
+        if (multi) {
+            TRY(comm_allreduce(ctx, host, count, 0));
+            if (to_device)
+                ACCH_CUDA(cudaMemcpyAsync(dev, host, sizeof(double) * count, cudaMemcpyHostToDevice, ctx->stream));
+        }
+        return ACCH_OK;
+    };
 
     double tmp[64];
-    TRY(dot_to(ctx, b, b, n, dh));
-    TRY(fetch(ctx, tmp, dh, 1));
+    TRY(dot_to(ctx, b + off, b + off, ni, dh));
+    TRY(reduce_dots(tmp, dh, 1, false));
     const double bnorm = sqrt(tmp[0]);
     const double tol = std::max(rel_tol * bnorm, abs_tol);
 
-    ACCH_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * n, ctx->stream));
-    ACCH_CUDA(cudaMemcpyAsync(R, b, sizeof(double) * n, cudaMemcpyDeviceToDevice, ctx->stream));
+    ACCH_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nv, ctx->stream));
+    ACCH_CUDA(cudaMemcpyAsync(R, b, sizeof(double) * nv, cudaMemcpyDeviceToDevice, ctx->stream));
     double res_norm = bnorm;
     int total = 0;
     std::vector<double> H((restart + 1) * restart), cs(restart), sn(restart), gv(restart + 1), y(restart);
@@ -294,62 +320,74 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
         std::fill(cs.begin(), cs.end(), 0.0);
         std::fill(sn.begin(), sn.end(), 0.0);
         std::fill(gv.begin(), gv.end(), 0.0);
-        TRY(scale_by(ctx, res_norm, R, col(0), n));
+        TRY(scale_by(ctx, res_norm, R, col(0), nv));
         gv[0] = res_norm;
         int j = 0;
         bool breakdown = false;
         while (j < restart && total < max_it) {
             const double *zj = col(j);
             if (pc) {
-                TRY(precond_apply_impl(pc, col(j), Z));
+                TRY(precond(col(j), Z));
                 zj = Z;
             }
             double *w = col(j + 1);
-            TRY(launch_matvec(ctx, coef, dt, zj, w));
+            TRY(matvec(zj, w));
             double norm_before, norm_after;
             if (ortho == 1) {
                 int ns = 0;
-                TRY(mdot_to(ctx, V, n, j + 1, w, n, dh, &ns));
-                TRY(mupdate_to(ctx, V, n, j + 1, dh, w, n, dh + 40));
-                TRY(fetch(ctx, tmp, dh, 41));
+                TRY(mdot_to(ctx, V + off, nv, j + 1, w + off, ni, dh, &ns));
+                if (multi) {
+                    TRY(reduce_dots(tmp, dh, ns, true));
+                    TRY(mupdate_to(ctx, V + off, nv, j + 1, dh, w + off, ni, dh + 40));
+                    double t40;
+                    TRY(reduce_dots(&t40, dh + 40, 1, false));
+                    tmp[40] = t40;
+                } else {
+                    TRY(mupdate_to(ctx, V + off, nv, j + 1, dh, w + off, ni, dh + 40));
+                    TRY(fetch(ctx, tmp, dh, 41));
+                }
                 for (int i = 0; i <= j; ++i) h(i, j) = tmp[i];
                 norm_before = sqrt(tmp[ns - 1]);
                 norm_after = sqrt(tmp[40]);
                 if (norm_after < 0.5 * norm_before) {
-                    TRY(mdot_to(ctx, V, n, j + 1, w, n, dh, &ns));
-                    TRY(mupdate_to(ctx, V, n, j + 1, dh, w, n, dh + 40));
-                    TRY(fetch(ctx, tmp, dh, 41));
-                    for (int i = 0; i <= j; ++i) h(i, j) += tmp[i];
-                    norm_after = sqrt(tmp[40]);
+                    TRY(mdot_to(ctx, V + off, nv, j + 1, w + off, ni, dh, &ns));
+                    double t2[64];
+                    if (multi) TRY(reduce_dots(t2, dh, ns, true));
+                    TRY(mupdate_to(ctx, V + off, nv, j + 1, dh, w + off, ni, dh + 40));
+                    if (multi) {
+                        double t40;
+                        TRY(reduce_dots(&t40, dh + 40, 1, false));
+                        t2[40] = t40;
+                    } else {
+                        TRY(fetch(ctx, t2, dh, 41));
+                    }
+                    for (int i = 0; i <= j; ++i) h(i, j) += t2[i];
+                    norm_after = sqrt(t2[40]);
                 }
             } else {
-                TRY(dot_to(ctx, w, w, n, dh + 40));
-                for (int i = 0; i <= j; ++i) {
-                    TRY(dot_to(ctx, col(i), w, n, dh + i));
-                    {
-                        ProfScope ps(ctx, PC_KUPDATE, 24.0 * n);
-                        axpy_dev_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(dh + i, col(i), w, n);
+                TRY(dot_to(ctx, w + off, w + off, ni, dh + 40));
+                if (multi) TRY(reduce_dots(tmp + 40, dh + 40, 1, false));
+                for (int pass = 0; pass < 2; ++pass) {
+                    for (int i = 0; i <= j; ++i) {
+                        TRY(dot_to(ctx, col(i) + off, w + off, ni, dh + i));
+                        if (multi) TRY(reduce_dots(tmp + i, dh + i, 1, true));
+                        ProfScope ps(ctx, PC_KUPDATE, 24.0 * ni);
+                        axpy_dev_kernel<<<vgrid(ni), kRedThreads, 0, ctx->stream>>>(dh + i, col(i) + off, w + off, ni);
                         ACCH_LAUNCHED(ctx);
                     }
-                }
-                TRY(dot_to(ctx, w, w, n, dh + 41));
-                TRY(fetch(ctx, tmp, dh, 42));
-                for (int i = 0; i <= j; ++i) h(i, j) = tmp[i];
-                norm_before = sqrt(tmp[40]);
-                norm_after = sqrt(tmp[41]);
-                if (norm_after < 0.5 * norm_before) {
-                    for (int i = 0; i <= j; ++i) {
-                        TRY(dot_to(ctx, col(i), w, n, dh + i));
-                        {
-                            ProfScope ps(ctx, PC_KUPDATE, 24.0 * n);
-                            axpy_dev_kernel<<<vgrid(n), kRedThreads, 0, ctx->stream>>>(dh + i, col(i), w, n);
-                            ACCH_LAUNCHED(ctx);
-                        }
+                    TRY(dot_to(ctx, w + off, w + off, ni, dh + 41));
+                    double hv[42];
+                    if (multi) {
+                        TRY(reduce_dots(hv + 41, dh + 41, 1, false));
+                        for (int i = 0; i <= j; ++i) hv[i] = tmp[i];
+                    } else {
+                        TRY(fetch(ctx, hv, dh, 42));
+                        if (pass == 0) tmp[40] = hv[40];
                     }
-                    TRY(dot_to(ctx, w, w, n, dh + 41));
-                    TRY(fetch(ctx, tmp, dh, 42));
-                    for (int i = 0; i <= j; ++i) h(i, j) += tmp[i];
-                    norm_after = sqrt(tmp[41]);
+                    for (int i = 0; i <= j; ++i) h(i, j) += hv[i];
+                    if (pass == 0) norm_before = sqrt(tmp[40]);
+                    norm_after = sqrt(hv[41]);
+                    if (!(norm_after < 0.5 * norm_before)) break;   // second pass only on severe cancellation
                 }
             }
             h(j + 1, j) = norm_after;
@@ -375,7 +413,7 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                 breakdown = true;
                 break;
             }
-            TRY(scale_by(ctx, norm_after, w, w, n));
+            TRY(scale_by(ctx, norm_after, w, w, nv));
             if (fabs(gv[j]) <= tol) break;
         }
         if (j > 0) {
@@ -386,20 +424,20 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                 y[i] = s / h(i, i);
             }
             ACCH_CUDA(cudaMemcpyAsync(dh, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, ctx->stream));
-            TRY(combine(ctx, V, n, j, dh, T, n));
+            TRY(combine(ctx, V, nv, j, dh, T, nv));
             if (pc) {
-                TRY(precond_apply_impl(pc, T, Z));
-                TRY(launch_axpby(ctx, 1.0, Z, 1.0, x, n));
+                TRY(precond(T, Z));
+                TRY(launch_axpby(ctx, 1.0, Z, 1.0, x, nv));
             } else {
-                TRY(launch_axpby(ctx, 1.0, T, 1.0, x, n));
+                TRY(launch_axpby(ctx, 1.0, T, 1.0, x, nv));
             }
             // the host array y is reused next cycle: make sure the copy landed
             ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
         }
-        TRY(launch_matvec(ctx, coef, dt, x, R));
-        TRY(launch_axpby(ctx, 1.0, b, -1.0, R, n));
-        TRY(dot_to(ctx, R, R, n, dh));
-        TRY(fetch(ctx, tmp, dh, 1));
+        TRY(matvec(x, R));
+        TRY(launch_axpby(ctx, 1.0, b, -1.0, R, nv));
+        TRY(dot_to(ctx, R + off, R + off, ni, dh));
+        TRY(reduce_dots(tmp, dh, 1, false));
         res_norm = sqrt(tmp[0]);
         if (breakdown && res_norm > tol) {
             *iterations = total; *converged = 0; *residual_norm = res_norm;

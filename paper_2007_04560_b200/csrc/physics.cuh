@@ -83,3 +83,25 @@ __device__ __forceinline__ int wrap_coord(int i, int n, int periodic)
     }
     return i < 0 ? 0 : (i >= n ? n - 1 : i);
 }
+
+// storage plane of local z-plane z (z may reach zg planes past either end)
+__device__ __forceinline__ int zplane(const GridDev &g, int z)
+{
+    if (g.zg == 0) return wrap_coord(z, g.nz, g.periodic);
+    if (z < 0 && g.zwall_lo) z = 0;
+    if (z >= g.nz && g.zwall_hi) z = g.nz - 1;
+    return z + g.zg;
+}
+
+// can a stencil step from local plane z to z + s (no physical wall crossed)?
+__device__ __forceinline__ bool zstep_ok(const GridDev &g, int z, int s)
+{
+    const int t = z + s;
+    if (g.zg == 0) return g.periodic || (t >= 0 && t < g.nz);
+    return !((t < 0 && g.zwall_lo) || (t >= g.nz && g.zwall_hi));
+}
+
+__device__ __forceinline__ long long cell_at(const GridDev &g, int x, int y, int zs)
+{
+    return ((long long)zs * g.ny + y) * g.nx + x;
+}

@@ -85,7 +85,9 @@ __device__ __forceinline__ void local_to_global(const GridDev &g, const ClassDev
     const int iz = l / (C.len[0] * C.len[1]);
     gx = wrap_coord(o.x + C.rel[0][ix], g.nx, g.periodic);
     gy = wrap_coord(o.y + C.rel[1][iy], g.ny, g.periodic);
-    gz = g.dim == 3 ? wrap_coord(o.z + C.rel[2][iz], g.nz, g.periodic) : 0;
+    // z: wrapped local plane for a whole-grid domain; in slab mode a raw local
+    // plane that may lie in a ghost plane (overlap into the neighbour slab)
+    gz = g.dim == 3 ? (g.zg ? o.z + C.rel[2][iz] : wrap_coord(o.z + C.rel[2][iz], g.nz, g.periodic)) : 0;
 }
 
 struct Blk {
@@ -225,7 +227,7 @@ apply_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restr
     for (int l = lane; l < C.nloc; l += TPS) {
         int gx, gy, gz;
         local_to_global(g, C, o, l, gx, gy, gz);
-        double2 v = r[(gz * ny + gy) * nx + gx];
+        double2 v = r[cell_at(g, gx, gy, zplane(g, gz))];
         if (VARIANT == 2 && !C.owned[l]) v = make_double2(0.0, 0.0);
         y[l] = v;
     }
@@ -298,7 +300,7 @@ apply_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restr
             if (!C.owned[l]) continue;
             int gx, gy, gz;
             local_to_global(g, C, o, l, gx, gy, gz);
-            z[(gz * ny + gy) * nx + gx] = y[l];
+            z[cell_at(g, gx, gy, zplane(g, gz))] = y[l];
         }
     } else if (use_smem) {
         for (int l = lane; l < C.nloc; l += TPS) ext_out[sub_ext_off[s] + l] = y[l];
@@ -381,7 +383,7 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     for (int l = lane; l < C.nloc; l += 32) {
         int gx, gy, gz;
         local_to_global(g, C, o, l, gx, gy, gz);
-        double2 v = r[(gz * ny + gy) * nx + gx];
+        double2 v = r[cell_at(g, gx, gy, zplane(g, gz))];
         if (VARIANT == 2 && !C.owned[l]) v = make_double2(0.0, 0.0);
         y[l] = v;
     }
@@ -496,7 +498,234 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
             if (!C.owned[l]) continue;
             int gx, gy, gz;
             local_to_global(g, C, o, l, gx, gy, gz);
-            z[(gz * ny + gy) * nx + gx] = y[l];
+            z[cell_at(g, gx, gy, zplane(g, gz))] = y[l];
+        }
+    } else {
+        for (int l = lane; l < C.nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// TMA-streamed warp solver.  Same sweeps as apply_warp_kernel, but each
+// level's factor slots and column ids are brought into a per-warp
+// shared-memory ring by cp.async.bulk (TMA) several levels ahead, completion
+// tracked by mbarriers, so the level loop computes from shared memory while
+// HBM streams the next levels.  Ring placement is a contiguous circular
+// allocator over levels consumed strictly in order.
+// ---------------------------------------------------------------------------
+
+constexpr int kRingSlots = 16;   // mbarriers = max levels in flight
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+struct TmaSmem {
+    WarpSmem w;
+    int ring_bytes;
+    __host__ __device__ size_t meta_end() const { return w.bytes(); }
+    __host__ __device__ size_t bar_off() const { return (meta_end() + 15) / 16 * 16; }
+    __host__ __device__ size_t ring_off() const { return bar_off() + sizeof(uint64_t) * kRingSlots + 16 * 2; }
+    __host__ __device__ size_t bytes() const { return ring_off() + (size_t)ring_bytes; }
+};
+
+template <int VARIANT>
+__global__ void __launch_bounds__(32)
+apply_tma_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
+                 const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
+                 const long long *__restrict__ sub_ext_off, const double4 *__restrict__ vals,
+                 const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
+                 TmaSmem L, long long nsub)
+{
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x;
+    const long long s = blockIdx.x;
+    if (s >= nsub) return;
+    const ClassDev C = classes[sub_class[s]];
+    const int4 o = sub_origin[s];
+    const double4 *__restrict__ A = vals + sub_off[s];
+    double2 *y = reinterpret_cast<double2 *>(smem_raw);
+    int *f_ptr = reinterpret_cast<int *>(smem_raw + L.w.y_bytes());
+    int *f_bs = f_ptr + (C.nlev + 1);
+    int *b_ptr = f_bs + C.nlev;
+    int *b_bs = b_ptr + (C.nlevb + 1);
+    unsigned short *f_rows = reinterpret_cast<unsigned short *>(b_bs + C.nlevb);
+    unsigned short *b_rows = f_rows + C.nloc;
+    unsigned short *f_len = b_rows + C.nloc;
+    unsigned short *b_len = f_len + C.nloc;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + L.bar_off());
+    unsigned char *ring = smem_raw + L.ring_off();
+
+    for (int i = lane; i <= C.nlev; i += 32) f_ptr[i] = C.lev_ptr[i];
+    for (int i = lane; i < C.nlev; i += 32) f_bs[i] = C.f_base[i];
+    for (int i = lane; i <= C.nlevb; i += 32) b_ptr[i] = C.levb_ptr[i];
+    for (int i = lane; i < C.nlevb; i += 32) b_bs[i] = C.b_base[i];
+    for (int i = lane; i < C.nloc; i += 32) {
+        f_rows[i] = C.f_rows16[i];
+        b_rows[i] = C.b_rows16[i];
+        f_len[i] = C.f_len8[i];
+        b_len[i] = C.b_len8[i];
+    }
+    if (lane == 0) {
+        for (int i = 0; i < kRingSlots; ++i) mbar_init(bars + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+
+    const int K = C.nlev + C.nlevb;
+    // slot range [lo, hi) of level k (forward levels, then backward levels)
+    auto range = [&](int k, int &lo, int &hi) {
+        if (k < C.nlev) {
+            lo = f_bs[k];
+            hi = k + 1 < C.nlev ? f_bs[k + 1] : (C.nlevb > 0 ? b_bs[0] : C.ell_total);
+        } else {
+            const int kb = k - C.nlev;
+            lo = b_bs[kb];
+            hi = kb + 1 < C.nlevb ? b_bs[kb + 1] : C.ell_total;
+        }
+    };
+    auto seg_bytes = [&](int ns) { return 32 * ns + 4 * ((ns + 3) & ~3); };
+    // uniform (all lanes) ring bookkeeping; lane 0 issues the copies
+    int issued = 0, head = 0, tail = 0;
+    int offs[kRingSlots];
+#pragma unroll
+    for (int i = 0; i < kRingSlots; ++i) offs[i] = 0;
+    auto try_issue = [&](int consumed) -> bool {
+        if (issued >= K || issued - consumed >= kRingSlots) return false;
+        int lo, hi;
+        range(issued, lo, hi);
+        const int ns = hi - lo;
+        const int bytes = seg_bytes(ns);
+        if (issued == consumed) head = tail = 0;   // ring empty
+        int at = -1;
+        if (head >= tail) {
+            if (head + bytes <= L.ring_bytes) at = head;
+            else if (bytes < tail) at = 0;
+        } else if (head + bytes < tail) {
+            at = head;
+        }
+        if (at < 0) return false;
+        const int slot = issued % kRingSlots;
+#pragma unroll
+        for (int i = 0; i < kRingSlots; ++i)
+            if (i == slot) offs[i] = at;
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const unsigned eb = 4u * (unsigned)((ns + 3) & ~3);
+            mbar_expect_tx(bars + slot, 32u * ns + eb);
+            if (ns > 0) bulk_g2s(ring + at, A + lo, 32u * ns, bars + slot);
+            if (eb > 0) bulk_g2s(ring + at + 32 * ns, C.ecol + lo, eb, bars + slot);
+        }
+        head = at + bytes;
+        ++issued;
+        return true;
+    };
+
+    const long long nx = g.nx, ny = g.ny;
+    for (int l = lane; l < C.nloc; l += 32) {
+        int gx, gy, gz;
+        local_to_global(g, C, o, l, gx, gy, gz);
+        double2 v = r[cell_at(g, gx, gy, zplane(g, gz))];
+        if (VARIANT == 2 && !C.owned[l]) v = make_double2(0.0, 0.0);
+        y[l] = v;
+    }
+    (void)nx;
+    (void)ny;
+    __syncwarp();
+
+    for (int k = 0; k < K; ++k) {
+        while (try_issue(k)) {
+        }
+        const int slot = k % kRingSlots;
+        int at = 0;
+#pragma unroll
+        for (int i = 0; i < kRingSlots; ++i)
+            if (i == slot) at = offs[i];
+        mbar_wait(bars + slot, (unsigned)((k / kRingSlots) & 1));
+        int lo, hi;
+        range(k, lo, hi);
+        const int ns = hi - lo;
+        const double4 *sa = reinterpret_cast<const double4 *>(ring + at);
+        const int *se = reinterpret_cast<const int *>(ring + at + 32 * ns);
+        const bool fwd = k < C.nlev;
+        const int lv = fwd ? k : k - C.nlev;
+        const int r0 = fwd ? f_ptr[lv] : b_ptr[lv];
+        const int m = (fwd ? f_ptr[lv + 1] : b_ptr[lv + 1]) - r0;
+        const unsigned short *rows = fwd ? f_rows : b_rows;
+        const unsigned short *lens = fwd ? f_len : b_len;
+        // lane owns rows lane and lane + 32 of the level (levels <= 64 wide)
+        const int first = fwd ? 0 : 1;            // backward: slot 0 is the inverted diagonal
+        const int len0 = lane < m ? (int)lens[r0 + lane] : 0;
+        const int len1 = lane + 32 < m ? (int)lens[r0 + lane + 32] : 0;
+        const int i0 = lane < m ? rows[r0 + lane] : 0;
+        const int i1 = lane + 32 < m ? rows[r0 + lane + 32] : 0;
+        double2 acc0 = y[i0], acc1 = y[i1];
+        int off = 0;
+        for (int t = 0;; ++t) {
+            const unsigned b0 = __ballot_sync(0xffffffffu, len0 > t), b1 = __ballot_sync(0xffffffffu, len1 > t);
+            if (!(b0 | b1)) break;
+            if (t >= first) {
+                if (t < len0) blk_sub(acc0, sa[off + lane], y[se[off + lane]]);
+                if (t < len1) blk_sub(acc1, sa[off + lane + 32], y[se[off + lane + 32]]);
+            }
+            off += __popc(b0) + __popc(b1);
+        }
+        if (fwd) {
+            if (lane < m) y[i0] = acc0;
+            if (lane + 32 < m) y[i1] = acc1;
+        } else {
+            if (lane < m) {
+                const double4 di = sa[lane];
+                y[i0] = make_double2(di.x * acc0.x + di.y * acc0.y, di.z * acc0.x + di.w * acc0.y);
+            }
+            if (lane + 32 < m) {
+                const double4 di = sa[lane + 32];
+                y[i1] = make_double2(di.x * acc1.x + di.y * acc1.y, di.z * acc1.x + di.w * acc1.y);
+            }
+        }
+        __syncwarp();
+        // level k consumed: the oldest live level is now k + 1
+        if (k + 1 < issued) {
+            const int ns2 = (k + 1) % kRingSlots;
+#pragma unroll
+            for (int i = 0; i < kRingSlots; ++i)
+                if (i == ns2) tail = offs[i];
+        } else {
+            tail = head;
+        }
+    }
+    if (VARIANT == 1) {
+        for (int l = lane; l < C.nloc; l += 32) {
+            if (!C.owned[l]) continue;
+            int gx, gy, gz;
+            local_to_global(g, C, o, l, gx, gy, gz);
+            z[cell_at(g, gx, gy, zplane(g, gz))] = y[l];
         }
     } else {
         for (int l = lane; l < C.nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
@@ -581,7 +810,7 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
             bool ok = true;
             for (int a = 0; a < dim && ok; ++a) {
                 int t = rel[a][ix[a]] + off[q][a];
-                if (g.periodic) t = ((t % nn[a]) + nn[a]) % nn[a];
+                if (g.periodic && !(a == 2 && g.zg > 0)) t = ((t % nn[a]) + nn[a]) % nn[a];
                 auto f = look[a].find(t);
                 if (f == look[a].end()) ok = false;
                 else jl[a] = f->second;
@@ -680,6 +909,7 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
             const int r0 = ptr[lv], m = ptr[lv + 1] - r0;
             std::stable_sort(rows.begin() + r0, rows.begin() + r0 + m, [&](int a, int b) { return rlen(a) > rlen(b); });
             const int w = m > 0 ? rlen(rows[r0]) : 0;
+            slot = (slot + 3) & ~3;     // 16-byte aligned column-id range for the bulk copies
             base[lv] = slot;
             std::vector<int> off(w + 1, 0);
             for (int t = 0; t < w; ++t) {
@@ -702,12 +932,12 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
     };
     layout(C.lev_ptr, C.lev_rows, true, C.f_base, C.f_len, C.f_jptr, C.f_joff, C.max_fwidth);
     layout(C.levb_ptr, C.levb_rows, false, C.b_base, C.b_len, C.b_jptr, C.b_joff, C.max_bwidth);
-    C.ell_total = slot;
+    C.ell_total = ((slot + 3) & ~3) + 4;   // tail padding: bulk copies round up to 4 slots
     C.f_rows16.assign(C.lev_rows.begin(), C.lev_rows.end());
     C.b_rows16.assign(C.levb_rows.begin(), C.levb_rows.end());
     C.f_len8.assign(C.f_len.begin(), C.f_len.end());
     C.b_len8.assign(C.b_len.begin(), C.b_len.end());
-    C.ecol.assign(slot, -1);
+    C.ecol.assign(C.ell_total, -1);
     for (int t = 0; t < C.nnzb; ++t) C.ecol[C.pos[t]] = C.col[t];
     for (auto &j : C.jmap)
         if (j >= 0) j = C.pos[j];
@@ -844,6 +1074,8 @@ struct acch_precond {
     int tps = 32;          // threads per subdomain in the solves
     int max_nloc = 0;
     int warp_mode = 0;     // apply_warp_kernel usable
+    int tma_mode = 0;      // apply_tma_kernel (TMA ring) in use
+    TmaSmem tl{};
     int pf_depth = 8;      // levels prefetched ahead into L2 (ACCH_PREFETCH_DEPTH overrides)
     WarpSmem wl{0, 0, 0};
 };
@@ -872,6 +1104,10 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         acch_set_error("acch_precond_create: invalid argument");
         return ACCH_ERR_INVALID_ARG;
     }
+    if (ctx->g.zg > 0 && (variant != 1 || overlap > ctx->g.zg)) {
+        acch_set_error("acch_precond_create: slab mode supports left-RAS with overlap <= ghost planes");
+        return ACCH_ERR_INVALID_ARG;
+    }
     const GridDev &g = ctx->g;
     const int dim = g.dim;
     const int nn[3] = {g.nx, g.ny, g.nz};
@@ -896,7 +1132,13 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             lo3[a] = (int)lo;
             own_len[a] = (int)(hi - lo);
             std::vector<int> ext;
-            if (g.periodic) {
+            if (a == 2 && g.zg > 0) {
+                // slab mode: z never wraps locally; an overlap past an interior
+                // slab boundary lands in the ghost planes, a physical wall clips
+                const long long zlo = g.zwall_lo ? 0 : -(long long)g.zg, zhi = g.zwall_hi ? nn[a] : nn[a] + g.zg;
+                for (long long c = std::max<long long>(lo - overlap, zlo); c < std::min<long long>(hi + overlap, zhi); ++c)
+                    ext.push_back((int)(c - lo));
+            } else if (g.periodic) {
                 std::vector<int> all;
                 for (long long c = lo - overlap; c < hi + overlap; ++c) all.push_back((int)(((c % nn[a]) + nn[a]) % nn[a]));
                 std::sort(all.begin(), all.end());
@@ -967,11 +1209,29 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         if (const char *e = getenv("ACCH_PREFETCH_DEPTH")) pc->pf_depth = atoi(e);
         if (const char *e = getenv("ACCH_SCHWARZ_BLOCK_SOLVER"))   // testing: force the CTA-wide solver
             if (atoi(e)) pc->warp_mode = 0, pc->tps = 128;
+        // TMA ring: at least two of the largest level segments
+        int max_seg = 0;
+        for (const auto &C : pc->classes) {
+            std::vector<int> bases(C.f_base.begin(), C.f_base.end());
+            bases.insert(bases.end(), C.b_base.begin(), C.b_base.end());
+            bases.push_back(C.ell_total);
+            for (size_t k = 0; k + 1 < bases.size(); ++k) {
+                const int ns = bases[k + 1] - bases[k];
+                max_seg = std::max(max_seg, 32 * ns + 4 * ((ns + 3) & ~3));
+            }
+        }
+        int ring_kb = 32;
+        if (const char *e = getenv("ACCH_RING_KB")) ring_kb = std::max(4, atoi(e));
+        pc->tl = TmaSmem{pc->wl, std::max(ring_kb * 1024, 2 * max_seg + 64)};
+        pc->tl.ring_bytes = (pc->tl.ring_bytes + 15) / 16 * 16;
+        pc->tma_mode = pc->warp_mode && pc->tl.bytes() <= 220 * 1024;
+        if (const char *e = getenv("ACCH_SCHWARZ_TMA"))
+            if (!atoi(e)) pc->tma_mode = 0;
         if (getenv("ACCH_DEBUG"))
             fprintf(stderr, "[acch] precond: %lld subdomains, %zu classes, max_nloc %d, max level width %d, "
                             "max row %d, warp smem %zu B -> %s solver\n",
                     (long long)n_sub, pc->classes.size(), max_nloc, max_width, max_len, pc->wl.bytes(),
-                    pc->warp_mode ? "warp" : "CTA");
+                    pc->tma_mode ? "TMA-ring warp" : (pc->warp_mode ? "warp" : "CTA"));
     }
     const int groups = 128 / pc->tps;
     pc->apply_smem = sizeof(double2) * (size_t)max_nloc * groups;
@@ -1053,6 +1313,13 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<0, 128>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<1, 128>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 128>, attr, b));
+    }
+    if (pc->tma_mode && pc->tl.bytes() > 48 * 1024) {
+        const int b = (int)pc->tl.bytes();
+        const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<0>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<1>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<2>, attr, b));
     }
     if (pc->warp_mode && pc->wl.bytes() > 48 * 1024) {
         const int b = (int)pc->wl.bytes();
@@ -1169,7 +1436,15 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         else if (pc->pf_depth <= 8) WAPPLY_D(V, 8);          \
         else WAPPLY_D(V, 16);                                \
     } while (0)
-    if (pc->warp_mode) {
+#define TAPPLY(V)                                                                                             \
+    apply_tma_kernel<V><<<(unsigned)pc->nsub, 32, pc->tl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,             \
+        pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
+        (double2 *)z, pc->d_ext_out, pc->tl, pc->nsub)
+    if (pc->tma_mode) {
+        if (pc->variant == 1) TAPPLY(1);
+        else if (pc->variant == 0) TAPPLY(0);
+        else TAPPLY(2);
+    } else if (pc->warp_mode) {
         if (pc->variant == 1) WAPPLY(1);
         else if (pc->variant == 0) WAPPLY(0);
         else WAPPLY(2);
@@ -1185,6 +1460,7 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
 #undef APPLY
 #undef WAPPLY
 #undef WAPPLY_D
+#undef TAPPLY
     ACCH_LAUNCHED(ctx);
     if (pc->variant != 1) {
         const long long n = ctx->g.n;
@@ -1201,6 +1477,8 @@ extern "C" acch_status acch_precond_apply(acch_precond *pc, const double *r, dou
         acch_set_error("acch_precond_apply: invalid argument");
         return ACCH_ERR_INVALID_ARG;
     }
+    const acch_status st = comm_halo(pc->ctx, r, 2, 1);
+    if (st != ACCH_OK) return st;
     return precond_apply_impl(pc, r, z);
 }
 

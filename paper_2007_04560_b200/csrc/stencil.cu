@@ -102,7 +102,7 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
     // plane kk of both states (tile + 2 halo) into ring slot kk mod 3, asynchronously
     auto load_plane = [&](int kk) {
         const int slot = (DIM == 3) ? mod3(kk) : 0;
-        const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
+        const int gz = zplane(g, kk);
         for (int i = tid; i < HX * HY; i += NT) {
             const int hx = i % HX, hy = i / HX;
             const int gx = wrap_coord(x0 + hx - 2, nx, g.periodic);
@@ -181,7 +181,7 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
             div += (fp - fm) * ihy;
         }
         if (DIM == 3) {
-            const bool lo = per || k > 0, hi = per || k < nz - 1;
+            const bool lo = zstep_ok(g, k, -1), hi = zstep_ok(g, k, +1);
             const double fp = hi ? 0.5 * (C0 + sCb[sp * GX * GY + gc]) * (sGu[sp * GX * GY + gc] - G0) : 0.0;
             const double fm = lo ? 0.5 * (C0 + sCb[sm * GX * GY + gc]) * (G0 - sGu[sm * GX * GY + gc]) : 0.0;
             div += (fp - fm) * ihz;
@@ -189,7 +189,7 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
         double2 f;
         f.x = (n0.x - o0.x) / dt - div;
         f.y = (n0.y - o0.y) / dt + (C0 / P.rho) * sGv[s0 * GX * GY + gc];
-        F[((long long)k * ny + y) * nx + x] = f;
+        F[cell_at(g, x, y, zplane(g, k))] = f;
         acc_norm += f.x * f.x + f.y * f.y;
         acc_gap = red_combine(acc_gap, cell_gap(n0.x, n0.y), RED_MIN);
     };
@@ -238,18 +238,24 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
 __global__ void jac_prepare_kernel(GridDev g, ParamsDev P, const double2 *__restrict__ xo,
                                    const double2 *__restrict__ xn, double *__restrict__ coef)
 {
-    const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (c >= g.n) return;
-    const int x = (int)(c % g.nx), y = (int)((c / g.nx) % g.ny), z = (int)(c / ((long long)g.nx * g.ny));
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= g.n) return;
+    const int x = (int)(q % g.nx), y = (int)((q / g.nx) % g.ny), z = (int)(q / ((long long)g.nx * g.ny));
+    const long long c = cell_at(g, x, y, zplane(g, z));
     const double2 n0 = xn[c], o0 = xo[c];
     double lun = 0.0, lvn = 0.0, luo = 0.0, lvo = 0.0;
     for (int a = 0; a < g.dim; ++a) {
-        int cm[3] = {x, y, z}, cp[3] = {x, y, z};
-        const int na = a == 0 ? g.nx : (a == 1 ? g.ny : g.nz);
-        cm[a] = wrap_coord(cm[a] - 1, na, g.periodic);
-        cp[a] = wrap_coord(cp[a] + 1, na, g.periodic);
-        const long long im = ((long long)cm[2] * g.ny + cm[1]) * g.nx + cm[0];
-        const long long ip = ((long long)cp[2] * g.ny + cp[1]) * g.nx + cp[0];
+        long long im, ip;
+        if (a == 0) {
+            im = cell_at(g, wrap_coord(x - 1, g.nx, g.periodic), y, zplane(g, z));
+            ip = cell_at(g, wrap_coord(x + 1, g.nx, g.periodic), y, zplane(g, z));
+        } else if (a == 1) {
+            im = cell_at(g, x, wrap_coord(y - 1, g.ny, g.periodic), zplane(g, z));
+            ip = cell_at(g, x, wrap_coord(y + 1, g.ny, g.periodic), zplane(g, z));
+        } else {
+            im = cell_at(g, x, y, zplane(g, z - 1));
+            ip = cell_at(g, x, y, zplane(g, z + 1));
+        }
         const double2 nm = xn[im], np_ = xn[ip], om = xo[im], op = xo[ip];
         lun += (np_.x - 2.0 * n0.x + nm.x) * g.ih2[a];
         lvn += (np_.y - 2.0 * n0.y + nm.y) * g.ih2[a];
@@ -259,7 +265,7 @@ __global__ void jac_prepare_kernel(GridDev g, ParamsDev P, const double2 *__rest
     double phi, psi, dp, dq;
     entropy_chord<true>(n0.x + n0.y, o0.x + o0.y, P, 0, phi, dp);
     entropy_chord<true>(n0.x - n0.y, o0.x - o0.y, P, 0, psi, dq);
-    const long long N = g.n;
+    const long long N = g.nstore;
     coef[CO_S * N + c] = P.theta * (dp + dq);
     coef[CO_D * N + c] = P.theta * (dp - dq);
     coef[CO_CBAR * N + c] = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
@@ -299,7 +305,7 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
     double *sCb = sEt + R * GX * GY;
     double *sGu = sCb + R * GX * GY;
 
-    const long long N = g.n;
+    const long long N = g.nstore;
     const double *__restrict__ cS = coef + CO_S * N;
     const double *__restrict__ cD = coef + CO_D * N;
     const double *__restrict__ cC = coef + CO_CBAR * N;
@@ -319,7 +325,7 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
 
     auto load_plane = [&](int kk) {
         const int slot = (DIM == 3) ? mod3(kk) : 0;
-        const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
+        const int gz = zplane(g, kk);
         for (int i = tid; i < HX * HY; i += NT) {
             const int hx = i % HX, hy = i / HX;
             const int gx = wrap_coord(x0 + hx - 2, nx, g.periodic);
@@ -333,7 +339,7 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
     // plane ahead into registers (latency hidden behind a whole plane)
     double pS[NJ], pD[NJ], pU[NJ], pV[NJ], pC[NJ], pG[NJ];
     auto prefetch_coef = [&](int kk) {
-        const int gz = (DIM == 3) ? wrap_coord(kk, nz, g.periodic) : 0;
+        const int gz = zplane(g, kk);
 #pragma unroll
         for (int j = 0; j < NJ; ++j) {
             const int i = tid + j * NT;
@@ -408,10 +414,10 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
         };
         face(b0 + 1, ihx, per || x > 0, per || x < nx - 1, b0 - 1);
         face(b0 + GX, ihy, per || y > 0, per || y < ny - 1, b0 - GX);
-        if (DIM == 3) face(sp * GX * GY + gc, ihz, per || k > 0, per || k < nz - 1, sm * GX * GY + gc);
+        if (DIM == 3) face(sp * GX * GY + gc, ihz, zstep_ok(g, k, -1), zstep_ok(g, k, +1), sm * GX * GY + gc);
         double lapv = lxy;
         if (DIM == 3) lapv += (wvp - 2.0 * w0.y + wvm) * ihz;
-        const long long c = ((long long)k * ny + y) * nx + x;
+        const long long c = cell_at(g, x, y, zplane(g, k));
         const double S = __ldg(cS + c), D = __ldg(cD + c), Gv = __ldg(cGv + c);
         double2 out;
         out.x = w0.x / dt - d1 - d2;
@@ -514,17 +520,24 @@ __global__ void diagnostics_kernel(GridDev g, ParamsDev P, const double2 *__rest
                                    unsigned int *counter, double *result)
 {
     double e = 0.0, m = 0.0, vmax = -INFINITY;
-    for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < g.n; c += (long long)gridDim.x * blockDim.x) {
-        const int xi = (int)(c % g.nx), yi = (int)((c / g.nx) % g.ny), zi = (int)(c / ((long long)g.nx * g.ny));
-        const double2 s = x[c];
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < g.n; q += (long long)gridDim.x * blockDim.x) {
+        const int xi = (int)(q % g.nx), yi = (int)((q / g.nx) % g.ny), zi = (int)(q / ((long long)g.nx * g.ny));
+        const int zs = zplane(g, zi);
+        const double2 s = x[cell_at(g, xi, yi, zs)];
         double gsu = 0.0, gsv = 0.0;
         for (int a = 0; a < g.dim; ++a) {
-            int cm[3] = {xi, yi, zi}, cp[3] = {xi, yi, zi};
-            const int na = a == 0 ? g.nx : (a == 1 ? g.ny : g.nz);
-            cm[a] = wrap_coord(cm[a] - 1, na, g.periodic);
-            cp[a] = wrap_coord(cp[a] + 1, na, g.periodic);
-            const double2 sm = x[((long long)cm[2] * g.ny + cm[1]) * g.nx + cm[0]];
-            const double2 sp = x[((long long)cp[2] * g.ny + cp[1]) * g.nx + cp[0]];
+            long long im, ip;
+            if (a == 0) {
+                im = cell_at(g, wrap_coord(xi - 1, g.nx, g.periodic), yi, zs);
+                ip = cell_at(g, wrap_coord(xi + 1, g.nx, g.periodic), yi, zs);
+            } else if (a == 1) {
+                im = cell_at(g, xi, wrap_coord(yi - 1, g.ny, g.periodic), zs);
+                ip = cell_at(g, xi, wrap_coord(yi + 1, g.ny, g.periodic), zs);
+            } else {
+                im = cell_at(g, xi, yi, zplane(g, zi - 1));
+                ip = cell_at(g, xi, yi, zplane(g, zi + 1));
+            }
+            const double2 sm = x[im], sp = x[ip];
             const double fu = (sp.x - s.x) * g.ih[a], bu = (s.x - sm.x) * g.ih[a];
             const double fv = (sp.y - s.y) * g.ih[a], bv = (s.y - sm.y) * g.ih[a];
             gsu += 0.5 * (fu * fu + bu * bu);
@@ -725,7 +738,7 @@ acch_status launch_gap(acch_ctx *ctx, const double *x)
 {
     ProfScope prof_scope(ctx, PC_REDUCE, 16.0 * ctx->g.n);
     const long long n = ctx->g.n;
-    gap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, ctx->d_partials, ctx->d_counter,
+    gap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x + ctx->g.zoff, ctx->d_partials, ctx->d_counter,
                                                             ctx->d_result);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
@@ -745,8 +758,9 @@ acch_status launch_trial(acch_ctx *ctx, const double *x, const double *s, double
 {
     ProfScope prof_scope(ctx, PC_REDUCE, 48.0 * ctx->g.n);
     const long long n = ctx->g.n;
-    trial_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, (const double2 *)s, lam,
-                                                              (double2 *)y, ctx->d_partials, ctx->d_counter,
+    trial_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x + ctx->g.zoff,
+                                                              (const double2 *)s + ctx->g.zoff, lam,
+                                                              (double2 *)y + ctx->g.zoff, ctx->d_partials, ctx->d_counter,
                                                               ctx->d_result);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
@@ -756,7 +770,8 @@ acch_status launch_feasible_cap(acch_ctx *ctx, const double *x, const double *s,
 {
     ProfScope prof_scope(ctx, PC_REDUCE, 32.0 * ctx->g.n);
     const long long n = ctx->g.n;
-    feasible_cap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, (const double2 *)s, margin,
+    feasible_cap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x + ctx->g.zoff,
+                                                                     (const double2 *)s + ctx->g.zoff, margin,
                                                                      ctx->d_partials, ctx->d_counter, ctx->d_result);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;

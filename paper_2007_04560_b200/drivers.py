@@ -122,8 +122,16 @@ def initial_fields(config: RunConfig):
 
 
 def build_initial_state(config: RunConfig, device=None) -> State:
+    grid = config.grid
+    if getattr(grid, "nz_global", 0):
+        # a slab: draw the global fields (bitwise the reference's inputs) and keep this rank's planes
+        from .slab import local_fields
+        from dataclasses import replace as _replace
+        u, v = initial_fields(_replace(config, grid=grid.global_grid()))
+        u, v = local_fields(grid, u, v)
+        return State.from_interior(grid, np.ascontiguousarray(u), np.ascontiguousarray(v), device=device)
     u, v = initial_fields(config)
-    return State.from_interior(config.grid, u, v, device=device)
+    return State.from_interior(grid, u, v, device=device)
 
 
 @dataclass
@@ -168,6 +176,8 @@ class Stepper:
         n_sub = config.solver.subdomains or threads
         self.decomposition = partition(self.grid, n_sub, config.solver.overlap)
         self.newton_cfg = config.make_newton_config()
+        from . import _native
+        self.ctx = _native.context_for(self.grid, config.params, state.device)
         self.precond = SchwarzPreconditioner(self.decomposition, config.solver.preconditioner,
                                              config.solver.subdomain_solver)
         self.t = 0.0
@@ -187,7 +197,7 @@ class Stepper:
         if self.step == 1 or self.x_prev is None:
             dt = ctl.initial_dt()
         else:
-            dt = ctl.predict_dt(self.x_now, self.x_prev, self.dt_prev)
+            dt = ctl.predict_dt(self.x_now, self.x_prev, self.dt_prev, ctx=self.ctx)
         if self.since >= self.refreeze_every:
             self.precond.invalidate()
             self.since = 0

@@ -66,6 +66,11 @@ class Grid:
         return int(np.prod(self.counts))
 
     @property
+    def n_store(self) -> int:
+        """Cells stored per field on this device (a slab adds ghost planes)."""
+        return self.n_cells
+
+    @property
     def array_shape(self) -> tuple:
         """Interior array shape, axis order reversed (x fastest)."""
         return tuple(reversed(self.counts))

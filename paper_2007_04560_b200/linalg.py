@@ -107,6 +107,8 @@ def partition(grid: Grid, n_subdomains: int, overlap: int) -> Decomposition:
         raise PartitionError("need at least one subdomain")
     if overlap < 0:
         raise PartitionError("overlap must be nonnegative")
+    if getattr(grid, "nz_global", 0):
+        return _slab_partition(grid, n_subdomains, overlap)
     best = None
     for f in _factor_tuples(int(n_subdomains), grid.dim):
         if any(f[a] > grid.counts[a] for a in range(grid.dim)):
@@ -133,6 +135,24 @@ def partition(grid: Grid, n_subdomains: int, overlap: int) -> Decomposition:
             lo[s, a] = bounds[a][0][idx[a]]
             hi[s, a] = bounds[a][1][idx[a]]
     return Decomposition(grid, int(n_subdomains), int(overlap), tuple(factors), lo, hi)
+
+
+def _slab_partition(slab, n_subdomains: int, overlap: int) -> Decomposition:
+    """The global partition's boxes that lie in this rank's z-slab, in local
+    z coordinates (box order kept).  Slab boundaries must fall on box
+    boundaries, so every global box belongs to exactly one rank."""
+    glob = partition(slab.global_grid(), n_subdomains, overlap)
+    z0, z1 = slab.z0, slab.z0 + slab.counts[2]
+    zl, zh = glob.owned_lo[:, 2], glob.owned_hi[:, 2]
+    inside = (zl >= z0) & (zh <= z1)
+    straddle = (zl < z1) & (zh > z0) & ~inside
+    if straddle.any():
+        raise PartitionError(f"box z-ranges do not align with the slab [{z0}, {z1}) of rank {slab.rank}")
+    lo = glob.owned_lo[inside].copy()
+    hi = glob.owned_hi[inside].copy()
+    lo[:, 2] -= z0
+    hi[:, 2] -= z0
+    return Decomposition(slab, int(inside.sum()), int(overlap), glob.factors, lo, hi)
 
 
 # ---------------------------------------------------------------------------
@@ -300,7 +320,7 @@ def gmres(matvec, b, precond=None, rel_tol: float = 1e-8, abs_tol: float = 1e-14
         raise TypeError("precond must be a SchwarzPreconditioner or None")
     if precond is not None and precond.handle is None:
         raise RuntimeError("preconditioner has no factorization; call update() first")
-    b = nat.dev_f64(b, 2 * op.n_cells, "b")
+    b = nat.dev_f64(b, 2 * op.n_store, "b")
     x = torch.empty_like(b)
     its, conv, rn = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
     nat.check(nat.lib().acch_gmres(op.ctx.bind(), nat.ptr(op.coef), op.dt,

@@ -75,9 +75,9 @@ class State:
     layout (scheme.py:58-66) so that ``x.view(-1)`` *is* the packed vector."""
 
     def __init__(self, grid: Grid, x: torch.Tensor):
-        x = nat.dev_f64(x, 2 * grid.n_cells, "state")
+        x = nat.dev_f64(x, 2 * grid.n_store, "state")
         self.grid = grid
-        self.x = x.view(grid.n_cells, 2)
+        self.x = x.view(grid.n_store, 2)
 
     @classmethod
     def from_interior(cls, grid: Grid, u, v, device=None) -> "State":
@@ -88,15 +88,20 @@ class State:
             v = np.asarray(v, dtype=float)
             if u.shape != grid.array_shape or v.shape != grid.array_shape:
                 raise ValueError(f"interior shape {u.shape} does not match grid {grid.array_shape}")
-            host = np.empty((grid.n_cells, 2))
-            host[:, 0] = u.ravel()
-            host[:, 1] = v.ravel()
+            host = np.zeros((grid.n_store, 2))
+            z0 = getattr(grid, "zoff", 0)
+            host[z0:z0 + grid.n_cells, 0] = u.ravel()
+            host[z0:z0 + grid.n_cells, 1] = v.ravel()
             return cls(grid, torch.from_numpy(host).to(device))
         ut = _as_device(u, device).reshape(-1)
         vt = _as_device(v, device).reshape(-1)
         if ut.numel() != grid.n_cells or vt.numel() != grid.n_cells:
             raise ValueError("interior shape does not match grid")
-        return cls(grid, torch.stack([ut, vt], dim=1).contiguous())
+        x = torch.zeros((grid.n_store, 2), dtype=torch.float64, device=device)
+        z0 = getattr(grid, "zoff", 0)
+        x[z0:z0 + grid.n_cells, 0] = ut
+        x[z0:z0 + grid.n_cells, 1] = vt
+        return cls(grid, x)
 
     @property
     def device(self):
@@ -107,13 +112,17 @@ class State:
         """The packed 2N solver vector (a view, not a copy)."""
         return self.x.view(-1)
 
+    def _interior(self):
+        z0 = getattr(self.grid, "zoff", 0)
+        return self.x[z0:z0 + self.grid.n_cells]
+
     @property
     def u(self) -> Field:
-        return Field(self.grid, self.x[:, 0].view(self.grid.array_shape))
+        return Field(self.grid, self._interior()[:, 0].view(self.grid.array_shape))
 
     @property
     def v(self) -> Field:
-        return Field(self.grid, self.x[:, 1].view(self.grid.array_shape))
+        return Field(self.grid, self._interior()[:, 1].view(self.grid.array_shape))
 
     def copy(self) -> "State":
         return State(self.grid, self.x.clone())
@@ -123,7 +132,7 @@ class State:
         return self
 
     def to_numpy(self):
-        h = self.x.detach().cpu().numpy()
+        h = self._interior().detach().cpu().numpy()
         return h[:, 0].reshape(self.grid.array_shape).copy(), h[:, 1].reshape(self.grid.array_shape).copy()
 
 

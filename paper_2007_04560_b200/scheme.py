@@ -40,7 +40,9 @@ def pack_fields(u, v) -> torch.Tensor:
 
 def unpack_vector(grid: Grid, x: torch.Tensor):
     """Views of the u and v components of a packed vector."""
-    x2 = x.view(grid.n_cells, 2)
+    x2 = x.view(grid.n_store, 2)
+    z0 = getattr(grid, "zoff", 0)
+    x2 = x2[z0:z0 + grid.n_cells]
     return x2[:, 0].view(grid.array_shape), x2[:, 1].view(grid.array_shape)
 
 
@@ -109,7 +111,7 @@ class StepProblem:
 def _vec(state_or_vec, grid: Grid) -> torch.Tensor:
     if isinstance(state_or_vec, State):
         return state_or_vec.vector
-    return nat.dev_f64(state_or_vec, 2 * grid.n_cells, "vector")
+    return nat.dev_f64(state_or_vec, 2 * grid.n_store, "vector")
 
 
 def residual_vector(prob: StepProblem, new) -> torch.Tensor:
@@ -137,6 +139,7 @@ class JacobianOperator:
         self.coef = coef
         self.dt = prob.dt
         self.n_cells = prob.grid.n_cells
+        self.n_store = prob.grid.n_store
 
     @property
     def shape(self):
@@ -153,7 +156,7 @@ class JacobianOperator:
 
     def matvec(self, w) -> torch.Tensor:
         w = nat.dev_f64(w if isinstance(w, torch.Tensor) else torch.as_tensor(w, device=self.coef.device),
-                        2 * self.n_cells, "w")
+                        2 * self.n_store, "w")
         return self.matvec_into(w, torch.empty_like(w))
 
     __call__ = matvec
@@ -215,7 +218,7 @@ def stencil_offsets(dim: int):
 def assemble_jacobian(prob: StepProblem, new) -> JacobianOperator:
     """Jacobian of the step residual at ``new`` (scheme.py:427-484)."""
     x = _vec(new, prob.grid)
-    coef = torch.empty(N_COEF * prob.grid.n_cells, dtype=torch.float64, device=x.device)
+    coef = torch.empty(N_COEF * prob.grid.n_store, dtype=torch.float64, device=x.device)
     gap = ctypes.c_double()
     nat.check(nat.lib().acch_admissibility_gap(prob.ctx.bind(), nat.ptr(x), ctypes.byref(gap)), "gap")
     if not gap.value >= ADMISSIBILITY_MARGIN:

@@ -287,13 +287,15 @@ def test_simulate_adaptive_3d_neumann_with_retries_matches_reference():
     _check_sim(*_run_sim("c3small"))
 
 
-@pytest.mark.parametrize("block_solver", ["0", "1"])
+@pytest.mark.parametrize("mode", ["tma", "warp", "cta"])
 @pytest.mark.parametrize("solver", ["ilu0", "ilu1"])
-def test_schwarz_wide_boxes_match_oracle(block_solver, solver, monkeypatch):
-    """Boxes whose levels are wider than a warp (and the CTA-wide solver
-    forced on small boxes) against the oracle's scalar ILU on kron(P, 1)."""
+def test_schwarz_wide_boxes_match_oracle(mode, solver, monkeypatch):
+    """Boxes whose levels are wider than a warp, with each of the three
+    subdomain solvers (TMA-ring warp, plain warp, CTA-wide) forced, against
+    the oracle's scalar ILU on kron(P, 1)."""
     from oracle import acch_oracle as O
-    monkeypatch.setenv("ACCH_SCHWARZ_BLOCK_SOLVER", block_solver)
+    monkeypatch.setenv("ACCH_SCHWARZ_BLOCK_SOLVER", "1" if mode == "cta" else "0")
+    monkeypatch.setenv("ACCH_SCHWARZ_TMA", "1" if mode == "tma" else "0")
     rng = np.random.default_rng(77)
     counts = (16, 14, 12)
     g = Grid(counts, (1.0, 1.0, 1.0), BoundaryCondition.NEUMANN)
