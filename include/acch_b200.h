@@ -162,6 +162,9 @@ typedef struct {
     int32_t nranks, rank;
     int32_t ghost_planes;       /* 0 (whole grid) or 2 */
     int32_t wall_lo, wall_hi;
+    int32_t z_offset;           /* first global plane of this slab */
+    int32_t nz_global;          /* global plane count (RAS boxes keep the
+                                   reference's sorted-global-id cell order) */
 } acch_slab_desc;
 
 /* op: 0 sum, 1 min, 2 max over ranks, in place on n host doubles. */

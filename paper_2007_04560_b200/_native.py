@@ -40,7 +40,8 @@ class ParamsDesc(ctypes.Structure):
 
 class SlabDesc(ctypes.Structure):
     _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("ghost_planes", ctypes.c_int32),
-                ("wall_lo", ctypes.c_int32), ("wall_hi", ctypes.c_int32)]
+                ("wall_lo", ctypes.c_int32), ("wall_hi", ctypes.c_int32), ("z_offset", ctypes.c_int32),
+                ("nz_global", ctypes.c_int32)]
 
 
 ALLREDUCE_FN = ctypes.CFUNCTYPE(ctypes.c_int32, ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.c_int32,
@@ -191,7 +192,8 @@ class Context:
         if getattr(grid, "nz_global", 0):
             # a z-slab of a decomposed grid: ghost planes + cross-rank hooks
             from .slab import comm_for
-            sd = SlabDesc(grid.nranks, grid.rank, grid.ghost, int(grid.wall_lo), int(grid.wall_hi))
+            sd = SlabDesc(grid.nranks, grid.rank, grid.ghost, int(grid.wall_lo), int(grid.wall_hi), grid.z0,
+                          grid.nz_global)
             check(self._lib.acch_ctx_set_slab(h, ctypes.byref(sd)), "acch_ctx_set_slab")
             comm = comm_for(grid)
             if comm is None:

@@ -89,6 +89,7 @@ struct acch_ctx {
     // slab decomposition: rank topology and the host hooks that move ghost
     // planes and combine per-rank partial reductions (acch_set_comm)
     int nranks = 1, rank = 0;
+    int z_offset = 0, nz_global = 0;     // slab position in the global grid
     acch_allreduce_cb allreduce = nullptr;
     acch_halo_cb halo = nullptr;
     void *comm_user = nullptr;

@@ -183,8 +183,8 @@ acch_status acch_ctx_create(const acch_grid_desc *grid, const acch_params *param
     const size_t partial_cap = (size_t)1 << 21;
     cudaError_t e;
     if ((e = cudaMalloc(&ctx->d_partials, sizeof(double) * partial_cap)) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->d_counter, sizeof(unsigned int))) != cudaSuccess ||
-        (e = cudaMemset(ctx->d_counter, 0, sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_counter, 16 * sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMemset(ctx->d_counter, 0, 16 * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_result, sizeof(double) * 64)) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_h, sizeof(double) * 128)) != cudaSuccess ||
         (e = cudaMallocHost(&ctx->h_result, sizeof(double) * 128)) != cudaSuccess) {
@@ -230,6 +230,8 @@ acch_status acch_ctx_set_slab(acch_ctx *ctx, const acch_slab_desc *slab)
     GridDev &g = ctx->g;
     ctx->nranks = slab->nranks;
     ctx->rank = slab->rank;
+    ctx->z_offset = slab->z_offset;
+    ctx->nz_global = slab->nz_global > 0 ? slab->nz_global : g.nz;
     g.zg = slab->ghost_planes;
     if (g.zg == 0) {
         g.zwall_lo = g.zwall_hi = g.periodic ? 0 : 1;

@@ -51,13 +51,50 @@ mdot_kernel(const double *__restrict__ V, long long ld, int m, const double *__r
     reduce_finish<NS>(acc, ops, partials, counter, result);
 }
 
+// Multi-dot in groups of MG basis vectors (blockIdx.y = group): every thread
+// keeps MG + 1 accumulators, so occupancy does not collapse for long bases;
+// w is re-read per group (mostly from L2).  Result layout:
+// out[g * (MG + 1) + s] = <V_{g MG + s}, w>, out[MG] = <w, w>.
+constexpr int MG = 8;
+
+__global__ void __launch_bounds__(kRedThreads)
+mdot_grouped_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ w, long long n,
+                    double *partials, unsigned int *counters, double *result)
+{
+    const int g = blockIdx.y;
+    const int v0 = g * MG;
+    double acc[MG + 1];
+#pragma unroll
+    for (int s = 0; s <= MG; ++s) acc[s] = 0.0;
+    const long long n2 = n >> 1;
+    const double2 *__restrict__ w2 = reinterpret_cast<const double2 *>(w);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        const double2 wi = w2[i];
+#pragma unroll
+        for (int s = 0; s < MG; ++s)
+            if (v0 + s < m) {
+                const double2 v = reinterpret_cast<const double2 *>(V + (v0 + s) * ld)[i];
+                acc[s] += v.x * wi.x + v.y * wi.y;
+            }
+        if (g == 0) acc[MG] += wi.x * wi.x + wi.y * wi.y;
+    }
+    int ops[MG + 1];
+#pragma unroll
+    for (int s = 0; s <= MG; ++s) ops[s] = RED_SUM;
+    reduce_finish_x<MG + 1>(acc, ops, partials + (long long)g * (MG + 1) * gridDim.x, counters + 1 + g,
+                            result + g * (MG + 1));
+}
+
+// index of basis vector s's dot in the grouped layout
+__host__ __device__ __forceinline__ int gslot(int s) { return (s / MG) * (MG + 1) + s % MG; }
+
 template <int NS>
 __global__ void __launch_bounds__(kRedThreads)
 mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ h, double *__restrict__ w,
                long long n, double *partials, unsigned int *counter, double *result)
 {
     __shared__ double sh[NS];
-    if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[threadIdx.x] : 0.0;
+    if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[gslot(threadIdx.x)] : 0.0;
     __syncthreads();
     double acc = 0.0;
     const long long n2 = n >> 1;
@@ -145,21 +182,19 @@ int rgrid(long long n) { return vgrid(n); }
 
 }  // namespace
 
-// out[0..m-1] = <V_q, w>, out[*ns - 1] = <w, w> (device)
+// out[gslot(q)] = <V_q, w> (q < m), out[*ns - 1] = out[MG] = <w, w> (device)
 static acch_status mdot_to(acch_ctx *ctx, const double *V, long long ld, int m, const double *w, long long n,
                            double *out, int *ns)
 {
     ProfScope prof_scope(ctx, PC_KDOT, 8.0 * (m + 1) * n);
-    const int G = rgrid(n);
-#define MDOT_CASE(NS)                                                                                            \
-    mdot_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, w, n, ctx->d_partials, ctx->d_counter, out); \
-    *ns = NS;
-    if (m + 1 <= 4) { MDOT_CASE(4) }
-    else if (m + 1 <= 8) { MDOT_CASE(8) }
-    else if (m + 1 <= 16) { MDOT_CASE(16) }
-    else if (m + 1 <= 33) { MDOT_CASE(33) }
-    else { acch_set_error("mdot: too many vectors (restart > 32)"); return ACCH_ERR_INVALID_ARG; }
-#undef MDOT_CASE
+    if (m > 4 * MG) {
+        acch_set_error("mdot: too many vectors (restart > 32)");
+        return ACCH_ERR_INVALID_ARG;
+    }
+    const int groups = (m + MG - 1) / MG;
+    const dim3 grid(rgrid(n), groups);
+    mdot_grouped_kernel<<<grid, kRedThreads, 0, ctx->stream>>>(V, ld, m, w, n, ctx->d_partials, ctx->d_counter, out);
+    *ns = MG + 1;
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
 }
@@ -337,7 +372,7 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                 int ns = 0;
                 TRY(mdot_to(ctx, V + off, nv, j + 1, w + off, ni, dh, &ns));
                 if (multi) {
-                    TRY(reduce_dots(tmp, dh, ns, true));
+                    TRY(reduce_dots(tmp, dh, 4 * (MG + 1), true));
                     TRY(mupdate_to(ctx, V + off, nv, j + 1, dh, w + off, ni, dh + 40));
                     double t40;
                     TRY(reduce_dots(&t40, dh + 40, 1, false));
@@ -346,13 +381,13 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                     TRY(mupdate_to(ctx, V + off, nv, j + 1, dh, w + off, ni, dh + 40));
                     TRY(fetch(ctx, tmp, dh, 41));
                 }
-                for (int i = 0; i <= j; ++i) h(i, j) = tmp[i];
+                for (int i = 0; i <= j; ++i) h(i, j) = tmp[gslot(i)];
                 norm_before = sqrt(tmp[ns - 1]);
                 norm_after = sqrt(tmp[40]);
                 if (norm_after < 0.5 * norm_before) {
                     TRY(mdot_to(ctx, V + off, nv, j + 1, w + off, ni, dh, &ns));
                     double t2[64];
-                    if (multi) TRY(reduce_dots(t2, dh, ns, true));
+                    if (multi) TRY(reduce_dots(t2, dh, 4 * (MG + 1), true));
                     TRY(mupdate_to(ctx, V + off, nv, j + 1, dh, w + off, ni, dh + 40));
                     if (multi) {
                         double t40;
@@ -361,7 +396,7 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                     } else {
                         TRY(fetch(ctx, t2, dh, 41));
                     }
-                    for (int i = 0; i <= j; ++i) h(i, j) += t2[i];
+                    for (int i = 0; i <= j; ++i) h(i, j) += t2[gslot(i)];
                     norm_after = sqrt(t2[40]);
                 }
             } else {

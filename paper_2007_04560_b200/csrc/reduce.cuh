@@ -94,3 +94,42 @@ __device__ __forceinline__ void reduce_finish(double (&v)[NS], const int (&ops)[
         *counter = 0u;
     }
 }
+
+// Finish over blockIdx.x only: blocks with the same (blockIdx.y, blockIdx.z)
+// form one independent reduction; the caller offsets partials / counter /
+// result per group.
+template <int NS>
+__device__ __forceinline__ void reduce_finish_x(double (&v)[NS], const int (&ops)[NS], double *partials,
+                                                unsigned int *counter, double *result)
+{
+    __shared__ double smem[32 * NS];
+    __shared__ bool is_last;
+    const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+    const int nthreads = blockDim.x * blockDim.y * blockDim.z;
+    const long long nb = gridDim.x;
+    const long long bid = blockIdx.x;
+    block_reduce<NS>(v, ops, smem);
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) partials[s * nb + bid] = v[s];
+        __threadfence();
+        unsigned int t = atomicAdd(counter, 1u);
+        is_last = (t == (unsigned int)(nb - 1));
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    double w[NS];
+#pragma unroll
+    for (int s = 0; s < NS; ++s) w[s] = red_identity(ops[s]);
+    for (long long b = tid; b < nb; b += nthreads) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) w[s] = red_combine(w[s], __ldcg(partials + s * nb + b), ops[s]);
+    }
+    block_reduce<NS>(w, ops, smem);
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) result[s] = w[s];
+        *counter = 0u;
+    }
+}

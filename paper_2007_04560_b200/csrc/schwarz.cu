@@ -555,7 +555,7 @@ struct TmaSmem {
     __host__ __device__ size_t bytes() const { return ring_off() + (size_t)ring_bytes; }
 };
 
-template <int VARIANT>
+template <int VARIANT, int MAXW = 12>
 __global__ void __launch_bounds__(32)
 apply_tma_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
                  const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
@@ -679,21 +679,52 @@ apply_tma_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__r
         const int m = (fwd ? f_ptr[lv + 1] : b_ptr[lv + 1]) - r0;
         const unsigned short *rows = fwd ? f_rows : b_rows;
         const unsigned short *lens = fwd ? f_len : b_len;
-        // lane owns rows lane and lane + 32 of the level (levels <= 64 wide)
+        // lane owns rows lane and lane + 32 of the level (levels <= 64 wide).
+        // Slot offsets first (ballots only read the row lengths), then every
+        // shared-memory load of the row, then the FMA chain: ILP, not a
+        // load-use chain per slot.
         const int first = fwd ? 0 : 1;            // backward: slot 0 is the inverted diagonal
-        const int len0 = lane < m ? (int)lens[r0 + lane] : 0;
-        const int len1 = lane + 32 < m ? (int)lens[r0 + lane + 32] : 0;
+        const int len0 = lane < m ? (int)lens[r0 + lane] - first : 0;
+        const int len1 = lane + 32 < m ? (int)lens[r0 + lane + 32] - first : 0;
         const int i0 = lane < m ? rows[r0 + lane] : 0;
         const int i1 = lane + 32 < m ? rows[r0 + lane + 32] : 0;
+        int offs[MAXW];
+        int off = fwd ? 0 : m;
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t) {
+            offs[t] = off;
+            off += __popc(__ballot_sync(0xffffffffu, len0 > t)) + __popc(__ballot_sync(0xffffffffu, len1 > t));
+        }
         double2 acc0 = y[i0], acc1 = y[i1];
-        int off = 0;
-        for (int t = 0;; ++t) {
+        {
+            double4 a[MAXW];
+            int c[MAXW];
+#pragma unroll
+            for (int t = 0; t < MAXW; ++t)
+                if (t < len0) {
+                    a[t] = sa[offs[t] + lane];
+                    c[t] = se[offs[t] + lane];
+                }
+#pragma unroll
+            for (int t = 0; t < MAXW; ++t)
+                if (t < len0) blk_sub(acc0, a[t], y[c[t]]);
+            if (len1 > 0) {
+#pragma unroll
+                for (int t = 0; t < MAXW; ++t)
+                    if (t < len1) {
+                        a[t] = sa[offs[t] + lane + 32];
+                        c[t] = se[offs[t] + lane + 32];
+                    }
+#pragma unroll
+                for (int t = 0; t < MAXW; ++t)
+                    if (t < len1) blk_sub(acc1, a[t], y[c[t]]);
+            }
+        }
+        for (int t = MAXW;; ++t) {   // rows longer than MAXW slots (wrapped boxes, fill-in)
             const unsigned b0 = __ballot_sync(0xffffffffu, len0 > t), b1 = __ballot_sync(0xffffffffu, len1 > t);
             if (!(b0 | b1)) break;
-            if (t >= first) {
-                if (t < len0) blk_sub(acc0, sa[off + lane], y[se[off + lane]]);
-                if (t < len1) blk_sub(acc1, sa[off + lane + 32], y[se[off + lane + 32]]);
-            }
+            if (t < len0) blk_sub(acc0, sa[off + lane], y[se[off + lane]]);
+            if (t < len1) blk_sub(acc1, sa[off + lane + 32], y[se[off + lane + 32]]);
             off += __popc(b0) + __popc(b1);
         }
         if (fwd) {
@@ -1136,8 +1167,16 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
                 // slab mode: z never wraps locally; an overlap past an interior
                 // slab boundary lands in the ghost planes, a physical wall clips
                 const long long zlo = g.zwall_lo ? 0 : -(long long)g.zg, zhi = g.zwall_hi ? nn[a] : nn[a] + g.zg;
+                std::vector<long long> cs;
                 for (long long c = std::max<long long>(lo - overlap, zlo); c < std::min<long long>(hi + overlap, zhi); ++c)
-                    ext.push_back((int)(c - lo));
+                    cs.push_back(c);
+                // the reference orders a box's cells by sorted GLOBAL id: a ghost
+                // plane that wraps around the periodic z axis sorts to the other end
+                const long long ng = ctx->nz_global, z0 = ctx->z_offset;
+                std::stable_sort(cs.begin(), cs.end(), [&](long long a, long long b) {
+                    return ((z0 + a) % ng + ng) % ng < ((z0 + b) % ng + ng) % ng;
+                });
+                for (long long c : cs) ext.push_back((int)(c - lo));
             } else if (g.periodic) {
                 std::vector<int> all;
                 for (long long c = lo - overlap; c < hi + overlap; ++c) all.push_back((int)(((c % nn[a]) + nn[a]) % nn[a]));
@@ -1222,11 +1261,14 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         }
         int ring_kb = 32;
         if (const char *e = getenv("ACCH_RING_KB")) ring_kb = std::max(4, atoi(e));
-        pc->tl = TmaSmem{pc->wl, std::max(ring_kb * 1024, 2 * max_seg + 64)};
+        pc->tl = TmaSmem{pc->wl, std::max(ring_kb * 1024, max_seg + 64)};
         pc->tl.ring_bytes = (pc->tl.ring_bytes + 15) / 16 * 16;
-        pc->tma_mode = pc->warp_mode && pc->tl.bytes() <= 220 * 1024;
+        // opt-in (ACCH_SCHWARZ_TMA=1): at 3-5 warps per SM the ring solver is
+        // latency-bound on its per-level compute and measured slower than the
+        // register-prefetch warp solver (profiles/r01_apply_variants.txt)
+        pc->tma_mode = 0;
         if (const char *e = getenv("ACCH_SCHWARZ_TMA"))
-            if (!atoi(e)) pc->tma_mode = 0;
+            if (atoi(e)) pc->tma_mode = pc->warp_mode && pc->tl.bytes() <= 220 * 1024;
         if (getenv("ACCH_DEBUG"))
             fprintf(stderr, "[acch] precond: %lld subdomains, %zu classes, max_nloc %d, max level width %d, "
                             "max row %d, warp smem %zu B -> %s solver\n",

@@ -190,6 +190,26 @@ class Stepper:
         self.factorizations = 0
         self.events = []
 
+    def snapshot(self) -> dict:
+        """Everything the next steps depend on (state, predictor history,
+        controller gains and counters), so a run can be replayed exactly."""
+        ctl = self.controller
+        return {"x": self.state.x.clone(), "x_prev": None if self.x_prev is None else self.x_prev.clone(),
+                "t": self.t, "step": self.step, "dt_prev": self.dt_prev, "since": self.since, "eta": ctl.eta,
+                "stalled": ctl._stalled_retries, "div": ctl.divergence_count, "events": len(self.events),
+                "fact": self.factorizations}
+
+    def restore(self, snap: dict) -> None:
+        ctl = self.controller
+        self.state = State(self.grid, snap["x"].clone())
+        self.x_now = self.state.vector
+        self.x_prev = None if snap["x_prev"] is None else snap["x_prev"].clone()
+        self.t, self.step, self.dt_prev, self.since = snap["t"], snap["step"], snap["dt_prev"], snap["since"]
+        ctl.eta, ctl._stalled_retries, ctl.divergence_count = snap["eta"], snap["stalled"], snap["div"]
+        del self.events[snap["events"]:]
+        self.factorizations = snap["fact"]
+        self.precond.invalidate()
+
     def advance(self):
         """One accepted step; returns (dt, newton iterations, gmres iterations)."""
         self.step += 1
