@@ -1,6 +1,8 @@
 // C ABI entry points of libacch_b200.so (include/acch_b200.h).
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <string>
 
@@ -191,6 +193,7 @@ acch_status acch_ctx_create(const acch_grid_desc *grid, const acch_params *param
         acch_ctx_destroy(ctx);
         return acch_cuda_fail(e, "acch_ctx_create allocation");
     }
+    if (const char *e = getenv("ACCH_MATVEC")) ctx->matvec_mode = strcmp(e, "twopass") == 0 ? 1 : 0;
     *out = ctx;
     return ACCH_OK;
 }
@@ -205,6 +208,7 @@ acch_status acch_ctx_destroy(acch_ctx *ctx)
     cudaFree(ctx->d_h);
     cudaFree(ctx->d_krylov);
     cudaFree(ctx->d_work);
+    cudaFree(ctx->d_mvtmp);
     if (ctx->h_result) cudaFreeHost(ctx->h_result);
     delete ctx;
     return ACCH_OK;

@@ -1363,6 +1363,28 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<1>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<2>, attr, b));
     }
+    {
+        // the solvers live on shared memory: ask for the full L1/shared carveout
+        const auto co = cudaFuncAttributePreferredSharedMemoryCarveout;
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 4>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 4>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 8>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 8>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 8>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 16>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<0>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<1>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<2>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<0, 32>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<1, 32>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 32>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<0, 128>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<1, 128>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 128>, co, 100));
+    }
     if (pc->warp_mode && pc->wl.bytes() > 48 * 1024) {
         const int b = (int)pc->wl.bytes();
         const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;

@@ -24,7 +24,7 @@
 namespace {
 
 constexpr int RTX = 32, RTY = 8;     // residual tile
-constexpr int MTX = 32, MTY = 8;     // matvec tile
+constexpr int MTX = 32, MTY = 8, MRPT = 1;    // matvec tile (rows per thread)
 constexpr int ZCHUNK = 32;           // z planes per block (3D)
 
 __host__ __device__ constexpr int ring_depth(int dim) { return dim == 3 ? 3 : 1; }
@@ -290,13 +290,13 @@ struct MatvecSmem {
     static constexpr size_t bytes = sizeof(double2) * R * HX * HY + 4 * sizeof(double) * R * GX * GY;
 };
 
-template <int DIM, int TX, int TY>
-__global__ void __launch_bounds__(TX *TY)
+template <int DIM, int TX, int TY, int RPT>
+__global__ void __launch_bounds__(TX *(TY / RPT))
 matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
               const double2 *__restrict__ w_g, double2 *__restrict__ yout)
 {
     using L = MatvecSmem<DIM, TX, TY>;
-    constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, NT = TX * TY;
+    constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, TB = TY / RPT, NT = TX * TB;
     constexpr int NJ = (GX * GY + NT - 1) / NT;   // tile+1-halo cells per thread
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *sw = reinterpret_cast<double2 *>(smem_raw);
@@ -381,21 +381,28 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
         }
     };
 
-    const int x = x0 + tx, y = y0 + ty;
-    const bool active = x < nx && y < ny;
-    const int gc = (ty + 1) * GX + (tx + 1);
-    const int hc = (ty + 2) * HX + (tx + 2);
+    // each thread owns RPT output rows of the tile: ty, ty + TB, ...
+    const int x = x0 + tx;
+    int yr[RPT], gcr[RPT], hcr[RPT];
+    bool act[RPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        yr[r] = y0 + ty + r * TB;
+        act[r] = x < nx && yr[r] < ny;
+        gcr[r] = (ty + r * TB + 1) * GX + (tx + 1);
+        hcr[r] = (ty + r * TB + 2) * HX + (tx + 2);
+    }
 
     // xy part of lap(w_v) at the thread's own cell of plane k (read before the
     // ring slot of plane k is recycled for plane k + 3)
-    auto lapv_xy = [&](int k) {
+    auto lapv_xy = [&](int k, int hc) {
         const double2 *w = sw + ((DIM == 3) ? mod3(k) : 0) * HX * HY;
         const double c = w[hc].y;
         return (w[hc + 1].y - 2.0 * c + w[hc - 1].y) * ihx + (w[hc + HX].y - 2.0 * c + w[hc - HX].y) * ihy;
     };
 
     // y at plane k: w(k) centre, xy lap(w_v), w_v(k -/+ 1) centres passed in
-    auto output = [&](int k, const double2 &w0, double lxy, double wvm, double wvp) {
+    auto output = [&](int k, int y, int gc, const double2 &w0, double lxy, double wvm, double wvp) {
         const int s0 = (DIM == 3) ? mod3(k) : 0;
         const int sm = (DIM == 3) ? mod3(k - 1) : 0;
         const int sp = (DIM == 3) ? mod3(k + 1) : 0;
@@ -432,7 +439,9 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
         __syncthreads();
         compute_dg(0);
         __syncthreads();
-        if (active) output(0, sw[hc], lapv_xy(0), 0.0, 0.0);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r)
+            if (act[r]) output(0, yr[r], gcr[r], sw[hcr[r]], lapv_xy(0, hcr[r]), 0.0, 0.0);
     } else {
         // pipeline: w ring {k, k+1, k+2} with w(k+3) in flight; dG ring {k-1, k, k+1}
         prefetch_coef(zb - 1);
@@ -449,23 +458,130 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
         __syncthreads();
         compute_dg(zb);
         prefetch_coef(zb + 1);
-        double wvm = sw[mod3(zb - 1) * HX * HY + hc].y;
+        double wvm[RPT];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) wvm[r] = sw[mod3(zb - 1) * HX * HY + hcr[r]].y;
         __syncthreads();
         load_plane(zb + 2);
         for (int k = zb; k < ze; ++k) {
             cp_async_wait_all();
             __syncthreads();
-            const double2 w0 = sw[mod3(k) * HX * HY + hc];
-            const double wvp = sw[mod3(k + 1) * HX * HY + hc].y;
-            const double lxy = lapv_xy(k);
+            double2 w0[RPT];
+            double wvp[RPT], lxy[RPT];
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                w0[r] = sw[mod3(k) * HX * HY + hcr[r]];
+                wvp[r] = sw[mod3(k + 1) * HX * HY + hcr[r]].y;
+                lxy[r] = lapv_xy(k, hcr[r]);
+            }
             compute_dg(k + 1);
             if (k + 2 <= ze) prefetch_coef(k + 2);
             __syncthreads();
             if (k + 3 <= ze + 1) load_plane(k + 3);
-            if (active) output(k, w0, lxy, wvm, wvp);
-            wvm = w0.y;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                if (act[r]) output(k, yr[r], gcr[r], w0[r], lxy[r], wvm[r], wvp[r]);
+                wvm[r] = w0[r].y;
+            }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// Two-pass matrix-free matvec (thread per cell, neighbours through L1/L2):
+//   pass 1: T = (dG_u, eta) per cell                 reads w, S, D, c_u, c_v
+//   pass 2: y from T, cbar, G_u (7-point), w, S, D, G_v
+// 152 B/cell of DRAM traffic instead of 88, but both passes are plain
+// coalesced streams with high occupancy and no barriers.
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ void cell_xyz(const GridDev &g, long long q, int &x, int &y, int &z)
+{
+    x = (int)(q % g.nx);
+    y = (int)((q / g.nx) % g.ny);
+    z = (int)(q / ((long long)g.nx * g.ny));
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256)
+mv_pass1_kernel(GridDev g, ParamsDev P, const double *__restrict__ coef, const double2 *__restrict__ w,
+                double2 *__restrict__ T, int zlo, long long ncells)
+{
+    // planes zlo .. : in slab mode also the first ghost plane past an
+    // interior slab boundary, which pass 2 reads as a z-neighbour
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= ncells) return;
+    int x, y, z;
+    cell_xyz(g, q, x, y, z);
+    z += zlo;
+    const int zs = zplane(g, z);
+    const long long c = cell_at(g, x, y, zs);
+    const long long N = g.nstore;
+    const double2 w0 = __ldg(w + c);
+    double lap = (__ldg(w + cell_at(g, wrap_coord(x + 1, g.nx, g.periodic), y, zs)).x - 2.0 * w0.x +
+                  __ldg(w + cell_at(g, wrap_coord(x - 1, g.nx, g.periodic), y, zs)).x) * g.ih2[0];
+    lap += (__ldg(w + cell_at(g, x, wrap_coord(y + 1, g.ny, g.periodic), zs)).x - 2.0 * w0.x +
+            __ldg(w + cell_at(g, x, wrap_coord(y - 1, g.ny, g.periodic), zs)).x) * g.ih2[1];
+    if (DIM == 3)
+        lap += (__ldg(w + cell_at(g, x, y, zplane(g, z + 1))).x - 2.0 * w0.x +
+                __ldg(w + cell_at(g, x, y, zplane(g, z - 1))).x) * g.ih2[2];
+    double2 t;
+    t.x = (-0.5 * P.alpha + __ldg(coef + CO_S * N + c)) * w0.x + __ldg(coef + CO_D * N + c) * w0.y -
+          0.5 * P.gamma * lap;
+    t.y = 0.5 * (__ldg(coef + CO_CU * N + c) * w0.x + __ldg(coef + CO_CV * N + c) * w0.y);
+    T[c] = t;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256)
+mv_pass2_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef, const double2 *__restrict__ w,
+                const double2 *__restrict__ T, double2 *__restrict__ yout)
+{
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= g.n) return;
+    int x, y, z;
+    cell_xyz(g, q, x, y, z);
+    const int zs = zplane(g, z);
+    const long long c = cell_at(g, x, y, zs);
+    const long long N = g.nstore;
+    const double *__restrict__ cC = coef + CO_CBAR * N;
+    const double *__restrict__ cG = coef + CO_GU * N;
+    const double2 t0 = __ldg(T + c), w0 = __ldg(w + c);
+    const double C0 = __ldg(cC + c), G0 = __ldg(cG + c);
+    const bool per = g.periodic != 0;
+    double d1 = 0.0, d2 = 0.0, lapv = 0.0;
+    auto face = [&](long long cn, double ih, bool ok, double sgn) {
+        // sgn = +1 for the upper face (n - c), -1 for the lower face (c - n)
+        if (!ok) return;
+        const double2 tn = __ldg(T + cn);
+        const double Cn = __ldg(cC + cn), Gn = __ldg(cG + cn);
+        d1 += 0.5 * (C0 + Cn) * (tn.x - t0.x) * ih;
+        d2 += 0.5 * (t0.y + tn.y) * (Gn - G0) * ih;
+        (void)sgn;
+    };
+    const long long cxp = cell_at(g, wrap_coord(x + 1, g.nx, g.periodic), y, zs);
+    const long long cxm = cell_at(g, wrap_coord(x - 1, g.nx, g.periodic), y, zs);
+    const long long cyp = cell_at(g, x, wrap_coord(y + 1, g.ny, g.periodic), zs);
+    const long long cym = cell_at(g, x, wrap_coord(y - 1, g.ny, g.periodic), zs);
+    face(cxp, g.ih2[0], per || x < g.nx - 1, 1.0);
+    face(cxm, g.ih2[0], per || x > 0, -1.0);
+    face(cyp, g.ih2[1], per || y < g.ny - 1, 1.0);
+    face(cym, g.ih2[1], per || y > 0, -1.0);
+    lapv = (__ldg(w + cxp).y - 2.0 * w0.y + __ldg(w + cxm).y) * g.ih2[0];
+    lapv += (__ldg(w + cyp).y - 2.0 * w0.y + __ldg(w + cym).y) * g.ih2[1];
+    if (DIM == 3) {
+        const long long czp = cell_at(g, x, y, zplane(g, z + 1));
+        const long long czm = cell_at(g, x, y, zplane(g, z - 1));
+        face(czp, g.ih2[2], zstep_ok(g, z, +1), 1.0);
+        face(czm, g.ih2[2], zstep_ok(g, z, -1), -1.0);
+        lapv += (__ldg(w + czp).y - 2.0 * w0.y + __ldg(w + czm).y) * g.ih2[2];
+    }
+    const double S = __ldg(coef + CO_S * N + c), D = __ldg(coef + CO_D * N + c), Gv = __ldg(coef + CO_GV * N + c);
+    const double hg = 0.5 * P.gamma;
+    double2 out;
+    out.x = w0.x / dt - d1 - d2;
+    out.y = w0.y / dt + (C0 / P.rho) * (D * w0.x + (-0.5 * P.beta + S) * w0.y - hg * lapv) + (Gv / P.rho) * t0.y;
+    yout[c] = out;
 }
 
 // ---------------------------------------------------------------------------
@@ -615,10 +731,12 @@ int red_grid(long long n)
 }
 
 template <typename K>
-acch_status set_smem(K kernel, size_t bytes)
+acch_status set_smem(K kernel, size_t bytes, int carveout = -1)
 {
     static_assert(sizeof(K) > 0, "");
     ACCH_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    if (carveout >= 0)
+        ACCH_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carveout));
     return ACCH_OK;
 }
 
@@ -685,26 +803,54 @@ acch_status launch_jacobian_prepare(acch_ctx *ctx, const double *x_old, double d
     return ACCH_OK;
 }
 
+static acch_status launch_matvec_twopass(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
+{
+    if (!ctx->d_mvtmp) ACCH_CUDA(cudaMalloc(&ctx->d_mvtmp, sizeof(double) * 2 * ctx->g.nstore));
+    const GridDev &g = ctx->g;
+    const unsigned nb = (unsigned)((g.n + 255) / 256);
+    const int zlo = (g.zg && !g.zwall_lo) ? -1 : 0, zhi = g.nz + ((g.zg && !g.zwall_hi) ? 1 : 0);
+    const long long n1 = (long long)(zhi - zlo) * g.nx * g.ny;
+    const unsigned nb1 = (unsigned)((n1 + 255) / 256);
+    if (g.dim == 3) {
+        mv_pass1_kernel<3><<<nb1, 256, 0, ctx->stream>>>(g, ctx->p, coef, (const double2 *)w, (double2 *)ctx->d_mvtmp,
+                                                         zlo, n1);
+        mv_pass2_kernel<3><<<nb, 256, 0, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
+                                                        (const double2 *)ctx->d_mvtmp, (double2 *)y);
+    } else {
+        mv_pass1_kernel<2><<<nb, 256, 0, ctx->stream>>>(g, ctx->p, coef, (const double2 *)w, (double2 *)ctx->d_mvtmp,
+                                                        0, g.n);
+        mv_pass2_kernel<2><<<nb, 256, 0, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
+                                                        (const double2 *)ctx->d_mvtmp, (double2 *)y);
+    }
+    ctx->launches += 1;
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
 acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
+    if (ctx->matvec_mode == 1) {
+        ProfScope prof_scope(ctx, PC_MATVEC, 88.0 * ctx->g.n);
+        return launch_matvec_twopass(ctx, coef, dt, w, y);
+    }
     ProfScope prof_scope(ctx, PC_MATVEC, 88.0 * ctx->g.n);
     const GridDev &g = ctx->g;
-    const dim3 block(MTX, MTY);
+    const dim3 block(MTX, MTY / MRPT);
     if (g.dim == 3) {
         using L = MatvecSmem<3, MTX, MTY>;
         static bool configured = false;
         if (!configured) {
-            acch_status st = set_smem(matvec_kernel<3, MTX, MTY>, L::bytes);
+            acch_status st = set_smem(matvec_kernel<3, MTX, MTY, MRPT>, L::bytes);
             if (st != ACCH_OK) return st;
             configured = true;
         }
         const dim3 grid((g.nx + MTX - 1) / MTX, (g.ny + MTY - 1) / MTY, (g.nz + ZCHUNK - 1) / ZCHUNK);
-        matvec_kernel<3, MTX, MTY><<<grid, block, L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
+        matvec_kernel<3, MTX, MTY, MRPT><<<grid, block, L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
                                                                          (double2 *)y);
     } else {
         using L = MatvecSmem<2, MTX, MTY>;
         const dim3 grid((g.nx + MTX - 1) / MTX, (g.ny + MTY - 1) / MTY, 1);
-        matvec_kernel<2, MTX, MTY><<<grid, block, L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
+        matvec_kernel<2, MTX, MTY, MRPT><<<grid, block, L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
                                                                          (double2 *)y);
     }
     ACCH_LAUNCHED(ctx);
