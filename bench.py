@@ -181,7 +181,7 @@ def cpu_sample(args, threads=1, counts=None):
     pre = O.SchwarzOracle(O.decompose(m, (ns // args.box) ** args.dim, 1), args.variant, args.solver, threads)
     t0 = time.perf_counter()
     J = st.jacobian(x)
-    pre.update(J.assemble())
+    pre.update(J.assemble_fast())
     t_fact = time.perf_counter() - t0
     b = -st.residual(x)
     its = 30

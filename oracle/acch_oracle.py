@@ -399,6 +399,98 @@ class JacobianOracle:
         skeleton I + D + D^2 (scheme.py:166-188), by structured probing."""
         return probe_blocks(self.mesh, self.matvec)
 
+    def assemble_fast(self):
+        """The same block CSR, assembled directly from the per-cell
+        coefficients (vectorised over cells, one stencil offset at a time);
+        tests pin it against ``assemble`` (probing of the matvec).  Used by
+        the CPU baseline, where probing would dominate the timing."""
+        m, co, st = self.mesh, self.step.co, self.step
+        d = m.dim
+        ih2 = [1.0 / (hh * hh) for hh in m.h]
+        hg = 0.5 * co.gamma
+        offs = [o for o in _stencil_offsets(d)]
+        oid = {o: i for i, o in enumerate(offs)}
+        units = [tuple((s if b == a else 0) for b in range(d)) for a in range(d) for s in (1, -1)]
+        zero = tuple(0 for _ in range(d))
+
+        def shift(f, o):
+            g = f
+            for a in range(d):
+                if o[a]:
+                    g = np.roll(g, -o[a], axis=m.np_axis(a))
+            return g
+
+        coords = np.indices(m.shape)
+
+        def valid(o):
+            if m.periodic:
+                return np.ones(m.shape, dtype=bool)
+            ok = np.ones(m.shape, dtype=bool)
+            for a in range(d):
+                c = coords[m.np_axis(a)] + o[a]
+                ok &= (c >= 0) & (c < m.counts[a])
+            return ok
+
+        vmask = {u: valid(u).astype(float) for u in units}
+        L = sum(vmask[u] * ih2[[a for a in range(d) if u[a]][0]] for u in units)
+        blk = {o: np.zeros(m.shape + (2, 2)) for o in offs}
+        cb, gu = self.cbar, self.gu
+        ktot = np.zeros(m.shape)
+        eta0 = np.zeros(m.shape)
+        terms = []
+        for u in units:
+            a = [b for b in range(d) if u[b]][0]
+            K = 0.5 * (cb + shift(cb, u)) * ih2[a] * vmask[u]
+            et = -0.5 * (shift(gu, u) - gu) * ih2[a] * vmask[u]
+            ktot += K
+            eta0 += et
+            terms.append((u, -K, et))
+        terms.insert(0, (zero, ktot, eta0))
+        for mo, wdg, weta in terms:
+            A = -0.5 * co.alpha + shift(self.S, mo) + hg * shift(L, mo)
+            b = blk[mo]
+            b[..., 0, 0] += wdg * A + weta * 0.5 * shift(self.cu, mo)
+            b[..., 0, 1] += wdg * shift(self.D, mo) + weta * 0.5 * shift(self.cv, mo)
+            for u2 in units:
+                a2 = [q for q in range(d) if u2[q]][0]
+                tgt = tuple(x + y for x, y in zip(mo, u2))
+                blk[tgt][..., 0, 0] += -wdg * hg * ih2[a2] * shift(vmask[u2], mo)
+        blk[zero][..., 0, 0] += 1.0 / st.dt
+        cr = cb / co.rho
+        blk[zero][..., 1, 0] += cr * self.D + self.gv * self.cu / (2.0 * co.rho)
+        blk[zero][..., 1, 1] += (1.0 / st.dt + cr * (-0.5 * co.beta + self.S) + hg * cr * L
+                                 + self.gv * self.cv / (2.0 * co.rho))
+        for u in units:
+            a = [b for b in range(d) if u[b]][0]
+            blk[u][..., 1, 1] += -hg * cr * ih2[a] * vmask[u]
+        n = m.n_cells
+        ids = np.arange(n).reshape(m.shape)
+        rows, cols, vals = [], [], []
+        for o in offs:
+            ok = valid(o).ravel()
+            rows.append(ids.ravel()[ok])
+            cols.append(shift(ids, o).ravel()[ok])
+            vals.append(blk[o].reshape(n, 2, 2)[ok])
+        rows = np.concatenate(rows)
+        cols = np.concatenate(cols)
+        vals = np.concatenate(vals)
+        keys = rows * n + cols
+        uk, inv = np.unique(keys, return_inverse=True)
+        out = np.zeros((len(uk), 2, 2))
+        np.add.at(out, inv, vals)
+        r = uk // n
+        indptr = np.zeros(n + 1, dtype=np.int64)
+        np.add.at(indptr, r + 1, 1)
+        return np.cumsum(indptr), (uk % n).astype(np.int64), out
+
+
+def _stencil_offsets(dim):
+    """Offsets with |dx|+|dy|+|dz| <= 2 (the radius-2 skeleton)."""
+    rng = range(-2, 3)
+    if dim == 2:
+        return [(x, y) for y in rng for x in rng if abs(x) + abs(y) <= 2]
+    return [(x, y, z) for z in rng for y in rng for x in rng if abs(x) + abs(y) + abs(z) <= 2]
+
 
 # ---------------------------------------------------------------------------
 # skeleton and probing assembly
@@ -922,7 +1014,7 @@ def newton_solve(step: Step, x0, cfg: NewtonSettings, precond: SchwarzOracle, tr
         jac = step.jacobian(x)
         reuse = (not cfg.refactor_on_entry) if m == 0 else cfg.reuse_factorization
         if not (reuse and precond.factors is not None):
-            precond.update(jac.assemble(), reuse=False)
+            precond.update(jac.assemble_fast(), reuse=False)
             facs += 1
         lin = gmres(jac.matvec, -f, precond.apply, cfg.lin_rel_tol, cfg.lin_abs_tol,
                     cfg.gmres_restart, cfg.max_linear_iterations)

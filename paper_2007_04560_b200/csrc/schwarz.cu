@@ -505,6 +505,182 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     }
 }
 
+// Warp solver with the column ids of level k+1 loaded during level k.  With
+// the ids already in registers, nothing in a level waits on a global load
+// until all of its factor loads (LDG.256) and the y gathers (LDS) are issued,
+// so in-order issue no longer serialises the loads: one HBM/L2 round trip per
+// level.  Rows 33-64 of a wide level take the plain path.
+template <int VARIANT, int MAXW = 12, int PREFETCH_DEPTH = 4>
+__global__ void __launch_bounds__(32, 8)
+apply_warp2_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
+                   const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
+                   const long long *__restrict__ sub_ext_off, const double4 *__restrict__ vals,
+                   const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
+                   WarpSmem L, long long nsub)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = threadIdx.x;
+    const long long s = blockIdx.x;
+    if (s >= nsub) return;
+    const ClassDev C = classes[sub_class[s]];
+    const int4 o = sub_origin[s];
+    const double4 *__restrict__ A = vals + sub_off[s];
+    double2 *y = reinterpret_cast<double2 *>(smem_raw);
+    int *f_ptr = reinterpret_cast<int *>(smem_raw + L.y_bytes());
+    int *f_bs = f_ptr + (C.nlev + 1);
+    int *b_ptr = f_bs + C.nlev;
+    int *b_bs = b_ptr + (C.nlevb + 1);
+    unsigned short *f_rows = reinterpret_cast<unsigned short *>(b_bs + C.nlevb);
+    unsigned short *b_rows = f_rows + C.nloc;
+    unsigned short *f_len = b_rows + C.nloc;
+    unsigned short *b_len = f_len + C.nloc;
+    for (int i = lane; i <= C.nlev; i += 32) f_ptr[i] = C.lev_ptr[i];
+    for (int i = lane; i < C.nlev; i += 32) f_bs[i] = C.f_base[i];
+    for (int i = lane; i <= C.nlevb; i += 32) b_ptr[i] = C.levb_ptr[i];
+    for (int i = lane; i < C.nlevb; i += 32) b_bs[i] = C.b_base[i];
+    for (int i = lane; i < C.nloc; i += 32) {
+        f_rows[i] = C.f_rows16[i];
+        b_rows[i] = C.b_rows16[i];
+        f_len[i] = C.f_len8[i];
+        b_len[i] = C.b_len8[i];
+    }
+    __syncwarp();
+    const int K = C.nlev + C.nlevb;
+    auto prefetch_level = [&](int k) {
+        if (k >= K) return;
+        int lo, hi;
+        if (k < C.nlev) {
+            lo = f_bs[k];
+            hi = k + 1 < C.nlev ? f_bs[k + 1] : (C.nlevb > 0 ? b_bs[0] : C.ell_total);
+        } else {
+            const int kb = k - C.nlev;
+            lo = b_bs[kb];
+            hi = kb + 1 < C.nlevb ? b_bs[kb + 1] : C.ell_total;
+        }
+        prefetch_l2(A + lo, (unsigned)(hi - lo) * 32u);
+    };
+    if (lane < PREFETCH_DEPTH) prefetch_level(lane);
+    for (int l = lane; l < C.nloc; l += 32) {
+        int gx, gy, gz;
+        local_to_global(g, C, o, l, gx, gy, gz);
+        double2 v = r[cell_at(g, gx, gy, zplane(g, gz))];
+        if (VARIANT == 2 && !C.owned[l]) v = make_double2(0.0, 0.0);
+        y[l] = v;
+    }
+    __syncwarp();
+
+    // level descriptor: rows [r0, r0+m), slot base, first U slot (backward), lane-0 row length
+    struct Lev {
+        int r0, m, base, first, len0, len1, i0, i1;
+    };
+    auto describe = [&](int k) {
+        Lev d;
+        const bool fwd = k < C.nlev;
+        const int lv = fwd ? k : k - C.nlev;
+        d.r0 = fwd ? f_ptr[lv] : b_ptr[lv];
+        d.m = (fwd ? f_ptr[lv + 1] : b_ptr[lv + 1]) - d.r0;
+        d.base = fwd ? f_bs[lv] : b_bs[lv];
+        d.first = fwd ? 0 : 1;
+        const unsigned short *rows = fwd ? f_rows : b_rows;
+        const unsigned short *lens = fwd ? f_len : b_len;
+        d.len0 = lane < d.m ? (int)lens[d.r0 + lane] - d.first : 0;
+        d.len1 = lane + 32 < d.m ? (int)lens[d.r0 + lane + 32] - d.first : 0;
+        d.i0 = lane < d.m ? rows[d.r0 + lane] : 0;
+        d.i1 = lane + 32 < d.m ? rows[d.r0 + lane + 32] : 0;
+        return d;
+    };
+    // jagged offsets (level-relative) of the lane's first row, and its ids
+    auto offsets_and_ids = [&](const Lev &d, int (&offs)[MAXW], int (&c)[MAXW]) {
+        int off = d.first ? d.m : 0;
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t) {
+            offs[t] = off;
+            if (t < d.len0) c[t] = __ldg(C.ecol + d.base + off + lane);
+            off += __popc(__ballot_sync(0xffffffffu, d.len0 > t)) + __popc(__ballot_sync(0xffffffffu, d.len1 > t));
+        }
+        return off;
+    };
+
+    Lev cur = describe(0);
+    int offs[MAXW], c[MAXW];
+    int tail_off = offsets_and_ids(cur, offs, c);
+    for (int k = 0; k < K; ++k) {
+        if (lane == 0) prefetch_level(k + PREFETCH_DEPTH);
+        // this level's factor slots and y gathers (ids already in registers)
+        double4 a[MAXW];
+        double2 yv[MAXW];
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t)
+            if (t < cur.len0) a[t] = ldg4(A + cur.base + offs[t] + lane);
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t)
+            if (t < cur.len0) yv[t] = y[c[t]];
+        // next level's ids, issued before this level's FMA chain
+        Lev nxt;
+        int offs_n[MAXW], c_n[MAXW];
+        int tail_n = 0;
+        if (k + 1 < K) {
+            nxt = describe(k + 1);
+            tail_n = offsets_and_ids(nxt, offs_n, c_n);
+        }
+        double2 acc0 = y[cur.i0];
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t)
+            if (t < cur.len0) blk_sub(acc0, a[t], yv[t]);
+        double2 acc1 = y[cur.i1];
+        if (cur.len1 > 0) {
+#pragma unroll
+            for (int t = 0; t < MAXW; ++t)
+                if (t < cur.len1) {
+                    const int e = cur.base + offs[t] + lane + 32;
+                    blk_sub(acc1, ldg4(A + e), y[__ldg(C.ecol + e)]);
+                }
+        }
+        int off = tail_off;
+        for (int t = MAXW;; ++t) {   // rows longer than MAXW slots (wrapped boxes, fill-in)
+            const unsigned b0 = __ballot_sync(0xffffffffu, cur.len0 > t), b1 = __ballot_sync(0xffffffffu, cur.len1 > t);
+            if (!(b0 | b1)) break;
+            const int e = cur.base + off + lane;
+            if (t < cur.len0) blk_sub(acc0, ldg4(A + e), y[__ldg(C.ecol + e)]);
+            if (t < cur.len1) blk_sub(acc1, ldg4(A + e + 32), y[__ldg(C.ecol + e + 32)]);
+            off += __popc(b0) + __popc(b1);
+        }
+        if (cur.first == 0) {
+            if (lane < cur.m) y[cur.i0] = acc0;
+            if (lane + 32 < cur.m) y[cur.i1] = acc1;
+        } else {
+            if (lane < cur.m) {
+                const double4 di = ldg4(A + cur.base + lane);
+                y[cur.i0] = make_double2(di.x * acc0.x + di.y * acc0.y, di.z * acc0.x + di.w * acc0.y);
+            }
+            if (lane + 32 < cur.m) {
+                const double4 di = ldg4(A + cur.base + lane + 32);
+                y[cur.i1] = make_double2(di.x * acc1.x + di.y * acc1.y, di.z * acc1.x + di.w * acc1.y);
+            }
+        }
+        __syncwarp();
+        if (k + 1 < K) {
+            cur = nxt;
+            tail_off = tail_n;
+#pragma unroll
+            for (int t = 0; t < MAXW; ++t) {
+                offs[t] = offs_n[t];
+                c[t] = c_n[t];
+            }
+        }
+    }
+    if (VARIANT == 1) {
+        for (int l = lane; l < C.nloc; l += 32) {
+            if (!C.owned[l]) continue;
+            int gx, gy, gz;
+            local_to_global(g, C, o, l, gx, gy, gz);
+            z[cell_at(g, gx, gy, zplane(g, gz))] = y[l];
+        }
+    } else {
+        for (int l = lane; l < C.nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
+    }
+}
+
 // ---------------------------------------------------------------------------
 // TMA-streamed warp solver.  Same sweeps as apply_warp_kernel, but each
 // level's factor slots and column ids are brought into a per-warp
@@ -1106,6 +1282,7 @@ struct acch_precond {
     int max_nloc = 0;
     int warp_mode = 0;     // apply_warp_kernel usable
     int tma_mode = 0;      // apply_tma_kernel (TMA ring) in use
+    int warp2 = 1;         // apply_warp2_kernel (ids one level ahead); ACCH_WARP2=0 -> apply_warp_kernel
     TmaSmem tl{};
     int pf_depth = 8;      // levels prefetched ahead into L2 (ACCH_PREFETCH_DEPTH overrides)
     WarpSmem wl{0, 0, 0};
@@ -1246,6 +1423,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         }
         pc->warp_mode = (max_width <= 64 && max_nloc <= 65535 && pc->wl.bytes() <= 200 * 1024) ? 1 : 0;
         if (const char *e = getenv("ACCH_PREFETCH_DEPTH")) pc->pf_depth = atoi(e);
+        if (const char *e = getenv("ACCH_WARP2")) pc->warp2 = atoi(e) ? 1 : 0;
         if (const char *e = getenv("ACCH_SCHWARZ_BLOCK_SOLVER"))   // testing: force the CTA-wide solver
             if (atoi(e)) pc->warp_mode = 0, pc->tps = 128;
         // TMA ring: at least two of the largest level segments
@@ -1375,6 +1553,9 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 16>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp2_kernel<0, 12, 4>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp2_kernel<1, 12, 4>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp2_kernel<2, 12, 4>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<0>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<1>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<2>, co, 100));
@@ -1494,9 +1675,14 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     apply_warp_kernel<V, 12, D><<<(unsigned)pc->nsub, 32, pc->wl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,    \
         pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
         (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub)
+#define W2APPLY(V)                                                                                            \
+    apply_warp2_kernel<V, 12, 4><<<(unsigned)pc->nsub, 32, pc->wl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,   \
+        pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
+        (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub)
 #define WAPPLY(V)                                            \
     do {                                                     \
-        if (pc->pf_depth <= 4) WAPPLY_D(V, 4);               \
+        if (pc->warp2) W2APPLY(V);                           \
+        else if (pc->pf_depth <= 4) WAPPLY_D(V, 4);          \
         else if (pc->pf_depth <= 8) WAPPLY_D(V, 8);          \
         else WAPPLY_D(V, 16);                                \
     } while (0)
@@ -1524,6 +1710,7 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
 #undef APPLY
 #undef WAPPLY
 #undef WAPPLY_D
+#undef W2APPLY
 #undef TAPPLY
     ACCH_LAUNCHED(ctx);
     if (pc->variant != 1) {

@@ -211,3 +211,14 @@ def test_simulate_adaptive_2d_matches_reference():
 
 def test_simulate_adaptive_3d_neumann_matches_reference():
     _compare_sim(*run_sim("c3small"))
+
+
+@pytest.mark.parametrize("tag", ["2d_neu", "2d_per", "2d_per4", "3d_neu", "3d_per"])
+def test_fast_assembly_equals_reference_blocks(tag):
+    z = golden(f"stencil_{tag}.npz")
+    m = mesh_of(z)
+    st = O.Step(m, CO, z["uo"], z["vo"], float(z["dt"]))
+    ip, ix, bl = st.jacobian(O.pack(z["un"], z["vn"])).assemble_fast()
+    assert np.array_equal(ip, z["J_indptr"])
+    assert np.array_equal(ix, z["J_indices"])
+    assert np.max(np.abs(bl - z["J_blocks"])) <= 1e-12 * np.max(np.abs(z["J_blocks"]))
