@@ -78,8 +78,11 @@ __device__ __forceinline__ double cell_gap(double u, double v)
 __device__ __forceinline__ int wrap_coord(int i, int n, int periodic)
 {
     if (periodic) {
-        i %= n;
-        return i < 0 ? i + n : i;
+        // stencil and box offsets stay within one period: two compares, the
+        // integer division only for a (never seen) farther offset
+        i = i < 0 ? i + n : (i >= n ? i - n : i);
+        if ((unsigned)i >= (unsigned)n) i = ((i % n) + n) % n;
+        return i;
     }
     return i < 0 ? 0 : (i >= n ? n - 1 : i);
 }

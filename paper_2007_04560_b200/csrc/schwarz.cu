@@ -61,6 +61,10 @@ struct ClassDev {
     // compact copies for staging into shared memory by the warp solver
     const unsigned short *f_rows16, *b_rows16;
     const unsigned short *f_len8, *b_len8;   // row lengths (slots) in level order
+    // the class-group solver's shared-memory image (byte offsets into meta):
+    // f_ptr | f_base | b_ptr | b_base (int) | f_rows | b_rows | f_len | b_len | ecol (uint16)
+    const unsigned char *meta;
+    int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol;
 };
 
 struct ClassHost {
@@ -72,6 +76,8 @@ struct ClassHost {
     std::vector<unsigned short> f_len8, b_len8;
     std::vector<int2> upd;
     std::vector<unsigned char> owned;
+    std::vector<unsigned char> meta;   // ClassDev::meta image
+    int m_off[9] = {0};
     int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
     void *dev_mem = nullptr;
     ClassDev dev;
@@ -197,6 +203,27 @@ __device__ __forceinline__ double4 ldg4(const double4 *p)
                  : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
                  : "l"(p));
     return v;
+}
+
+// predicated LDG.256 into an in/out register quad: v keeps its old value when
+// !pred, so the last load of a batch always defines v and can anchor a data
+// dependency (see sweep_level)
+// Factor slots are read exactly once per apply: the loads carry an
+// L2::evict_first policy (and skip L1), so the dead lines they leave behind
+// go before the levels the TMA engine has prefetched but not yet consumed.
+// (v is left undefined when !pred; it is only read as a dependency anchor.)
+__device__ __forceinline__ uint64_t evict_first_policy()
+{
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void ldg4_pred(double4 &v, const double4 *p, bool pred, uint64_t pol)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+                 "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %6;\n\t}"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p), "r"((unsigned)pred), "l"(pol));
 }
 
 __device__ __forceinline__ void blk_sub(double2 &acc, const double4 &a, const double2 &y)
@@ -505,180 +532,193 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     }
 }
 
-// Warp solver with the column ids of level k+1 loaded during level k.  With
-// the ids already in registers, nothing in a level waits on a global load
-// until all of its factor loads (LDG.256) and the y gathers (LDS) are issued,
-// so in-order issue no longer serialises the loads: one HBM/L2 round trip per
-// level.  Rows 33-64 of a wide level take the plain path.
-template <int VARIANT, int MAXW = 12, int PREFETCH_DEPTH = 4>
-__global__ void __launch_bounds__(32, 8)
-apply_warp2_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
-                   const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
-                   const long long *__restrict__ sub_ext_off, const double4 *__restrict__ vals,
-                   const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
-                   WarpSmem L, long long nsub)
+// ---------------------------------------------------------------------------
+// Class-group solver (default).  One CTA = NW warps = up to NW subdomains of
+// the SAME class: the class's symbolic data (level tables, row lists, row
+// lengths, slot column ids as uint16) is copied once into shared memory and
+// shared by the NW warps, each of which keeps its own y (double2 per cell).
+// A level then costs one global round trip -- the factor slots, L2-prefetched
+// PD levels ahead by the TMA engine -- because every index it needs (rows,
+// lengths, jagged offsets by ballot, column ids) is on-chip.
+// ---------------------------------------------------------------------------
+
+// one level of a triangular sweep for the rows owned by this lane (q, q + 32)
+//   first = 0: forward (L) rows, y_i -= sum L_ij y_j
+//   first = m: backward (U) rows, slot 0..m-1 hold inv(D_i); y_i = inv(D_i)(y_i - sum U_ij y_j)
+//
+// All of the lane's factor loads are issued before the first FMA: the
+// accumulator's initial shared-memory read takes its address through the last
+// load's result (masked by `zero`, a runtime 0 the compiler cannot fold), so
+// ptxas cannot start consuming loads 0..5 before it has issued loads 6..11 --
+// the interleaving that otherwise costs a second memory round trip per level.
+template <int MAXW>
+__device__ __forceinline__ void sweep_level(const double4 *__restrict__ A, const unsigned short *__restrict__ ecol,
+                                            double2 *y, int base, int m, int len0, int len1, int i0, int i1,
+                                            bool backward, int lane, int zero, uint64_t pol)
 {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int lane = threadIdx.x;
-    const long long s = blockIdx.x;
-    if (s >= nsub) return;
-    const ClassDev C = classes[sub_class[s]];
+    int offs[MAXW];
+    double4 a[MAXW];
+    int c[MAXW];
+    int off = backward ? m : 0;
+    double4 d0, d1;
+    if (backward) {
+        ldg4_pred(d0, A + base + lane, lane < m, pol);
+        ldg4_pred(d1, A + base + lane + 32, lane + 32 < m, pol);
+    }
+#pragma unroll
+    for (int t = 0; t < MAXW; ++t) {
+        offs[t] = off;
+        ldg4_pred(a[t], A + base + off + lane, t < len0, pol);
+        c[t] = t < len0 ? ecol[base + off + lane] : 0;
+        off += __popc(__ballot_sync(0xffffffffu, len0 > t)) + __popc(__ballot_sync(0xffffffffu, len1 > t));
+    }
+    const int dep = __double2hiint(a[MAXW - 1].x) & zero;
+    double2 acc0 = y[i0 + dep], acc1 = y[i1];
+#pragma unroll
+    for (int t = 0; t < MAXW; ++t)
+        if (t < len0) blk_sub(acc0, a[t], y[c[t]]);
+    if (len1 > 0) {
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t)
+            if (t < len1) {
+                a[t] = ldg4(A + base + offs[t] + lane + 32);
+                c[t] = ecol[base + offs[t] + lane + 32];
+            }
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t)
+            if (t < len1) blk_sub(acc1, a[t], y[c[t]]);
+    }
+    for (int t = MAXW;; ++t) {   // rows longer than MAXW slots (wrapped boxes, fill-in)
+        const unsigned b0 = __ballot_sync(0xffffffffu, len0 > t), b1 = __ballot_sync(0xffffffffu, len1 > t);
+        if (!(b0 | b1)) break;
+        if (t < len0) blk_sub(acc0, ldg4(A + base + off + lane), y[ecol[base + off + lane]]);
+        if (t < len1) blk_sub(acc1, ldg4(A + base + off + lane + 32), y[ecol[base + off + lane + 32]]);
+        off += __popc(b0) + __popc(b1);
+    }
+    if (backward) {
+        acc0 = make_double2(d0.x * acc0.x + d0.y * acc0.y, d0.z * acc0.x + d0.w * acc0.y);
+        acc1 = make_double2(d1.x * acc1.x + d1.y * acc1.y, d1.z * acc1.x + d1.w * acc1.y);
+    }
+    if (lane < m) y[i0] = acc0;
+    if (lane + 32 < m) y[i1] = acc1;
+    __syncwarp();
+}
+
+// one subdomain of a class group: gather, forward and backward sweeps, scatter
+template <int VARIANT, int MAXW>
+__device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev &C, const unsigned char *smem_meta,
+                                             double2 *y, int s, const int4 *__restrict__ sub_origin,
+                                             const long long *__restrict__ sub_off,
+                                             const long long *__restrict__ sub_ext_off,
+                                             const double4 *__restrict__ vals, const double2 *__restrict__ r,
+                                             double2 *__restrict__ z, double2 *__restrict__ ext_out, int zero, int pd)
+{
+    const int lane = threadIdx.x & 31;
+    const int nlev = C.nlev, nlevb = C.nlevb, nloc = C.nloc, ell_total = C.ell_total;
+    const int *f_ptr = reinterpret_cast<const int *>(smem_meta);
+    const int *f_bs = reinterpret_cast<const int *>(smem_meta + C.m_fbs);
+    const int *b_ptr = reinterpret_cast<const int *>(smem_meta + C.m_bptr);
+    const int *b_bs = reinterpret_cast<const int *>(smem_meta + C.m_bbs);
+    const unsigned short *f_rows = reinterpret_cast<const unsigned short *>(smem_meta + C.m_frows);
+    const unsigned short *b_rows = reinterpret_cast<const unsigned short *>(smem_meta + C.m_brows);
+    const unsigned short *f_len = reinterpret_cast<const unsigned short *>(smem_meta + C.m_flen);
+    const unsigned short *b_len = reinterpret_cast<const unsigned short *>(smem_meta + C.m_blen);
+    const unsigned short *ecol = reinterpret_cast<const unsigned short *>(smem_meta + C.m_ecol);
+    const uint64_t pol = evict_first_policy();
     const int4 o = sub_origin[s];
     const double4 *__restrict__ A = vals + sub_off[s];
-    double2 *y = reinterpret_cast<double2 *>(smem_raw);
-    int *f_ptr = reinterpret_cast<int *>(smem_raw + L.y_bytes());
-    int *f_bs = f_ptr + (C.nlev + 1);
-    int *b_ptr = f_bs + C.nlev;
-    int *b_bs = b_ptr + (C.nlevb + 1);
-    unsigned short *f_rows = reinterpret_cast<unsigned short *>(b_bs + C.nlevb);
-    unsigned short *b_rows = f_rows + C.nloc;
-    unsigned short *f_len = b_rows + C.nloc;
-    unsigned short *b_len = f_len + C.nloc;
-    for (int i = lane; i <= C.nlev; i += 32) f_ptr[i] = C.lev_ptr[i];
-    for (int i = lane; i < C.nlev; i += 32) f_bs[i] = C.f_base[i];
-    for (int i = lane; i <= C.nlevb; i += 32) b_ptr[i] = C.levb_ptr[i];
-    for (int i = lane; i < C.nlevb; i += 32) b_bs[i] = C.b_base[i];
-    for (int i = lane; i < C.nloc; i += 32) {
-        f_rows[i] = C.f_rows16[i];
-        b_rows[i] = C.b_rows16[i];
-        f_len[i] = C.f_len8[i];
-        b_len[i] = C.b_len8[i];
-    }
-    __syncwarp();
-    const int K = C.nlev + C.nlevb;
+    const int nall = nlev + nlevb;
     auto prefetch_level = [&](int k) {
-        if (k >= K) return;
+        if (k >= nall) return;
         int lo, hi;
-        if (k < C.nlev) {
+        if (k < nlev) {
             lo = f_bs[k];
-            hi = k + 1 < C.nlev ? f_bs[k + 1] : (C.nlevb > 0 ? b_bs[0] : C.ell_total);
+            hi = k + 1 < nlev ? f_bs[k + 1] : (nlevb > 0 ? b_bs[0] : ell_total);
         } else {
-            const int kb = k - C.nlev;
+            const int kb = k - nlev;
             lo = b_bs[kb];
-            hi = kb + 1 < C.nlevb ? b_bs[kb + 1] : C.ell_total;
+            hi = kb + 1 < nlevb ? b_bs[kb + 1] : ell_total;
         }
         prefetch_l2(A + lo, (unsigned)(hi - lo) * 32u);
     };
-    if (lane < PREFETCH_DEPTH) prefetch_level(lane);
-    for (int l = lane; l < C.nloc; l += 32) {
-        int gx, gy, gz;
-        local_to_global(g, C, o, l, gx, gy, gz);
-        double2 v = r[cell_at(g, gx, gy, zplane(g, gz))];
-        if (VARIANT == 2 && !C.owned[l]) v = make_double2(0.0, 0.0);
-        y[l] = v;
+    if (lane < pd) prefetch_level(lane);
+    // gather r into y, GB independent loads in flight per lane
+    constexpr int GB = 4;
+    for (int l0 = 0; l0 < nloc; l0 += 32 * GB) {
+        double2 v[GB];
+#pragma unroll
+        for (int j = 0; j < GB; ++j) {
+            const int l = l0 + j * 32 + lane;
+            if (l < nloc) {
+                int gx, gy, gz;
+                local_to_global(g, C, o, l, gx, gy, gz);
+                v[j] = r[cell_at(g, gx, gy, zplane(g, gz))];
+                if (VARIANT == 2 && !C.owned[l]) v[j] = make_double2(0.0, 0.0);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < GB; ++j) {
+            const int l = l0 + j * 32 + lane;
+            if (l < nloc) y[l] = v[j];
+        }
     }
     __syncwarp();
-
-    // level descriptor: rows [r0, r0+m), slot base, first U slot (backward), lane-0 row length
-    struct Lev {
-        int r0, m, base, first, len0, len1, i0, i1;
-    };
-    auto describe = [&](int k) {
-        Lev d;
-        const bool fwd = k < C.nlev;
-        const int lv = fwd ? k : k - C.nlev;
-        d.r0 = fwd ? f_ptr[lv] : b_ptr[lv];
-        d.m = (fwd ? f_ptr[lv + 1] : b_ptr[lv + 1]) - d.r0;
-        d.base = fwd ? f_bs[lv] : b_bs[lv];
-        d.first = fwd ? 0 : 1;
-        const unsigned short *rows = fwd ? f_rows : b_rows;
-        const unsigned short *lens = fwd ? f_len : b_len;
-        d.len0 = lane < d.m ? (int)lens[d.r0 + lane] - d.first : 0;
-        d.len1 = lane + 32 < d.m ? (int)lens[d.r0 + lane + 32] - d.first : 0;
-        d.i0 = lane < d.m ? rows[d.r0 + lane] : 0;
-        d.i1 = lane + 32 < d.m ? rows[d.r0 + lane + 32] : 0;
-        return d;
-    };
-    // jagged offsets (level-relative) of the lane's first row, and its ids
-    auto offsets_and_ids = [&](const Lev &d, int (&offs)[MAXW], int (&c)[MAXW]) {
-        int off = d.first ? d.m : 0;
-#pragma unroll
-        for (int t = 0; t < MAXW; ++t) {
-            offs[t] = off;
-            if (t < d.len0) c[t] = __ldg(C.ecol + d.base + off + lane);
-            off += __popc(__ballot_sync(0xffffffffu, d.len0 > t)) + __popc(__ballot_sync(0xffffffffu, d.len1 > t));
-        }
-        return off;
-    };
-
-    Lev cur = describe(0);
-    int offs[MAXW], c[MAXW];
-    int tail_off = offsets_and_ids(cur, offs, c);
-    for (int k = 0; k < K; ++k) {
-        if (lane == 0) prefetch_level(k + PREFETCH_DEPTH);
-        // this level's factor slots and y gathers (ids already in registers)
-        double4 a[MAXW];
-        double2 yv[MAXW];
-#pragma unroll
-        for (int t = 0; t < MAXW; ++t)
-            if (t < cur.len0) a[t] = ldg4(A + cur.base + offs[t] + lane);
-#pragma unroll
-        for (int t = 0; t < MAXW; ++t)
-            if (t < cur.len0) yv[t] = y[c[t]];
-        // next level's ids, issued before this level's FMA chain
-        Lev nxt;
-        int offs_n[MAXW], c_n[MAXW];
-        int tail_n = 0;
-        if (k + 1 < K) {
-            nxt = describe(k + 1);
-            tail_n = offsets_and_ids(nxt, offs_n, c_n);
-        }
-        double2 acc0 = y[cur.i0];
-#pragma unroll
-        for (int t = 0; t < MAXW; ++t)
-            if (t < cur.len0) blk_sub(acc0, a[t], yv[t]);
-        double2 acc1 = y[cur.i1];
-        if (cur.len1 > 0) {
-#pragma unroll
-            for (int t = 0; t < MAXW; ++t)
-                if (t < cur.len1) {
-                    const int e = cur.base + offs[t] + lane + 32;
-                    blk_sub(acc1, ldg4(A + e), y[__ldg(C.ecol + e)]);
-                }
-        }
-        int off = tail_off;
-        for (int t = MAXW;; ++t) {   // rows longer than MAXW slots (wrapped boxes, fill-in)
-            const unsigned b0 = __ballot_sync(0xffffffffu, cur.len0 > t), b1 = __ballot_sync(0xffffffffu, cur.len1 > t);
-            if (!(b0 | b1)) break;
-            const int e = cur.base + off + lane;
-            if (t < cur.len0) blk_sub(acc0, ldg4(A + e), y[__ldg(C.ecol + e)]);
-            if (t < cur.len1) blk_sub(acc1, ldg4(A + e + 32), y[__ldg(C.ecol + e + 32)]);
-            off += __popc(b0) + __popc(b1);
-        }
-        if (cur.first == 0) {
-            if (lane < cur.m) y[cur.i0] = acc0;
-            if (lane + 32 < cur.m) y[cur.i1] = acc1;
-        } else {
-            if (lane < cur.m) {
-                const double4 di = ldg4(A + cur.base + lane);
-                y[cur.i0] = make_double2(di.x * acc0.x + di.y * acc0.y, di.z * acc0.x + di.w * acc0.y);
-            }
-            if (lane + 32 < cur.m) {
-                const double4 di = ldg4(A + cur.base + lane + 32);
-                y[cur.i1] = make_double2(di.x * acc1.x + di.y * acc1.y, di.z * acc1.x + di.w * acc1.y);
-            }
-        }
-        __syncwarp();
-        if (k + 1 < K) {
-            cur = nxt;
-            tail_off = tail_n;
-#pragma unroll
-            for (int t = 0; t < MAXW; ++t) {
-                offs[t] = offs_n[t];
-                c[t] = c_n[t];
-            }
-        }
+    for (int lev = 0; lev < nlev; ++lev) {
+        if (lane == 0) prefetch_level(lev + pd);
+        const int r0 = f_ptr[lev], m = f_ptr[lev + 1] - r0;
+        const int len0 = lane < m ? f_len[r0 + lane] : 0;
+        const int len1 = lane + 32 < m ? f_len[r0 + lane + 32] : 0;
+        const int i0 = lane < m ? f_rows[r0 + lane] : 0;
+        const int i1 = lane + 32 < m ? f_rows[r0 + lane + 32] : 0;
+        sweep_level<MAXW>(A, ecol, y, f_bs[lev], m, len0, len1, i0, i1, false, lane, zero, pol);
+    }
+    for (int lev = 0; lev < nlevb; ++lev) {
+        if (lane == 0) prefetch_level(nlev + lev + pd);
+        const int r0 = b_ptr[lev], m = b_ptr[lev + 1] - r0;
+        // slot 0 of every backward row is its inverted diagonal block; U slots follow
+        const int len0 = lane < m ? b_len[r0 + lane] - 1 : 0;
+        const int len1 = lane + 32 < m ? b_len[r0 + lane + 32] - 1 : 0;
+        const int i0 = lane < m ? b_rows[r0 + lane] : 0;
+        const int i1 = lane + 32 < m ? b_rows[r0 + lane + 32] : 0;
+        sweep_level<MAXW>(A, ecol, y, b_bs[lev], m, len0, len1, i0, i1, true, lane, zero, pol);
     }
     if (VARIANT == 1) {
-        for (int l = lane; l < C.nloc; l += 32) {
+        for (int l = lane; l < nloc; l += 32) {
             if (!C.owned[l]) continue;
             int gx, gy, gz;
             local_to_global(g, C, o, l, gx, gy, gz);
             z[cell_at(g, gx, gy, zplane(g, gz))] = y[l];
         }
     } else {
-        for (int l = lane; l < C.nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
+        for (int l = lane; l < nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
     }
+    __syncwarp();   // y is reused by the warp's next subdomain
+}
+
+template <int VARIANT, int NW, int MAXW = 12>
+__global__ void __launch_bounds__(NW * 32, 1)
+apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *__restrict__ groups,
+                   const int *__restrict__ grp_sub, const int4 *__restrict__ sub_origin,
+                   const long long *__restrict__ sub_off, const long long *__restrict__ sub_ext_off,
+                   const double4 *__restrict__ vals, const double2 *__restrict__ r, double2 *__restrict__ z,
+                   double2 *__restrict__ ext_out, int meta_max, int y_stride, int zero, int pd)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int4 G = groups[blockIdx.x];   // (class, first entry of grp_sub, count, -)
+    const ClassDev &C = classes[G.x];
+    {
+        const uint4 *__restrict__ src = reinterpret_cast<const uint4 *>(C.meta);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem_raw);
+        for (int i = threadIdx.x; i < C.meta_bytes / 16; i += NW * 32) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    double2 *y = reinterpret_cast<double2 *>(smem_raw + meta_max + (size_t)warp * y_stride);
+    // one subdomain per warp (a loop over several per warp measured slower:
+    // it pushes the sweep past 255 registers into spills)
+    if (warp < G.z)
+        group_solve_one<VARIANT, MAXW>(g, C, smem_raw, y, grp_sub[G.y + warp], sub_origin, sub_off,
+                                           sub_ext_off, vals, r, z, ext_out, zero, pd);
 }
 
 // ---------------------------------------------------------------------------
@@ -1165,8 +1205,40 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
 template <typename T>
 size_t padded(size_t n) { return ((n * sizeof(T) + 255) / 256) * 256; }
 
+// shared-memory image of a class for apply_group_kernel (ClassDev::meta)
+void build_meta(ClassHost &C)
+{
+    size_t at = 0;
+    auto seg = [&](size_t bytes) { size_t o = at; at += (bytes + 15) / 16 * 16; return (int)o; };
+    const int nlev = (int)C.lev_ptr.size() - 1, nlevb = (int)C.levb_ptr.size() - 1;
+    int *m = C.m_off;
+    m[0] = seg(sizeof(int) * (nlev + 1));
+    m[1] = seg(sizeof(int) * nlev);
+    m[2] = seg(sizeof(int) * (nlevb + 1));
+    m[3] = seg(sizeof(int) * nlevb);
+    m[4] = seg(2 * (size_t)C.nloc);
+    m[5] = seg(2 * (size_t)C.nloc);
+    m[6] = seg(2 * (size_t)C.nloc);
+    m[7] = seg(2 * (size_t)C.nloc);
+    m[8] = seg(2 * (size_t)C.ell_total);
+    C.meta.assign(at, 0);
+    auto put = [&](int o, const void *src, size_t bytes) { if (bytes) memcpy(C.meta.data() + o, src, bytes); };
+    put(m[0], C.lev_ptr.data(), sizeof(int) * (nlev + 1));
+    put(m[1], C.f_base.data(), sizeof(int) * nlev);
+    put(m[2], C.levb_ptr.data(), sizeof(int) * (nlevb + 1));
+    put(m[3], C.b_base.data(), sizeof(int) * nlevb);
+    put(m[4], C.f_rows16.data(), 2 * (size_t)C.nloc);
+    put(m[5], C.b_rows16.data(), 2 * (size_t)C.nloc);
+    put(m[6], C.f_len8.data(), 2 * (size_t)C.nloc);
+    put(m[7], C.b_len8.data(), 2 * (size_t)C.nloc);
+    std::vector<unsigned short> e16(C.ell_total);
+    for (int t = 0; t < C.ell_total; ++t) e16[t] = C.ecol[t] < 0 ? 0 : (unsigned short)C.ecol[t];
+    put(m[8], e16.data(), 2 * (size_t)C.ell_total);
+}
+
 acch_status upload_class(ClassHost &C)
 {
+    build_meta(C);
     size_t total = 0;
     auto add = [&](size_t bytes) { size_t o = total; total += ((bytes + 255) / 256) * 256; return o; };
     size_t o_rel[3];
@@ -1184,6 +1256,7 @@ acch_status upload_class(ClassHost &C)
     const size_t o_fl8 = add(2 * C.f_len8.size()), o_bl8 = add(2 * C.b_len8.size());
     const size_t o_fjp = add(sizeof(int) * C.f_jptr.size()), o_fjo = add(sizeof(int) * std::max<size_t>(1, C.f_joff.size()));
     const size_t o_bjp = add(sizeof(int) * C.b_jptr.size()), o_bjo = add(sizeof(int) * std::max<size_t>(1, C.b_joff.size()));
+    const size_t o_meta = add(C.meta.size());
     ACCH_CUDA(cudaMalloc(&C.dev_mem, total));
     std::vector<unsigned char> h(total, 0);
     auto put = [&](size_t o, const void *src, size_t bytes) { if (bytes) memcpy(h.data() + o, src, bytes); };
@@ -1213,6 +1286,7 @@ acch_status upload_class(ClassHost &C)
     put(o_fjo, C.f_joff.data(), sizeof(int) * C.f_joff.size());
     put(o_bjp, C.b_jptr.data(), sizeof(int) * C.b_jptr.size());
     put(o_bjo, C.b_joff.data(), sizeof(int) * C.b_joff.size());
+    put(o_meta, C.meta.data(), C.meta.size());
     ACCH_CUDA(cudaMemcpy(C.dev_mem, h.data(), total, cudaMemcpyHostToDevice));
     unsigned char *b = (unsigned char *)C.dev_mem;
     ClassDev &d = C.dev;
@@ -1249,6 +1323,16 @@ acch_status upload_class(ClassHost &C)
     d.f_joff = (const int *)(b + o_fjo);
     d.b_jptr = (const int *)(b + o_bjp);
     d.b_joff = (const int *)(b + o_bjo);
+    d.meta = b + o_meta;
+    d.meta_bytes = (int)C.meta.size();
+    d.m_fbs = C.m_off[1];
+    d.m_bptr = C.m_off[2];
+    d.m_bbs = C.m_off[3];
+    d.m_frows = C.m_off[4];
+    d.m_brows = C.m_off[5];
+    d.m_flen = C.m_off[6];
+    d.m_blen = C.m_off[7];
+    d.m_ecol = C.m_off[8];
     d.ell_total = C.ell_total;
     d.max_fwidth = C.max_fwidth;
     d.max_bwidth = C.max_bwidth;
@@ -1282,9 +1366,14 @@ struct acch_precond {
     int max_nloc = 0;
     int warp_mode = 0;     // apply_warp_kernel usable
     int tma_mode = 0;      // apply_tma_kernel (TMA ring) in use
-    int warp2 = 1;         // apply_warp2_kernel (ids one level ahead); ACCH_WARP2=0 -> apply_warp_kernel
+    // class-group solver (apply_group_kernel): groups of <= group_nw subdomains of one class
+    int group_mode = 0, group_nw = 8, group_per_warp = 1, meta_max = 0, y_stride = 0;
+    size_t group_smem = 0;
+    std::vector<int4> groups;
+    int4 *d_groups = nullptr;
+    int *d_grp_sub = nullptr;
     TmaSmem tl{};
-    int pf_depth = 8;      // levels prefetched ahead into L2 (ACCH_PREFETCH_DEPTH overrides)
+    int pf_depth = 2;      // levels prefetched ahead into L2 (ACCH_PREFETCH_DEPTH overrides; 2 measured best for the group solver)
     WarpSmem wl{0, 0, 0};
 };
 
@@ -1302,6 +1391,8 @@ static void free_precond(acch_precond *pc)
     cudaFree(pc->d_ext_out);
     cudaFree(pc->d_cell_ptr);
     cudaFree(pc->d_cell_src);
+    cudaFree(pc->d_groups);
+    cudaFree(pc->d_grp_sub);
 }
 
 extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t overlap, const int64_t *owned_lo,
@@ -1423,7 +1514,6 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         }
         pc->warp_mode = (max_width <= 64 && max_nloc <= 65535 && pc->wl.bytes() <= 200 * 1024) ? 1 : 0;
         if (const char *e = getenv("ACCH_PREFETCH_DEPTH")) pc->pf_depth = atoi(e);
-        if (const char *e = getenv("ACCH_WARP2")) pc->warp2 = atoi(e) ? 1 : 0;
         if (const char *e = getenv("ACCH_SCHWARZ_BLOCK_SOLVER"))   // testing: force the CTA-wide solver
             if (atoi(e)) pc->warp_mode = 0, pc->tps = 128;
         // TMA ring: at least two of the largest level segments
@@ -1553,9 +1643,6 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 16>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16>, co, 100));
-        PC_CUDA(cudaFuncSetAttribute(apply_warp2_kernel<0, 12, 4>, co, 100));
-        PC_CUDA(cudaFuncSetAttribute(apply_warp2_kernel<1, 12, 4>, co, 100));
-        PC_CUDA(cudaFuncSetAttribute(apply_warp2_kernel<2, 12, 4>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<0>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<1>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<2>, co, 100));
@@ -1579,8 +1666,61 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16>, attr, b));
     }
-    if (pc->warp_mode && !pc->d_ext_out && variant == 1) {
-        // ext_out is not needed by the warp kernel for left-RAS
+    {
+        // class-group solver: NW subdomains of one class per CTA sharing the
+        // class's symbolic data in shared memory (ACCH_GROUP=0 disables,
+        // ACCH_GROUP_WARPS=4|8 picks the group size)
+        int meta_max = 0;
+        for (const auto &C : pc->classes) meta_max = std::max(meta_max, (int)C.meta.size());
+        pc->meta_max = (meta_max + 15) / 16 * 16;
+        pc->y_stride = (int)((sizeof(double2) * (size_t)max_nloc + 15) / 16 * 16);
+        int enable = pc->warp_mode && !pc->tma_mode;
+        if (const char *e = getenv("ACCH_GROUP")) enable = enable && atoi(e) != 0;
+        int nw = 8;
+        if (const char *e = getenv("ACCH_GROUP_WARPS")) nw = atoi(e) <= 4 ? 4 : 8;
+        const size_t limit = 227 * 1024;
+        while (nw >= 4 && (size_t)pc->meta_max + (size_t)nw * pc->y_stride > limit) nw /= 2;
+        if (enable && nw >= 4) {
+            pc->group_mode = 1;
+            pc->group_nw = nw;
+            pc->group_smem = (size_t)pc->meta_max + (size_t)nw * pc->y_stride;
+            std::vector<std::vector<int>> members(pc->classes.size());
+            for (long long s = 0; s < n_sub; ++s) members[pc->sub_class[s]].push_back((int)s);
+            const long long per = 1;
+            pc->group_per_warp = (int)per;
+            const size_t gsize = (size_t)nw * per;
+            std::vector<int> order;
+            for (size_t c = 0; c < members.size(); ++c)
+                for (size_t i = 0; i < members[c].size(); i += gsize) {
+                    const int cnt = (int)std::min<size_t>(gsize, members[c].size() - i);
+                    pc->groups.push_back(make_int4((int)c, (int)order.size(), cnt, 0));
+                    for (int q = 0; q < cnt; ++q) order.push_back(members[c][i + q]);
+                }
+            PC_CUDA(cudaMalloc(&pc->d_groups, sizeof(int4) * pc->groups.size()));
+            PC_CUDA(cudaMalloc(&pc->d_grp_sub, sizeof(int) * order.size()));
+            PC_CUDA(cudaMemcpy(pc->d_groups, pc->groups.data(), sizeof(int4) * pc->groups.size(),
+                               cudaMemcpyHostToDevice));
+            PC_CUDA(cudaMemcpy(pc->d_grp_sub, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
+            const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+            const int b = (int)pc->group_smem;
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 8>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 8>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4>, attr, b));
+        }
+        if (getenv("ACCH_DEBUG"))
+        {
+            int occ = 0;
+            if (pc->group_mode)
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, apply_group_kernel<1, 8>, pc->group_nw * 32,
+                                                              pc->group_smem);
+            fprintf(stderr, "[acch] group solver %s: %d warps/CTA, %d subdomains/warp, %zu groups, meta %d B, "
+                            "smem %zu B, CTAs/SM %d\n",
+                    pc->group_mode ? "on" : "off", pc->group_nw, pc->group_per_warp, pc->groups.size(),
+                    pc->meta_max, pc->group_smem, occ);
+        }
     }
 #undef PC_CUDA
     *out = pc;
@@ -1675,14 +1815,18 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     apply_warp_kernel<V, 12, D><<<(unsigned)pc->nsub, 32, pc->wl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,    \
         pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
         (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub)
-#define W2APPLY(V)                                                                                            \
-    apply_warp2_kernel<V, 12, 4><<<(unsigned)pc->nsub, 32, pc->wl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,   \
-        pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
-        (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub)
+#define GAPPLY_W(V, NW)                                                                                       \
+    apply_group_kernel<V, NW><<<(unsigned)pc->groups.size(), NW * 32, pc->group_smem, ctx->stream>>>(ctx->g,         \
+        pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, \
+        (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride, 0, pc->pf_depth)
+#define GAPPLY(V)                                  \
+    do {                                           \
+        if (pc->group_nw == 8) GAPPLY_W(V, 8);     \
+        else GAPPLY_W(V, 4);                       \
+    } while (0)
 #define WAPPLY(V)                                            \
     do {                                                     \
-        if (pc->warp2) W2APPLY(V);                           \
-        else if (pc->pf_depth <= 4) WAPPLY_D(V, 4);          \
+        if (pc->pf_depth <= 4) WAPPLY_D(V, 4);               \
         else if (pc->pf_depth <= 8) WAPPLY_D(V, 8);          \
         else WAPPLY_D(V, 16);                                \
     } while (0)
@@ -1690,7 +1834,11 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     apply_tma_kernel<V><<<(unsigned)pc->nsub, 32, pc->tl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,             \
         pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
         (double2 *)z, pc->d_ext_out, pc->tl, pc->nsub)
-    if (pc->tma_mode) {
+    if (pc->group_mode) {
+        if (pc->variant == 1) GAPPLY(1);
+        else if (pc->variant == 0) GAPPLY(0);
+        else GAPPLY(2);
+    } else if (pc->tma_mode) {
         if (pc->variant == 1) TAPPLY(1);
         else if (pc->variant == 0) TAPPLY(0);
         else TAPPLY(2);
@@ -1710,7 +1858,8 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
 #undef APPLY
 #undef WAPPLY
 #undef WAPPLY_D
-#undef W2APPLY
+#undef GAPPLY
+#undef GAPPLY_W
 #undef TAPPLY
     ACCH_LAUNCHED(ctx);
     if (pc->variant != 1) {

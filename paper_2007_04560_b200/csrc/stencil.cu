@@ -41,7 +41,8 @@ struct ResidualSmem {
     static constexpr size_t bytes = 2 * xbytes + 3 * gbytes;
 };
 
-__device__ __forceinline__ int mod3(int k) { return ((k % 3) + 3) % 3; }
+// ring slot of plane k; k >= -3 everywhere (z chunks start at 0, at most 2 planes below)
+__device__ __forceinline__ int mod3(int k) { return (int)((unsigned)(k + 3) % 3u); }
 
 // cp.async (LDGSTS) 16-byte global -> shared copies, grouped per plane
 __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
