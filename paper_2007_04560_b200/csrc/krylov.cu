@@ -91,10 +91,10 @@ __host__ __device__ __forceinline__ int gslot(int s) { return (s / MG) * (MG + 1
 template <int NS>
 __global__ void __launch_bounds__(kRedThreads)
 mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ h, double *__restrict__ w,
-               long long n, double *partials, unsigned int *counter, double *result)
+               long long n, double *partials, unsigned int *counter, double *result, int h_grouped)
 {
     __shared__ double sh[NS];
-    if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[gslot(threadIdx.x)] : 0.0;
+    if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[h_grouped ? gslot(threadIdx.x) : threadIdx.x] : 0.0;
     __syncthreads();
     double acc = 0.0;
     const long long n2 = n >> 1;
@@ -114,6 +114,53 @@ mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *
     double v[1] = {acc};
     const int ops[1] = {RED_SUM};
     reduce_finish<1>(v, ops, partials, counter, result);
+}
+
+// Fused CGS pass boundary: w <- w - V h (as mupdate_kernel), and in the same
+// sweep the next pass's projections <V_s, w_new> and ||w_new||^2.  Per-thread
+// accumulation order, block tree and partial fold are those of mupdate_kernel
+// and mdot_grouped_kernel on the same grid, so every value is bitwise what the
+// two separate kernels give -- but the basis is read once instead of twice.
+// (The reference decides the second pass only after seeing ||w_new||; the
+// speculative projections cost flops, not HBM traffic.)
+// result[0] = ||w_new||^2, result[1 + s] = <V_s, w_new>.  h is in gslot layout.
+template <int NS>
+__global__ void __launch_bounds__(kRedThreads)
+mupdate_mdot_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ h,
+                    double *__restrict__ w, long long n, double *partials, unsigned int *counter, double *result)
+{
+    __shared__ double sh[NS];
+    if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[gslot(threadIdx.x)] : 0.0;
+    __syncthreads();
+    double acc[NS + 1];
+#pragma unroll
+    for (int s = 0; s <= NS; ++s) acc[s] = 0.0;
+    const long long n2 = n >> 1;
+    double2 *__restrict__ w2 = reinterpret_cast<double2 *>(w);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        // all of the element's basis values in flight at once (register-resident
+        // for both the update and the projections)
+        double2 v[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+            v[s] = s < m ? __ldg(reinterpret_cast<const double2 *>(V + s * ld) + i) : make_double2(0.0, 0.0);
+        double2 wi = w2[i];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+            if (s < m) {
+                wi.x -= sh[s] * v[s].x;
+                wi.y -= sh[s] * v[s].y;
+            }
+        w2[i] = wi;
+        acc[0] += wi.x * wi.x + wi.y * wi.y;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+            if (s < m) acc[1 + s] += v[s].x * wi.x + v[s].y * wi.y;
+    }
+    int ops[NS + 1];
+#pragma unroll
+    for (int s = 0; s <= NS; ++s) ops[s] = RED_SUM;
+    reduce_finish<NS + 1>(acc, ops, partials, counter, result);
 }
 
 template <int NS>
@@ -200,18 +247,37 @@ static acch_status mdot_to(acch_ctx *ctx, const double *V, long long ld, int m, 
 }
 
 static acch_status mupdate_to(acch_ctx *ctx, const double *V, long long ld, int m, const double *h, double *w,
-                              long long n, double *out)
+                              long long n, double *out, int h_grouped = 1)
 {
     ProfScope prof_scope(ctx, PC_KUPDATE, 8.0 * (m + 2) * n);
     const int G = rgrid(n);
 #define MUP_CASE(NS) \
-    mupdate_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter, out);
+    mupdate_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter, out, \
+                                                           h_grouped);
     if (m <= 4) { MUP_CASE(4) }
     else if (m <= 8) { MUP_CASE(8) }
     else if (m <= 16) { MUP_CASE(16) }
     else if (m <= 32) { MUP_CASE(32) }
     else { acch_set_error("mupdate: too many vectors"); return ACCH_ERR_INVALID_ARG; }
 #undef MUP_CASE
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+// w -= V h (h in gslot layout); out[0] = ||w||^2, out[1 + s] = <V_s, w>
+static acch_status mupdate_mdot_to(acch_ctx *ctx, const double *V, long long ld, int m, const double *h, double *w,
+                                   long long n, double *out)
+{
+    ProfScope prof_scope(ctx, PC_KUPDATE, 8.0 * (m + 2) * n);
+    const int G = rgrid(n);
+#define MUD_CASE(NS) \
+    mupdate_mdot_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter, out);
+    if (m <= 4) { MUD_CASE(4) }
+    else if (m <= 8) { MUD_CASE(8) }
+    else if (m <= 16) { MUD_CASE(16) }
+    else if (m <= 32) { MUD_CASE(32) }
+    else { acch_set_error("mupdate_mdot: too many vectors"); return ACCH_ERR_INVALID_ARG; }
+#undef MUD_CASE
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
 }
@@ -329,7 +395,7 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
         return ACCH_OK;
     };
 
-    double tmp[64];
+    double tmp[128];
     TRY(dot_to(ctx, b + off, b + off, ni, dh));
     TRY(reduce_dots(tmp, dh, 1, false));
     const double bnorm = sqrt(tmp[0]);
@@ -369,35 +435,30 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
             TRY(matvec(zj, w));
             double norm_before, norm_after;
             if (ortho == 1) {
+                // pass 1: h1 = V^T w (+ ||w||^2); w -= V h1 fused with the
+                // second pass's projections h2 = V^T w (+ ||w||^2), which are
+                // used only when the reference's cancellation test fires
                 int ns = 0;
-                TRY(mdot_to(ctx, V + off, nv, j + 1, w + off, ni, dh, &ns));
+                const int m = j + 1;
+                double *d2 = dh + 64;   // [||w||^2, h2_0 .. h2_{m-1}]
+                TRY(mdot_to(ctx, V + off, nv, m, w + off, ni, dh, &ns));
+                if (multi) TRY(reduce_dots(tmp, dh, 4 * (MG + 1), true));
+                TRY(mupdate_mdot_to(ctx, V + off, nv, m, dh, w + off, ni, d2));
                 if (multi) {
-                    TRY(reduce_dots(tmp, dh, 4 * (MG + 1), true));
-                    TRY(mupdate_to(ctx, V + off, nv, j + 1, dh, w + off, ni, dh + 40));
-                    double t40;
-                    TRY(reduce_dots(&t40, dh + 40, 1, false));
-                    tmp[40] = t40;
+                    TRY(reduce_dots(tmp + 64, d2, 1 + m, true));
                 } else {
-                    TRY(mupdate_to(ctx, V + off, nv, j + 1, dh, w + off, ni, dh + 40));
-                    TRY(fetch(ctx, tmp, dh, 41));
+                    TRY(fetch(ctx, tmp, dh, 64 + 1 + m));
                 }
                 for (int i = 0; i <= j; ++i) h(i, j) = tmp[gslot(i)];
                 norm_before = sqrt(tmp[ns - 1]);
-                norm_after = sqrt(tmp[40]);
+                norm_after = sqrt(tmp[64]);
                 if (norm_after < 0.5 * norm_before) {
-                    TRY(mdot_to(ctx, V + off, nv, j + 1, w + off, ni, dh, &ns));
-                    double t2[64];
-                    if (multi) TRY(reduce_dots(t2, dh, 4 * (MG + 1), true));
-                    TRY(mupdate_to(ctx, V + off, nv, j + 1, dh, w + off, ni, dh + 40));
-                    if (multi) {
-                        double t40;
-                        TRY(reduce_dots(&t40, dh + 40, 1, false));
-                        t2[40] = t40;
-                    } else {
-                        TRY(fetch(ctx, t2, dh, 41));
-                    }
-                    for (int i = 0; i <= j; ++i) h(i, j) += t2[gslot(i)];
-                    norm_after = sqrt(t2[40]);
+                    TRY(mupdate_to(ctx, V + off, nv, m, d2 + 1, w + off, ni, dh + 40, 0));
+                    double t40;
+                    if (multi) TRY(reduce_dots(&t40, dh + 40, 1, false));
+                    else TRY(fetch(ctx, &t40, dh + 40, 1));
+                    for (int i = 0; i <= j; ++i) h(i, j) += tmp[65 + i];
+                    norm_after = sqrt(t40);
                 }
             } else {
                 TRY(dot_to(ctx, w + off, w + off, ni, dh + 40));

@@ -1377,6 +1377,17 @@ struct acch_precond {
     WarpSmem wl{0, 0, 0};
 };
 
+// cudaFuncAttributeMaxDynamicSharedMemorySize is process-wide per kernel, so
+// every preconditioner raises it to the device's opt-in maximum (a smaller
+// value set by a later preconditioner would break launches of an earlier one)
+static int smem_optin()
+{
+    int dev = 0, v = 48 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    return v;
+}
+
 static void free_precond(acch_precond *pc)
 {
     for (auto &C : pc->classes)
@@ -1615,7 +1626,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaMemcpy(pc->d_cell_src, src.data(), sizeof(long long) * src.size(), cudaMemcpyHostToDevice));
     }
     if (pc->use_smem && pc->apply_smem > 48 * 1024) {
-        const int b = (int)pc->apply_smem;
+        const int b = smem_optin();   // per-function state: never lower it under another live preconditioner
         const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<0, 32>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<1, 32>, attr, b));
@@ -1625,7 +1636,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 128>, attr, b));
     }
     if (pc->tma_mode && pc->tl.bytes() > 48 * 1024) {
-        const int b = (int)pc->tl.bytes();
+        const int b = smem_optin();   // per-function state: never lower it under another live preconditioner
         const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<0>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<1>, attr, b));
@@ -1654,7 +1665,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 128>, co, 100));
     }
     if (pc->warp_mode && pc->wl.bytes() > 48 * 1024) {
-        const int b = (int)pc->wl.bytes();
+        const int b = smem_optin();   // per-function state: never lower it under another live preconditioner
         const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 4>, attr, b));
@@ -1702,7 +1713,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
                                cudaMemcpyHostToDevice));
             PC_CUDA(cudaMemcpy(pc->d_grp_sub, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
             const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-            const int b = (int)pc->group_smem;
+            const int b = smem_optin();   // per-function state: never lower it under another live preconditioner
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 8>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 8>, attr, b));
