@@ -64,7 +64,8 @@ struct ClassDev {
     // the class-group solver's shared-memory image (byte offsets into meta):
     // f_ptr | f_base | b_ptr | b_base (int) | f_rows | b_rows | f_len | b_len | ecol (uint16)
     const unsigned char *meta;
-    int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol;
+    const int *lin;   // local cell -> storage offset from the box origin (boxes that do not wrap)
+    int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
 };
 
 struct ClassHost {
@@ -77,7 +78,8 @@ struct ClassHost {
     std::vector<int2> upd;
     std::vector<unsigned char> owned;
     std::vector<unsigned char> meta;   // ClassDev::meta image
-    int m_off[9] = {0};
+    std::vector<int> lin;
+    int m_off[13] = {0};
     int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
     void *dev_mem = nullptr;
     ClassDev dev;
@@ -551,15 +553,16 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
 // load's result (masked by `zero`, a runtime 0 the compiler cannot fold), so
 // ptxas cannot start consuming loads 0..5 before it has issued loads 6..11 --
 // the interleaving that otherwise costs a second memory round trip per level.
-template <int MAXW>
+template <int MAXW, int DBG = 0>   // DBG (experiments only): 1 = no factor loads, 2 = no y dependency
 __device__ __forceinline__ void sweep_level(const double4 *__restrict__ A, const unsigned short *__restrict__ ecol,
-                                            double2 *y, int base, int m, int len0, int len1, int i0, int i1,
-                                            bool backward, int lane, int zero, uint64_t pol)
+                                            const unsigned short *__restrict__ jo, double2 *y, int base, int m,
+                                            int len0, int len1, int i0, int i1, bool backward, int lane, int zero,
+                                            uint64_t pol)
 {
-    int offs[MAXW];
+    // jo[t]: level-relative slot offset of diagonal t (jagged layout; shared
+    // memory, warp-uniform), so lane q's slot t is base + jo[t] + q
     double4 a[MAXW];
     int c[MAXW];
-    int off = backward ? m : 0;
     double4 d0, d1;
     if (backward) {
         ldg4_pred(d0, A + base + lane, lane < m, pol);
@@ -567,33 +570,41 @@ __device__ __forceinline__ void sweep_level(const double4 *__restrict__ A, const
     }
 #pragma unroll
     for (int t = 0; t < MAXW; ++t) {
-        offs[t] = off;
-        ldg4_pred(a[t], A + base + off + lane, t < len0, pol);
-        c[t] = t < len0 ? ecol[base + off + lane] : 0;
-        off += __popc(__ballot_sync(0xffffffffu, len0 > t)) + __popc(__ballot_sync(0xffffffffu, len1 > t));
+        const int e = base + jo[t] + lane;
+        if (DBG == 1) a[t] = make_double4(1e-3 * e, 1e-3, 2e-3, 1e-3 * t);
+        else ldg4_pred(a[t], A + e, t < len0, pol);
+        c[t] = t < len0 ? ecol[e] : 0;
     }
     const int dep = __double2hiint(a[MAXW - 1].x) & zero;
     double2 acc0 = y[i0 + dep], acc1 = y[i1];
 #pragma unroll
     for (int t = 0; t < MAXW; ++t)
         if (t < len0) blk_sub(acc0, a[t], y[c[t]]);
+    if (DBG == 2) {   // loads only: fold them into one value, no FMA chain on y
+        double sink = 0.0;
+#pragma unroll
+        for (int t = 0; t < MAXW; ++t)
+            if (t < len0) sink += a[t].x + a[t].w;
+        if (lane < m && sink == 12345.678) y[i0] = make_double2(sink, sink);
+        __syncwarp();
+        return;
+    }
     if (len1 > 0) {
 #pragma unroll
         for (int t = 0; t < MAXW; ++t)
             if (t < len1) {
-                a[t] = ldg4(A + base + offs[t] + lane + 32);
-                c[t] = ecol[base + offs[t] + lane + 32];
+                const int e = base + jo[t] + lane + 32;
+                a[t] = ldg4(A + e);
+                c[t] = ecol[e];
             }
 #pragma unroll
         for (int t = 0; t < MAXW; ++t)
             if (t < len1) blk_sub(acc1, a[t], y[c[t]]);
     }
-    for (int t = MAXW;; ++t) {   // rows longer than MAXW slots (wrapped boxes, fill-in)
-        const unsigned b0 = __ballot_sync(0xffffffffu, len0 > t), b1 = __ballot_sync(0xffffffffu, len1 > t);
-        if (!(b0 | b1)) break;
-        if (t < len0) blk_sub(acc0, ldg4(A + base + off + lane), y[ecol[base + off + lane]]);
-        if (t < len1) blk_sub(acc1, ldg4(A + base + off + lane + 32), y[ecol[base + off + lane + 32]]);
-        off += __popc(b0) + __popc(b1);
+    for (int t = MAXW; __any_sync(0xffffffffu, len0 > t || len1 > t); ++t) {   // rows longer than MAXW slots
+        const int e = base + jo[t] + lane;
+        if (t < len0) blk_sub(acc0, ldg4(A + e), y[ecol[e]]);
+        if (t < len1) blk_sub(acc1, ldg4(A + e + 32), y[ecol[e + 32]]);
     }
     if (backward) {
         acc0 = make_double2(d0.x * acc0.x + d0.y * acc0.y, d0.z * acc0.x + d0.w * acc0.y);
@@ -605,7 +616,7 @@ __device__ __forceinline__ void sweep_level(const double4 *__restrict__ A, const
 }
 
 // one subdomain of a class group: gather, forward and backward sweeps, scatter
-template <int VARIANT, int MAXW>
+template <int VARIANT, int MAXW, int DBG = 0>
 __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev &C, const unsigned char *smem_meta,
                                              double2 *y, int s, const int4 *__restrict__ sub_origin,
                                              const long long *__restrict__ sub_off,
@@ -624,8 +635,13 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     const unsigned short *f_len = reinterpret_cast<const unsigned short *>(smem_meta + C.m_flen);
     const unsigned short *b_len = reinterpret_cast<const unsigned short *>(smem_meta + C.m_blen);
     const unsigned short *ecol = reinterpret_cast<const unsigned short *>(smem_meta + C.m_ecol);
+    const int *f_jp = reinterpret_cast<const int *>(smem_meta + C.m_fjp);
+    const int *b_jp = reinterpret_cast<const int *>(smem_meta + C.m_bjp);
+    const unsigned short *f_jo = reinterpret_cast<const unsigned short *>(smem_meta + C.m_fjo);
+    const unsigned short *b_jo = reinterpret_cast<const unsigned short *>(smem_meta + C.m_bjo);
     const uint64_t pol = evict_first_policy();
     const int4 o = sub_origin[s];
+    const long long obase = cell_at(g, o.x, o.y, zplane(g, o.z));   // used when o.w (no wrap)
     const double4 *__restrict__ A = vals + sub_off[s];
     const int nall = nlev + nlevb;
     auto prefetch_level = [&](int k) {
@@ -650,9 +666,15 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         for (int j = 0; j < GB; ++j) {
             const int l = l0 + j * 32 + lane;
             if (l < nloc) {
-                int gx, gy, gz;
-                local_to_global(g, C, o, l, gx, gy, gz);
-                v[j] = r[cell_at(g, gx, gy, zplane(g, gz))];
+                long long idx;
+                if (o.w) {
+                    idx = obase + __ldg(C.lin + l);
+                } else {
+                    int gx, gy, gz;
+                    local_to_global(g, C, o, l, gx, gy, gz);
+                    idx = cell_at(g, gx, gy, zplane(g, gz));
+                }
+                v[j] = r[idx];
                 if (VARIANT == 2 && !C.owned[l]) v[j] = make_double2(0.0, 0.0);
             }
         }
@@ -670,7 +692,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         const int len1 = lane + 32 < m ? f_len[r0 + lane + 32] : 0;
         const int i0 = lane < m ? f_rows[r0 + lane] : 0;
         const int i1 = lane + 32 < m ? f_rows[r0 + lane + 32] : 0;
-        sweep_level<MAXW>(A, ecol, y, f_bs[lev], m, len0, len1, i0, i1, false, lane, zero, pol);
+        sweep_level<MAXW, DBG>(A, ecol, f_jo + f_jp[lev], y, f_bs[lev], m, len0, len1, i0, i1, false, lane, zero, pol);
     }
     for (int lev = 0; lev < nlevb; ++lev) {
         if (lane == 0) prefetch_level(nlev + lev + pd);
@@ -680,14 +702,21 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         const int len1 = lane + 32 < m ? b_len[r0 + lane + 32] - 1 : 0;
         const int i0 = lane < m ? b_rows[r0 + lane] : 0;
         const int i1 = lane + 32 < m ? b_rows[r0 + lane + 32] : 0;
-        sweep_level<MAXW>(A, ecol, y, b_bs[lev], m, len0, len1, i0, i1, true, lane, zero, pol);
+        sweep_level<MAXW, DBG>(A, ecol, b_jo + b_jp[lev] + 1, y, b_bs[lev], m, len0, len1, i0, i1, true, lane, zero,
+                          pol);
     }
     if (VARIANT == 1) {
         for (int l = lane; l < nloc; l += 32) {
             if (!C.owned[l]) continue;
-            int gx, gy, gz;
-            local_to_global(g, C, o, l, gx, gy, gz);
-            z[cell_at(g, gx, gy, zplane(g, gz))] = y[l];
+            long long idx;
+            if (o.w) {
+                idx = obase + __ldg(C.lin + l);
+            } else {
+                int gx, gy, gz;
+                local_to_global(g, C, o, l, gx, gy, gz);
+                idx = cell_at(g, gx, gy, zplane(g, gz));
+            }
+            z[idx] = y[l];
         }
     } else {
         for (int l = lane; l < nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
@@ -695,7 +724,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     __syncwarp();   // y is reused by the warp's next subdomain
 }
 
-template <int VARIANT, int NW, int MAXW = 12>
+template <int VARIANT, int NW, int MAXW = 12, int DBG = 0>
 __global__ void __launch_bounds__(NW * 32, 1)
 apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *__restrict__ groups,
                    const int *__restrict__ grp_sub, const int4 *__restrict__ sub_origin,
@@ -717,7 +746,7 @@ apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *
     // one subdomain per warp (a loop over several per warp measured slower:
     // it pushes the sweep past 255 registers into spills)
     if (warp < G.z)
-        group_solve_one<VARIANT, MAXW>(g, C, smem_raw, y, grp_sub[G.y + warp], sub_origin, sub_off,
+        group_solve_one<VARIANT, MAXW, DBG>(g, C, smem_raw, y, grp_sub[G.y + warp], sub_origin, sub_off,
                                            sub_ext_off, vals, r, z, ext_out, zero, pd);
 }
 
@@ -1031,6 +1060,16 @@ void symbolic_fill(int n, const std::vector<int> &rp, const std::vector<int> &ci
     }
 }
 
+// a periodic box's relative coordinates are stored mod n (n - 1 for the cell
+// left of the origin); the signed representative makes origin + rel linear
+// for every box that does not actually wrap
+int signed_rel(const GridDev &g, int axis, int r)
+{
+    const int n = axis == 0 ? g.nx : (axis == 1 ? g.ny : g.nz);
+    if (axis == 2 && g.zg > 0) return r;   // slab z offsets are raw local planes
+    return (g.periodic && r > n / 2) ? r - n : r;
+}
+
 bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, const int own_len[3], int fill,
                  ClassHost &C, std::string &err)
 {
@@ -1192,6 +1231,12 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
         u.x = C.pos[u.x];
         u.y = C.pos[u.y];
     }
+    C.lin.assign(nloc, 0);
+    for (int l = 0; l < nloc; ++l) {
+        const int ix = l % lx, iy = (l / lx) % ly, iz = l / (lx * ly);
+        const long long rz = dim == 3 ? signed_rel(g, 2, rel[2][iz]) : 0;
+        C.lin[l] = (int)((rz * g.ny + signed_rel(g, 1, rel[1][iy])) * g.nx + signed_rel(g, 0, rel[0][ix]));
+    }
     C.owned.assign(nloc, 0);
     for (int l = 0; l < nloc; ++l) {
         const int ix[3] = {l % lx, (l / lx) % ly, l / (lx * ly)};
@@ -1221,6 +1266,12 @@ void build_meta(ClassHost &C)
     m[6] = seg(2 * (size_t)C.nloc);
     m[7] = seg(2 * (size_t)C.nloc);
     m[8] = seg(2 * (size_t)C.ell_total);
+    // jagged offsets (+ kJoPad zero entries so a sweep may read MAXW past the last level)
+    constexpr size_t kJoPad = 64;
+    m[9] = seg(sizeof(int) * C.f_jptr.size());
+    m[10] = seg(sizeof(int) * C.b_jptr.size());
+    m[11] = seg(2 * (C.f_joff.size() + kJoPad));
+    m[12] = seg(2 * (C.b_joff.size() + kJoPad));
     C.meta.assign(at, 0);
     auto put = [&](int o, const void *src, size_t bytes) { if (bytes) memcpy(C.meta.data() + o, src, bytes); };
     put(m[0], C.lev_ptr.data(), sizeof(int) * (nlev + 1));
@@ -1234,6 +1285,12 @@ void build_meta(ClassHost &C)
     std::vector<unsigned short> e16(C.ell_total);
     for (int t = 0; t < C.ell_total; ++t) e16[t] = C.ecol[t] < 0 ? 0 : (unsigned short)C.ecol[t];
     put(m[8], e16.data(), 2 * (size_t)C.ell_total);
+    put(m[9], C.f_jptr.data(), sizeof(int) * C.f_jptr.size());
+    put(m[10], C.b_jptr.data(), sizeof(int) * C.b_jptr.size());
+    std::vector<unsigned short> j16(C.f_joff.begin(), C.f_joff.end());
+    put(m[11], j16.data(), 2 * j16.size());
+    j16.assign(C.b_joff.begin(), C.b_joff.end());
+    put(m[12], j16.data(), 2 * j16.size());
 }
 
 acch_status upload_class(ClassHost &C)
@@ -1257,6 +1314,7 @@ acch_status upload_class(ClassHost &C)
     const size_t o_fjp = add(sizeof(int) * C.f_jptr.size()), o_fjo = add(sizeof(int) * std::max<size_t>(1, C.f_joff.size()));
     const size_t o_bjp = add(sizeof(int) * C.b_jptr.size()), o_bjo = add(sizeof(int) * std::max<size_t>(1, C.b_joff.size()));
     const size_t o_meta = add(C.meta.size());
+    const size_t o_lin = add(sizeof(int) * C.lin.size());
     ACCH_CUDA(cudaMalloc(&C.dev_mem, total));
     std::vector<unsigned char> h(total, 0);
     auto put = [&](size_t o, const void *src, size_t bytes) { if (bytes) memcpy(h.data() + o, src, bytes); };
@@ -1287,6 +1345,7 @@ acch_status upload_class(ClassHost &C)
     put(o_bjp, C.b_jptr.data(), sizeof(int) * C.b_jptr.size());
     put(o_bjo, C.b_joff.data(), sizeof(int) * C.b_joff.size());
     put(o_meta, C.meta.data(), C.meta.size());
+    put(o_lin, C.lin.data(), sizeof(int) * C.lin.size());
     ACCH_CUDA(cudaMemcpy(C.dev_mem, h.data(), total, cudaMemcpyHostToDevice));
     unsigned char *b = (unsigned char *)C.dev_mem;
     ClassDev &d = C.dev;
@@ -1324,6 +1383,7 @@ acch_status upload_class(ClassHost &C)
     d.b_jptr = (const int *)(b + o_bjp);
     d.b_joff = (const int *)(b + o_bjo);
     d.meta = b + o_meta;
+    d.lin = (const int *)(b + o_lin);
     d.meta_bytes = (int)C.meta.size();
     d.m_fbs = C.m_off[1];
     d.m_bptr = C.m_off[2];
@@ -1333,6 +1393,10 @@ acch_status upload_class(ClassHost &C)
     d.m_flen = C.m_off[6];
     d.m_blen = C.m_off[7];
     d.m_ecol = C.m_off[8];
+    d.m_fjp = C.m_off[9];
+    d.m_bjp = C.m_off[10];
+    d.m_fjo = C.m_off[11];
+    d.m_bjo = C.m_off[12];
     d.ell_total = C.ell_total;
     d.max_fwidth = C.max_fwidth;
     d.max_bwidth = C.max_bwidth;
@@ -1368,6 +1432,7 @@ struct acch_precond {
     int tma_mode = 0;      // apply_tma_kernel (TMA ring) in use
     // class-group solver (apply_group_kernel): groups of <= group_nw subdomains of one class
     int group_mode = 0, group_nw = 8, group_per_warp = 1, meta_max = 0, y_stride = 0;
+    int dbg = 0;   // ACCH_APPLY_DBG (timing experiments only; results are wrong): 1 no factor loads, 2 loads only
     size_t group_smem = 0;
     std::vector<int4> groups;
     int4 *d_groups = nullptr;
@@ -1491,7 +1556,17 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             cls = f->second;
         }
         pc->sub_class.push_back(cls);
-        pc->sub_origin.push_back(make_int4(lo3[0], lo3[1], lo3[2], 0));
+        // w = 1: every cell of the box sits at origin + rel without wrapping
+        // (slab z: ghost planes are stored), so its storage index is linear
+        int nowrap = 1;
+        for (int a = 0; a < dim; ++a) {
+            if (a == 2 && g.zg > 0) continue;
+            for (int r : rel[a]) {
+                const int d = signed_rel(g, a, r);
+                if (lo3[a] + d < 0 || lo3[a] + d >= nn[a]) nowrap = 0;
+            }
+        }
+        pc->sub_origin.push_back(make_int4(lo3[0], lo3[1], lo3[2], nowrap));
     }
     // offsets
     long long vo = 0, eo = 0;
@@ -1720,6 +1795,9 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 1>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 2>, attr, b));
+            if (const char *e = getenv("ACCH_APPLY_DBG")) pc->dbg = atoi(e);
         }
         if (getenv("ACCH_DEBUG"))
         {
@@ -1830,10 +1908,16 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     apply_group_kernel<V, NW><<<(unsigned)pc->groups.size(), NW * 32, pc->group_smem, ctx->stream>>>(ctx->g,         \
         pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, \
         (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride, 0, pc->pf_depth)
-#define GAPPLY(V)                                  \
-    do {                                           \
-        if (pc->group_nw == 8) GAPPLY_W(V, 8);     \
-        else GAPPLY_W(V, 4);                       \
+#define GAPPLY_DBG(D)                                                                                          \
+    apply_group_kernel<1, 8, 12, D><<<(unsigned)pc->groups.size(), 256, pc->group_smem, ctx->stream>>>(ctx->g,      \
+        pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, \
+        (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride, 0, pc->pf_depth)
+#define GAPPLY(V)                                                            \
+    do {                                                                     \
+        if (V == 1 && pc->group_nw == 8 && pc->dbg == 1) GAPPLY_DBG(1);      \
+        else if (V == 1 && pc->group_nw == 8 && pc->dbg == 2) GAPPLY_DBG(2); \
+        else if (pc->group_nw == 8) GAPPLY_W(V, 8);                          \
+        else GAPPLY_W(V, 4);                                                 \
     } while (0)
 #define WAPPLY(V)                                            \
     do {                                                     \
@@ -1871,6 +1955,7 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
 #undef WAPPLY_D
 #undef GAPPLY
 #undef GAPPLY_W
+#undef GAPPLY_DBG
 #undef TAPPLY
     ACCH_LAUNCHED(ctx);
     if (pc->variant != 1) {
