@@ -65,6 +65,8 @@ struct ClassDev {
     // f_ptr | f_base | b_ptr | b_base (int) | f_rows | b_rows | f_len | b_len | ecol (uint16)
     const unsigned char *meta;
     const int *lin;   // local cell -> storage offset from the box origin (boxes that do not wrap)
+    const int *own_list;   // local ids of the owned cells, ascending
+    int n_owned;
     int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
 };
 
@@ -78,7 +80,7 @@ struct ClassHost {
     std::vector<int2> upd;
     std::vector<unsigned char> owned;
     std::vector<unsigned char> meta;   // ClassDev::meta image
-    std::vector<int> lin;
+    std::vector<int> lin, own_list;
     int m_off[13] = {0};
     int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
     void *dev_mem = nullptr;
@@ -577,6 +579,8 @@ __device__ __forceinline__ void sweep_level(const double4 *__restrict__ A, const
     }
     const int dep = __double2hiint(a[MAXW - 1].x) & zero;
     double2 acc0 = y[i0 + dep], acc1 = y[i1];
+    // (an all-products-first ordering -- bitwise the same result -- measured
+    // 17% slower: it gathers y for inactive slots and lengthens the schedule)
 #pragma unroll
     for (int t = 0; t < MAXW; ++t)
         if (t < len0) blk_sub(acc0, a[t], y[c[t]]);
@@ -658,30 +662,40 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         prefetch_l2(A + lo, (unsigned)(hi - lo) * 32u);
     };
     if (lane < pd) prefetch_level(lane);
-    // gather r into y, GB independent loads in flight per lane
-    constexpr int GB = 4;
-    for (int l0 = 0; l0 < nloc; l0 += 32 * GB) {
-        double2 v[GB];
+    // gather r into y with many independent loads in flight per lane
+    if (o.w) {
+        constexpr int GB = 16;
+        for (int l0 = 0; l0 < nloc; l0 += 32 * GB) {
+            double2 v[GB];
 #pragma unroll
-        for (int j = 0; j < GB; ++j) {
-            const int l = l0 + j * 32 + lane;
-            if (l < nloc) {
-                long long idx;
-                if (o.w) {
-                    idx = obase + __ldg(C.lin + l);
-                } else {
-                    int gx, gy, gz;
-                    local_to_global(g, C, o, l, gx, gy, gz);
-                    idx = cell_at(g, gx, gy, zplane(g, gz));
-                }
-                v[j] = r[idx];
-                if (VARIANT == 2 && !C.owned[l]) v[j] = make_double2(0.0, 0.0);
+            for (int j = 0; j < GB; ++j) {
+                const int l = l0 + j * 32 + lane;
+                if (l < nloc) v[j] = r[obase + __ldg(C.lin + l)];
+            }
+#pragma unroll
+            for (int j = 0; j < GB; ++j) {
+                const int l = l0 + j * 32 + lane;
+                if (l < nloc) y[l] = (VARIANT == 2 && !C.owned[l]) ? make_double2(0.0, 0.0) : v[j];
             }
         }
+    } else {
+        constexpr int GB = 4;
+        for (int l0 = 0; l0 < nloc; l0 += 32 * GB) {
+            double2 v[GB];
 #pragma unroll
-        for (int j = 0; j < GB; ++j) {
-            const int l = l0 + j * 32 + lane;
-            if (l < nloc) y[l] = v[j];
+            for (int j = 0; j < GB; ++j) {
+                const int l = l0 + j * 32 + lane;
+                if (l < nloc) {
+                    int gx, gy, gz;
+                    local_to_global(g, C, o, l, gx, gy, gz);
+                    v[j] = r[cell_at(g, gx, gy, zplane(g, gz))];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < GB; ++j) {
+                const int l = l0 + j * 32 + lane;
+                if (l < nloc) y[l] = (VARIANT == 2 && !C.owned[l]) ? make_double2(0.0, 0.0) : v[j];
+            }
         }
     }
     __syncwarp();
@@ -706,8 +720,9 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
                           pol);
     }
     if (VARIANT == 1) {
-        for (int l = lane; l < nloc; l += 32) {
-            if (!C.owned[l]) continue;
+        // owned cells only (left RAS), from the class's owned-cell list
+        for (int k = lane; k < C.n_owned; k += 32) {
+            const int l = __ldg(C.own_list + k);
             long long idx;
             if (o.w) {
                 idx = obase + __ldg(C.lin + l);
@@ -1243,6 +1258,7 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
         bool own = true;
         for (int a = 0; a < dim; ++a) own = own && rel[a][ix[a]] >= 0 && rel[a][ix[a]] < own_len[a];
         C.owned[l] = own ? 1 : 0;
+        if (own) C.own_list.push_back(l);
     }
     return true;
 }
@@ -1315,6 +1331,7 @@ acch_status upload_class(ClassHost &C)
     const size_t o_bjp = add(sizeof(int) * C.b_jptr.size()), o_bjo = add(sizeof(int) * std::max<size_t>(1, C.b_joff.size()));
     const size_t o_meta = add(C.meta.size());
     const size_t o_lin = add(sizeof(int) * C.lin.size());
+    const size_t o_own = add(sizeof(int) * std::max<size_t>(1, C.own_list.size()));
     ACCH_CUDA(cudaMalloc(&C.dev_mem, total));
     std::vector<unsigned char> h(total, 0);
     auto put = [&](size_t o, const void *src, size_t bytes) { if (bytes) memcpy(h.data() + o, src, bytes); };
@@ -1346,6 +1363,7 @@ acch_status upload_class(ClassHost &C)
     put(o_bjo, C.b_joff.data(), sizeof(int) * C.b_joff.size());
     put(o_meta, C.meta.data(), C.meta.size());
     put(o_lin, C.lin.data(), sizeof(int) * C.lin.size());
+    put(o_own, C.own_list.data(), sizeof(int) * C.own_list.size());
     ACCH_CUDA(cudaMemcpy(C.dev_mem, h.data(), total, cudaMemcpyHostToDevice));
     unsigned char *b = (unsigned char *)C.dev_mem;
     ClassDev &d = C.dev;
@@ -1384,6 +1402,8 @@ acch_status upload_class(ClassHost &C)
     d.b_joff = (const int *)(b + o_bjo);
     d.meta = b + o_meta;
     d.lin = (const int *)(b + o_lin);
+    d.own_list = (const int *)(b + o_own);
+    d.n_owned = (int)C.own_list.size();
     d.meta_bytes = (int)C.meta.size();
     d.m_fbs = C.m_off[1];
     d.m_bptr = C.m_off[2];
