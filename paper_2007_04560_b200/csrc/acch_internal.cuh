@@ -85,7 +85,7 @@ struct acch_ctx {
     double *d_work = nullptr;         // 3 * 2N: z (precond out), r, t
     double *d_h = nullptr;            // small device array for Hessenberg column
     double *d_mvtmp = nullptr;        // two-pass matvec intermediate (dG_u, eta), 2 * nstore
-    int matvec_mode = 0;              // 0 fused z-marching kernel, 1 two-pass (ACCH_MATVEC=twopass)
+    int matvec_mode = 1;              // 1 two-pass (default, measured faster), 0 fused z-marching kernel (ACCH_MATVEC=fused)
     long long launches = 0;
     ProfState prof;
     // slab decomposition: rank topology and the host hooks that move ghost

@@ -16,6 +16,8 @@
 // (G_u, or dG_u; tile + 1 halo) in shared memory, so every input byte is read
 // from HBM once per sweep and the expensive entropy chords are evaluated only
 // on the tile + 1 halo.
+#include <string.h>
+
 #include "acch_internal.cuh"
 #include "physics.cuh"
 #include "reduce.cuh"
@@ -322,6 +324,7 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
     const int ze = (DIM == 3) ? min(zb + ZCHUNK, nz) : 1;
     const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
     const double hg = 0.5 * P.gamma;
+    const double idt = 1.0 / dt, irho = 1.0 / P.rho;
     const bool per = g.periodic != 0;
 
     auto load_plane = [&](int kk) {
@@ -428,8 +431,10 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
         const long long c = cell_at(g, x, y, zplane(g, k));
         const double S = __ldg(cS + c), D = __ldg(cD + c), Gv = __ldg(cGv + c);
         double2 out;
-        out.x = w0.x / dt - d1 - d2;
-        out.y = w0.y / dt + (C0 / P.rho) * (D * w0.x + (-0.5 * P.beta + S) * w0.y - hg * lapv) + (Gv / P.rho) * E0;
+        // reciprocals as in the reference's assembled blocks (idt = 1/dt,
+        // scheme.py:471); 1/rho once per thread instead of two divisions per cell
+        out.x = w0.x * idt - d1 - d2;
+        out.y = w0.y * idt + (C0 * irho) * (D * w0.x + (-0.5 * P.beta + S) * w0.y - hg * lapv) + (Gv * irho) * E0;
         yout[c] = out;
     };
 
@@ -503,18 +508,19 @@ __device__ __forceinline__ void cell_xyz(const GridDev &g, long long q, int &x, 
     z = (int)(q / ((long long)g.nx * g.ny));
 }
 
+// thread (x, y) of a 32 x 8 tile, blockIdx.z = plane: no index division
+constexpr int PTX = 32, PTY = 8;
+
 template <int DIM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(PTX * PTY)
 mv_pass1_kernel(GridDev g, ParamsDev P, const double *__restrict__ coef, const double2 *__restrict__ w,
-                double2 *__restrict__ T, int zlo, long long ncells)
+                double2 *__restrict__ T, int zlo)
 {
     // planes zlo .. : in slab mode also the first ghost plane past an
     // interior slab boundary, which pass 2 reads as a z-neighbour
-    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (q >= ncells) return;
-    int x, y, z;
-    cell_xyz(g, q, x, y, z);
-    z += zlo;
+    const int x = blockIdx.x * PTX + threadIdx.x, y = blockIdx.y * PTY + threadIdx.y;
+    if (x >= g.nx || y >= g.ny) return;
+    const int z = (int)blockIdx.z + zlo;
     const int zs = zplane(g, z);
     const long long c = cell_at(g, x, y, zs);
     const long long N = g.nstore;
@@ -534,14 +540,13 @@ mv_pass1_kernel(GridDev g, ParamsDev P, const double *__restrict__ coef, const d
 }
 
 template <int DIM>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(PTX * PTY)
 mv_pass2_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef, const double2 *__restrict__ w,
                 const double2 *__restrict__ T, double2 *__restrict__ yout)
 {
-    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-    if (q >= g.n) return;
-    int x, y, z;
-    cell_xyz(g, q, x, y, z);
+    const int x = blockIdx.x * PTX + threadIdx.x, y = blockIdx.y * PTY + threadIdx.y;
+    if (x >= g.nx || y >= g.ny) return;
+    const int z = (int)blockIdx.z;
     const int zs = zplane(g, z);
     const long long c = cell_at(g, x, y, zs);
     const long long N = g.nstore;
@@ -580,8 +585,9 @@ mv_pass2_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ co
     const double S = __ldg(coef + CO_S * N + c), D = __ldg(coef + CO_D * N + c), Gv = __ldg(coef + CO_GV * N + c);
     const double hg = 0.5 * P.gamma;
     double2 out;
-    out.x = w0.x / dt - d1 - d2;
-    out.y = w0.y / dt + (C0 / P.rho) * (D * w0.x + (-0.5 * P.beta + S) * w0.y - hg * lapv) + (Gv / P.rho) * t0.y;
+    const double idt = 1.0 / dt, irho = 1.0 / P.rho;   // reciprocals (see matvec_kernel)
+    out.x = w0.x * idt - d1 - d2;
+    out.y = w0.y * idt + (C0 * irho) * (D * w0.x + (-0.5 * P.beta + S) * w0.y - hg * lapv) + (Gv * irho) * t0.y;
     yout[c] = out;
 }
 
@@ -808,19 +814,19 @@ static acch_status launch_matvec_twopass(acch_ctx *ctx, const double *coef, doub
 {
     if (!ctx->d_mvtmp) ACCH_CUDA(cudaMalloc(&ctx->d_mvtmp, sizeof(double) * 2 * ctx->g.nstore));
     const GridDev &g = ctx->g;
-    const unsigned nb = (unsigned)((g.n + 255) / 256);
     const int zlo = (g.zg && !g.zwall_lo) ? -1 : 0, zhi = g.nz + ((g.zg && !g.zwall_hi) ? 1 : 0);
-    const long long n1 = (long long)(zhi - zlo) * g.nx * g.ny;
-    const unsigned nb1 = (unsigned)((n1 + 255) / 256);
+    const dim3 blk(PTX, PTY);
+    const dim3 g1((g.nx + PTX - 1) / PTX, (g.ny + PTY - 1) / PTY, g.dim == 3 ? zhi - zlo : 1);
+    const dim3 g2((g.nx + PTX - 1) / PTX, (g.ny + PTY - 1) / PTY, g.dim == 3 ? g.nz : 1);
     if (g.dim == 3) {
-        mv_pass1_kernel<3><<<nb1, 256, 0, ctx->stream>>>(g, ctx->p, coef, (const double2 *)w, (double2 *)ctx->d_mvtmp,
-                                                         zlo, n1);
-        mv_pass2_kernel<3><<<nb, 256, 0, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
+        mv_pass1_kernel<3><<<g1, blk, 0, ctx->stream>>>(g, ctx->p, coef, (const double2 *)w, (double2 *)ctx->d_mvtmp,
+                                                        zlo);
+        mv_pass2_kernel<3><<<g2, blk, 0, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
                                                         (const double2 *)ctx->d_mvtmp, (double2 *)y);
     } else {
-        mv_pass1_kernel<2><<<nb, 256, 0, ctx->stream>>>(g, ctx->p, coef, (const double2 *)w, (double2 *)ctx->d_mvtmp,
-                                                        0, g.n);
-        mv_pass2_kernel<2><<<nb, 256, 0, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
+        mv_pass1_kernel<2><<<g1, blk, 0, ctx->stream>>>(g, ctx->p, coef, (const double2 *)w, (double2 *)ctx->d_mvtmp,
+                                                        0);
+        mv_pass2_kernel<2><<<g2, blk, 0, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
                                                         (const double2 *)ctx->d_mvtmp, (double2 *)y);
     }
     ctx->launches += 1;
@@ -830,6 +836,10 @@ static acch_status launch_matvec_twopass(acch_ctx *ctx, const double *coef, doub
 
 acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
+    // ACCH_MATVEC=fused selects the z-marching kernel (read per call so tests
+    // can exercise both forms on one context)
+    const char *mode = getenv("ACCH_MATVEC");
+    ctx->matvec_mode = (mode && strcmp(mode, "fused") == 0) ? 0 : 1;
     if (ctx->matvec_mode == 1) {
         ProfScope prof_scope(ctx, PC_MATVEC, 88.0 * ctx->g.n);
         return launch_matvec_twopass(ctx, coef, dt, w, y);

@@ -73,8 +73,10 @@ def test_residual_matches_reference(tag):
     assert np.max(np.abs(F0 - z["F0"])) <= 1e-12 * np.max(np.abs(z["F0"]))
 
 
+@pytest.mark.parametrize("form", ["twopass", "fused"])
 @pytest.mark.parametrize("tag", STENCIL)
-def test_jacobian_matvec_matches_reference(tag):
+def test_jacobian_matvec_matches_reference(tag, form, monkeypatch):
+    monkeypatch.setenv("ACCH_MATVEC", form)
     z = golden(f"stencil_{tag}.npz")
     g = grid_of(z)
     prob = StepProblem.create(g, PARAMS, st(g, z["uo"], z["vo"]), float(z["dt"]))
@@ -287,15 +289,17 @@ def test_simulate_adaptive_3d_neumann_with_retries_matches_reference():
     _check_sim(*_run_sim("c3small"))
 
 
-@pytest.mark.parametrize("mode", ["tma", "warp", "cta"])
+@pytest.mark.parametrize("mode", ["group", "group4", "tma", "warp", "cta"])
 @pytest.mark.parametrize("solver", ["ilu0", "ilu1"])
 def test_schwarz_wide_boxes_match_oracle(mode, solver, monkeypatch):
-    """Boxes whose levels are wider than a warp, with each of the three
-    subdomain solvers (TMA-ring warp, plain warp, CTA-wide) forced, against
-    the oracle's scalar ILU on kron(P, 1)."""
+    """Boxes whose levels are wider than a warp, with each subdomain solver
+    (class-group with 8 or 4 warps per CTA, TMA-ring warp, plain warp,
+    CTA-wide) forced, against the oracle's scalar ILU on kron(P, 1)."""
     from oracle import acch_oracle as O
     monkeypatch.setenv("ACCH_SCHWARZ_BLOCK_SOLVER", "1" if mode == "cta" else "0")
     monkeypatch.setenv("ACCH_SCHWARZ_TMA", "1" if mode == "tma" else "0")
+    monkeypatch.setenv("ACCH_GROUP", "1" if mode.startswith("group") else "0")
+    monkeypatch.setenv("ACCH_GROUP_WARPS", "4" if mode == "group4" else "8")
     rng = np.random.default_rng(77)
     counts = (16, 14, 12)
     g = Grid(counts, (1.0, 1.0, 1.0), BoundaryCondition.NEUMANN)
