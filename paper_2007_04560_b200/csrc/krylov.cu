@@ -21,6 +21,23 @@
 
 namespace {
 
+// Predicated 16-byte read-only load into an output pair (undefined when
+// !pred; such values are never used).  With the first use of a batch tied to
+// the LAST load's result (see anchor below), ptxas issues the whole batch
+// before the dependent chain instead of interleaving load / FMA pairs, which
+// serialises the round trips at the occupancy these kernels run at.
+__device__ __forceinline__ double2 ldg2_pred(const double2 *p, bool pred)
+{
+    double2 v;
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\t"
+                 "@q ld.global.nc.v2.f64 {%0, %1}, [%2];\n\t}"
+                 : "=d"(v.x), "=d"(v.y)
+                 : "l"(p), "r"((unsigned)pred));
+    return v;
+}
+// 0 at run time (zero == 0), but data-dependent on v as far as ptxas knows
+__device__ __forceinline__ int anchor(const double2 &v, int zero) { return __double2hiint(v.x) & zero; }
+
 // All vector kernels stream double2 (16 B) per thread; n (= 2N) is even.
 constexpr int kVecBlocks = 148 * 8;   // fixed grid: 8 CTAs of 256 threads per SM, deterministic reductions
 
@@ -91,7 +108,7 @@ __host__ __device__ __forceinline__ int gslot(int s) { return (s / MG) * (MG + 1
 template <int NS>
 __global__ void __launch_bounds__(kRedThreads)
 mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ h, double *__restrict__ w,
-               long long n, double *partials, unsigned int *counter, double *result, int h_grouped)
+               long long n, double *partials, unsigned int *counter, double *result, int h_grouped, int zero)
 {
     __shared__ double sh[NS];
     if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[h_grouped ? gslot(threadIdx.x) : threadIdx.x] : 0.0;
@@ -100,6 +117,8 @@ mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *
     const long long n2 = n >> 1;
     double2 *__restrict__ w2 = reinterpret_cast<double2 *>(w);
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        // (plain loop: at this kernel's occupancy, batching the loads with an
+        // anchor measured 2x slower -- see profiles/r01_krylov.txt)
         double2 wi = w2[i];
 #pragma unroll
         for (int s = 0; s < NS; ++s)
@@ -127,7 +146,8 @@ mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *
 template <int NS>
 __global__ void __launch_bounds__(kRedThreads)
 mupdate_mdot_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ h,
-                    double *__restrict__ w, long long n, double *partials, unsigned int *counter, double *result)
+                    double *__restrict__ w, long long n, double *partials, unsigned int *counter, double *result,
+                    int zero)
 {
     __shared__ double sh[NS];
     if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[gslot(threadIdx.x)] : 0.0;
@@ -142,14 +162,15 @@ mupdate_mdot_kernel(const double *__restrict__ V, long long ld, int m, const dou
         // for both the update and the projections)
         double2 v[NS];
 #pragma unroll
-        for (int s = 0; s < NS; ++s)
-            v[s] = s < m ? __ldg(reinterpret_cast<const double2 *>(V + s * ld) + i) : make_double2(0.0, 0.0);
+        for (int s = 0; s < NS; ++s) v[s] = ldg2_pred(reinterpret_cast<const double2 *>(V + s * ld) + i, s < m);
         double2 wi = w2[i];
+        const int a0 = anchor(v[NS - 1], zero);
 #pragma unroll
         for (int s = 0; s < NS; ++s)
             if (s < m) {
-                wi.x -= sh[s] * v[s].x;
-                wi.y -= sh[s] * v[s].y;
+                const double hs = sh[s + (s == 0 ? a0 : 0)];
+                wi.x -= hs * v[s].x;
+                wi.y -= hs * v[s].y;
             }
         w2[i] = wi;
         acc[0] += wi.x * wi.x + wi.y * wi.y;
@@ -161,6 +182,99 @@ mupdate_mdot_kernel(const double *__restrict__ V, long long ld, int m, const dou
 #pragma unroll
     for (int s = 0; s <= NS; ++s) ops[s] = RED_SUM;
     reduce_finish<NS + 1>(acc, ops, partials, counter, result);
+}
+
+// The same fused pass for 17..32 basis vectors, with each element handled by
+// a lane PAIR: the even lane holds V_0..V_15, the odd lane V_16..V_31, so the
+// basis values stay in registers (64 per lane instead of 128) at twice the
+// occupancy.  Each lane forms its half of V h (a chain in basis order); the
+// halves are exchanged with one shuffle and w_new = (w - [V h]_lo) - [V h]_hi
+// on both lanes.  (A regrouping of the update's sums: the values differ from
+// the single-lane kernel's in the last bits, as any CGS ordering does from the
+// reference's MGS; the reductions are regrouped too.)
+// result[0] = ||w_new||^2, result[1 + s] = <V_s, w_new>.  h is in gslot layout.
+__global__ void __launch_bounds__(kRedThreads, 2)
+mupdate_mdot32_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ h,
+                      double *__restrict__ w, long long n, double *partials, unsigned int *counter,
+                      double *result, int zero)
+{
+    constexpr int H = 16, NV = 2 * H + 1;   // values reduced: norm + 32 dots
+    __shared__ double sh[2 * H];
+    __shared__ double red[kRedThreads / 32][2][H + 1];
+    __shared__ bool is_last;
+    if (threadIdx.x < 2 * H) sh[threadIdx.x] = threadIdx.x < m ? h[gslot(threadIdx.x)] : 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = threadIdx.x & 1;
+    const int s0 = half * H;
+    double acc[H + 1];
+#pragma unroll
+    for (int k = 0; k <= H; ++k) acc[k] = 0.0;
+    const long long n2 = n >> 1;
+    double2 *__restrict__ w2 = reinterpret_cast<double2 *>(w);
+    const long long pairs = (long long)gridDim.x * (blockDim.x >> 1);
+    // warp-uniform trip count (the pair shuffles need every lane present)
+    for (long long base = blockIdx.x * (long long)(blockDim.x >> 1) + warp * 16; base < n2; base += pairs) {
+        const long long i = base + (lane >> 1);
+        const bool ok = i < n2;
+        double2 v[H];
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+            v[k] = ldg2_pred(reinterpret_cast<const double2 *>(V + (s0 + k) * ld) + i, ok && s0 + k < m);
+        double2 wi = ok ? w2[i] : make_double2(0.0, 0.0);
+        const int a0 = anchor(v[H - 1], zero);
+        double2 part = make_double2(0.0, 0.0);   // this lane's half of V h
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+            if (s0 + k < m) {
+                const double hs = sh[s0 + k + (k == 0 ? a0 : 0)];
+                part.x += hs * v[k].x;
+                part.y += hs * v[k].y;
+            }
+        double2 other;
+        other.x = __shfl_xor_sync(0xffffffffu, part.x, 1);
+        other.y = __shfl_xor_sync(0xffffffffu, part.y, 1);
+        const double2 lo = half == 0 ? part : other, hi = half == 0 ? other : part;
+        wi.x = (wi.x - lo.x) - hi.x;
+        wi.y = (wi.y - lo.y) - hi.y;
+        if (half == 1) {
+            if (ok) w2[i] = wi;
+            acc[0] += wi.x * wi.x + wi.y * wi.y;   // 0 when !ok
+        }
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+            if (s0 + k < m) acc[1 + k] += v[k].x * wi.x + v[k].y * wi.y;
+    }
+    // reduce even lanes and odd lanes separately (xor offsets 16..2)
+#pragma unroll
+    for (int off = 16; off >= 2; off >>= 1)
+#pragma unroll
+        for (int k = 0; k <= H; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+    if (lane < 2)
+#pragma unroll
+        for (int k = 0; k <= H; ++k) red[warp][lane][k] = acc[k];
+    __syncthreads();
+    // value j: 0 = norm (odd lanes), 1 + s = dot s (half s / H, slot s % H)
+    const long long nb = gridDim.x;
+    if (threadIdx.x < NV) {
+        const int j = threadIdx.x;
+        const int hh = j == 0 ? 1 : (j - 1) / H, kk = j == 0 ? 0 : 1 + (j - 1) % H;
+        double t = 0.0;
+        for (int q = 0; q < kRedThreads / 32; ++q) t += red[q][hh][kk];
+        partials[j * nb + blockIdx.x] = t;
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(counter, 1u) == (unsigned int)(nb - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    if (threadIdx.x < NV) {
+        double t = 0.0;
+        for (long long b = 0; b < nb; ++b) t += __ldcg(partials + threadIdx.x * nb + b);
+        result[threadIdx.x] = t;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
 }
 
 template <int NS>
@@ -253,7 +367,7 @@ static acch_status mupdate_to(acch_ctx *ctx, const double *V, long long ld, int 
     const int G = rgrid(n);
 #define MUP_CASE(NS) \
     mupdate_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter, out, \
-                                                           h_grouped);
+                                                           h_grouped, 0);
     if (m <= 4) { MUP_CASE(4) }
     else if (m <= 8) { MUP_CASE(8) }
     else if (m <= 16) { MUP_CASE(16) }
@@ -271,12 +385,15 @@ static acch_status mupdate_mdot_to(acch_ctx *ctx, const double *V, long long ld,
     ProfScope prof_scope(ctx, PC_KUPDATE, 8.0 * (m + 2) * n);
     const int G = rgrid(n);
 #define MUD_CASE(NS) \
-    mupdate_mdot_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter, out);
+    mupdate_mdot_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter, out, \
+                                                                0);
     if (m <= 4) { MUD_CASE(4) }
     else if (m <= 8) { MUD_CASE(8) }
     else if (m <= 16) { MUD_CASE(16) }
-    else if (m <= 32) { MUD_CASE(32) }
-    else { acch_set_error("mupdate_mdot: too many vectors"); return ACCH_ERR_INVALID_ARG; }
+    else if (m <= 32) {
+        mupdate_mdot32_kernel<<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter,
+                                                                   out, 0);
+    } else { acch_set_error("mupdate_mdot: too many vectors"); return ACCH_ERR_INVALID_ARG; }
 #undef MUD_CASE
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
