@@ -699,88 +699,8 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         }
     }
     __syncwarp();
-    if (DBG == 4) {
-        // software-pipelined sweeps: level k+1's row descriptors, slot offsets
-        // and column ids (all y-independent, from shared memory) are read
-        // while level k's factor loads are in flight
-        struct LevD {
-            int base, m, len0, len1, i0, i1, bwd;
-            const unsigned short *jo;
-        };
-        auto describe = [&](int k) {
-            LevD d;
-            d.bwd = k >= nlev;
-            const int lv = d.bwd ? k - nlev : k;
-            const int *ptr = d.bwd ? b_ptr : f_ptr;
-            const unsigned short *rows = d.bwd ? b_rows : f_rows, *lens = d.bwd ? b_len : f_len;
-            const int r0 = ptr[lv];
-            d.m = ptr[lv + 1] - r0;
-            d.base = d.bwd ? b_bs[lv] : f_bs[lv];
-            d.jo = d.bwd ? b_jo + b_jp[lv] + 1 : f_jo + f_jp[lv];
-            d.len0 = lane < d.m ? lens[r0 + lane] - d.bwd : 0;
-            d.len1 = lane + 32 < d.m ? lens[r0 + lane + 32] - d.bwd : 0;
-            d.i0 = lane < d.m ? rows[r0 + lane] : 0;
-            d.i1 = lane + 32 < d.m ? rows[r0 + lane + 32] : 0;
-            return d;
-        };
-        const int K = nlev + nlevb;
-        LevD cur = describe(0);
-        int e[MAXW], c[MAXW];
-#pragma unroll
-        for (int t = 0; t < MAXW; ++t) {
-            e[t] = cur.base + cur.jo[t] + lane;
-            c[t] = t < cur.len0 ? ecol[e[t]] : 0;
-        }
-        for (int k = 0; k < K; ++k) {
-            if (lane == 0) prefetch_level(k + pd);
-            double4 a[MAXW], d0, d1;
-            if (cur.bwd) {
-                ldg4_pred(d0, A + cur.base + lane, lane < cur.m, pol);
-                ldg4_pred(d1, A + cur.base + lane + 32, lane + 32 < cur.m, pol);
-            }
-#pragma unroll
-            for (int t = 0; t < MAXW; ++t) ldg4_pred(a[t], A + e[t], t < cur.len0, pol);
-            LevD nxt = cur;
-            int en[MAXW], cn[MAXW];
-            if (k + 1 < K) nxt = describe(k + 1);
-#pragma unroll
-            for (int t = 0; t < MAXW; ++t) {
-                en[t] = nxt.base + nxt.jo[t] + lane;
-                cn[t] = (k + 1 < K && t < nxt.len0) ? ecol[en[t]] : 0;
-            }
-            const int dep = __double2hiint(a[MAXW - 1].x) & zero;
-            double2 acc0 = y[cur.i0 + dep], acc1 = y[cur.i1];
-#pragma unroll
-            for (int t = 0; t < MAXW; ++t)
-                if (t < cur.len0) blk_sub(acc0, a[t], y[c[t]]);
-            if (cur.len1 > 0) {
-#pragma unroll
-                for (int t = 0; t < MAXW; ++t)
-                    if (t < cur.len1) {
-                        const int q = e[t] + 32;
-                        blk_sub(acc1, ldg4(A + q), y[ecol[q]]);
-                    }
-            }
-            for (int t = MAXW; __any_sync(0xffffffffu, cur.len0 > t || cur.len1 > t); ++t) {
-                const int q = cur.base + cur.jo[t] + lane;
-                if (t < cur.len0) blk_sub(acc0, ldg4(A + q), y[ecol[q]]);
-                if (t < cur.len1) blk_sub(acc1, ldg4(A + q + 32), y[ecol[q + 32]]);
-            }
-            if (cur.bwd) {
-                acc0 = make_double2(d0.x * acc0.x + d0.y * acc0.y, d0.z * acc0.x + d0.w * acc0.y);
-                acc1 = make_double2(d1.x * acc1.x + d1.y * acc1.y, d1.z * acc1.x + d1.w * acc1.y);
-            }
-            if (lane < cur.m) y[cur.i0] = acc0;
-            if (lane + 32 < cur.m) y[cur.i1] = acc1;
-            __syncwarp();
-            cur = nxt;
-#pragma unroll
-            for (int t = 0; t < MAXW; ++t) {
-                e[t] = en[t];
-                c[t] = cn[t];
-            }
-        }
-    } else {
+    // (software-pipelining level k+1's shared-memory index reads under level
+    // k's loads measured 1% slower: profiles/r01_apply_sweeps_group.txt)
     for (int lev = 0; lev < nlev; ++lev) {
         if (lane == 0) prefetch_level(lev + pd);
         const int r0 = f_ptr[lev], m = f_ptr[lev + 1] - r0;
@@ -800,7 +720,6 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         const int i1 = lane + 32 < m ? b_rows[r0 + lane + 32] : 0;
         sweep_level<MAXW, DBG>(A, ecol, b_jo + b_jp[lev] + 1, y, b_bs[lev], m, len0, len1, i0, i1, true, lane, zero,
                           pol);
-    }
     }
     if (VARIANT == 1) {
         // owned cells only (left RAS), from the class's owned-cell list
@@ -1900,7 +1819,6 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 1>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 2>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 4>, attr, b));
             if (const char *e = getenv("ACCH_APPLY_DBG")) pc->dbg = atoi(e);
         }
         if (getenv("ACCH_DEBUG"))
@@ -2020,7 +1938,6 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     do {                                                                     \
         if (V == 1 && pc->group_nw == 8 && pc->dbg == 1) GAPPLY_DBG(1);      \
         else if (V == 1 && pc->group_nw == 8 && pc->dbg == 2) GAPPLY_DBG(2); \
-        else if (V == 1 && pc->group_nw == 8 && pc->dbg == 4) GAPPLY_DBG(4); \
         else if (pc->group_nw == 8) GAPPLY_W(V, 8);                          \
         else GAPPLY_W(V, 4);                                                 \
     } while (0)
