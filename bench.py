@@ -223,6 +223,19 @@ def run_reference(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 
+def measured_traffic(category):
+    """DRAM bytes (read + write) per launch of the dominant kernel category
+    from the committed `ncu --set full` captures (profiles/traffic.json,
+    written by tools/ncu_traffic.py); None when not captured."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if category not in ("precond_apply", "matvec") or not os.path.exists(path):
+        return None, None
+    ent = [v for v in json.load(open(path)).values() if v.get("category") == category]
+    if not ent:
+        return None, None
+    return sum(v["traffic_bytes"] for v in ent), "ncu --set full: " + ", ".join(v["source"] for v in ent)
+
+
 def microbench_stencils(args, stepper, peaks, reps=20):
     """Standalone residual and Jacobian-matvec launches at the current state
     (U' = U^n + 1e-4 N(0,1): the chords take the series branch)."""
@@ -381,8 +394,9 @@ def run_ours(args):
                    "frac": round(gbs / peaks["hbm_gbs"], 4)}
     dom = max(cats, key=lambda k: cats[k]["ms"]) if cats else "matvec"
     d = cats.get(dom, {})
+    traffic, traffic_src = measured_traffic(dom)
     roofline = {"bound": "hbm", "kernel": dom, "achieved": d.get("gb_s"), "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": d.get("frac"), "traffic": None,
+                "unit": "GB/s", "frac": d.get("frac"), "traffic": traffic, "traffic_source": traffic_src,
                 "avg_launch_ms": (d["ms"] / d["launches"]) if d else None,
                 "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "peak_source": peaks["source"]}
 
