@@ -28,16 +28,17 @@ __device__ __forceinline__ int stencil_offset_id(int dx, int dy, int dz)
 }
 
 
-template <int DIM>
-__device__ __forceinline__ void jac_row_blocks(const GridDev &g, const ParamsDev &P, double dt, const double *__restrict__ coef,
-                               int x, int y, int z, double (*blk)[4], int noff)
+// The row's contributions in a fixed order: emit(o, comp, value) adds value
+// to component comp (0 uu, 1 uv, 2 vu, 3 vv) of the block at stencil offset o.
+template <int DIM, typename Emit>
+__device__ __forceinline__ void jac_row_emit(const GridDev &g, const ParamsDev &P, double dt, const double *__restrict__ coef,
+                                             int x, int y, int z, Emit &&emit)
 {
     // x, y wrap or clamp; z stays a raw local plane index (it may address a
     // slab ghost plane) and is mapped to storage by zplane()
     const long long N = g.nstore;
     const int cc[3] = {x, y, z};
     const int nn[3] = {g.nx, g.ny, g.nz};
-    for (int o = 0; o < noff; ++o) blk[o][0] = blk[o][1] = blk[o][2] = blk[o][3] = 0.0;
     auto cid = [&](const int (&q)[3]) -> long long { return cell_at(g, q[0], q[1], zplane(g, q[2])); };
     auto offid = [&](int dx, int dy, int dz) { return stencil_offset_id<DIM>(dx, dy, dz); };
     // neighbour m = c + e_a s exists (periodic, inside the box, or across a slab boundary)
@@ -94,16 +95,16 @@ __device__ __forceinline__ void jac_row_blocks(const GridDev &g, const ParamsDev
                 lsum += g.ih2[a];
                 const int o = offid(mo[3 * j] + (a == 0 ? s : 0), mo[3 * j + 1] + (a == 1 ? s : 0),
                                     mo[3 * j + 2] + (a == 2 ? s : 0));
-                blk[o][0] += -wdg[j] * hg * g.ih2[a];
+                emit(o, 0, -wdg[j] * hg * g.ih2[a]);
             }
         }
         const int om = offid(mo[3 * j], mo[3 * j + 1], mo[3 * j + 2]);
         const double A = -0.5 * P.alpha + coef[CO_S * N + cm] + hg * lsum;
-        blk[om][0] += wdg[j] * A + weta[j] * 0.5 * coef[CO_CU * N + cm];
-        blk[om][1] += wdg[j] * coef[CO_D * N + cm] + weta[j] * 0.5 * coef[CO_CV * N + cm];
+        emit(om, 0, wdg[j] * A + weta[j] * 0.5 * coef[CO_CU * N + cm]);
+        emit(om, 1, wdg[j] * coef[CO_D * N + cm] + weta[j] * 0.5 * coef[CO_CV * N + cm]);
     }
     const int o0 = offid(0, 0, 0);
-    blk[o0][0] += 1.0 / dt;
+    emit(o0, 0, 1.0 / dt);
     // v row
     const double cr = cb0 / P.rho;
     const double S0 = coef[CO_S * N + c0], D0 = coef[CO_D * N + c0], Gv0 = coef[CO_GV * N + c0];
@@ -113,10 +114,18 @@ __device__ __forceinline__ void jac_row_blocks(const GridDev &g, const ParamsDev
             if (!valid(cc, a, s)) continue;
             lsum0 += g.ih2[a];
             const int o = offid(a == 0 ? s : 0, a == 1 ? s : 0, a == 2 ? s : 0);
-            blk[o][3] += -hg * cr * g.ih2[a];
+            emit(o, 3, -hg * cr * g.ih2[a]);
         }
     }
-    blk[o0][2] += cr * D0 + Gv0 * coef[CO_CU * N + c0] / (2.0 * P.rho);
-    blk[o0][3] += 1.0 / dt + cr * (-0.5 * P.beta + S0) + hg * cr * lsum0 + Gv0 * coef[CO_CV * N + c0] / (2.0 * P.rho);
+    emit(o0, 2, cr * D0 + Gv0 * coef[CO_CU * N + c0] / (2.0 * P.rho));
+    emit(o0, 3, 1.0 / dt + cr * (-0.5 * P.beta + S0) + hg * cr * lsum0 + Gv0 * coef[CO_CV * N + c0] / (2.0 * P.rho));
+}
+
+template <int DIM>
+__device__ __forceinline__ void jac_row_blocks(const GridDev &g, const ParamsDev &P, double dt, const double *__restrict__ coef,
+                               int x, int y, int z, double (*blk)[4], int noff)
+{
+    for (int o = 0; o < noff; ++o) blk[o][0] = blk[o][1] = blk[o][2] = blk[o][3] = 0.0;
+    jac_row_emit<DIM>(g, P, dt, coef, x, y, z, [&](int o, int c, double v) { blk[o][c] += v; });
 }
 

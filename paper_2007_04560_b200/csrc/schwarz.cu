@@ -67,6 +67,10 @@ struct ClassDev {
     const int *lin;   // local cell -> storage offset from the box origin (boxes that do not wrap)
     const int *own_list;   // local ids of the owned cells, ascending
     int n_owned;
+    // row-local forms for factor_warp_kernel: J stencil entry -> index within
+    // the row's CSR pattern, update target -> index within row i's pattern
+    const int *jmap_local, *upd_dl;
+    int rmax;   // longest pattern row
     int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
 };
 
@@ -80,7 +84,8 @@ struct ClassHost {
     std::vector<int2> upd;
     std::vector<unsigned char> owned;
     std::vector<unsigned char> meta;   // ClassDev::meta image
-    std::vector<int> lin, own_list;
+    std::vector<int> lin, own_list, jmap_local, upd_dl;
+    int rmax = 0;
     int m_off[13] = {0};
     int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
     void *dev_mem = nullptr;
@@ -176,6 +181,96 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
             A[pd] = make_double4(D.w / det, -D.y / det, -D.z / det, D.x / det);
         }
         __syncthreads();
+    }
+}
+
+// Warp-per-subdomain factorisation (default when a row fits the row buffer).
+// Lane q owns row q of the current level: its pattern row is assembled from
+// the 7 coefficient planes straight into a shared-memory row buffer (no
+// zero-fill pass over the factor array), eliminated there -- the IKJ updates
+// read the finished U rows of earlier levels from global memory (L2-resident:
+// a row reaches at most ~2 box planes back) in batches of 8 loads -- and
+// written to its factor slots once.  The factor array therefore sees one
+// write per block instead of a read-modify-write per update.
+template <int DIM, int NW>
+__global__ void __launch_bounds__(NW * 32)
+factor_warp_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
+                   const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
+                   const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
+                   double4 *__restrict__ vals, int *__restrict__ bad_row, long long nsub, int rstride)
+{
+    constexpr int NOFF = DIM == 3 ? 25 : 13;
+    constexpr int UB = 8;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const long long s = (long long)blockIdx.x * NW + warp;
+    if (s >= nsub) return;
+    const ClassDev &C = classes[sub_class[s]];
+    const int4 o = sub_origin[s];
+    double4 *A = vals + sub_off[s];
+    // row buffer: entry j of the lane's row at rb[j * 32] (conflict-free across lanes)
+    double4 *rb = reinterpret_cast<double4 *>(smem_raw) + (size_t)warp * 32 * rstride + lane;
+    for (int lev = 0; lev < C.nlev; ++lev) {
+        const int q1 = C.lev_ptr[lev + 1];
+        for (int q0 = C.lev_ptr[lev]; q0 < q1; q0 += 32) {
+            const int q = q0 + lane;
+            if (q < q1) {
+                const int i = C.lev_rows[q];
+                const int r0 = C.rowptr[i], len = C.rowptr[i + 1] - r0, d = C.diag[i] - r0;
+                for (int j = 0; j < len; ++j) rb[j * 32] = make_double4(0.0, 0.0, 0.0, 0.0);
+                {
+                    // J's row straight into the row buffer (no local-memory block array)
+                    int gx, gy, gz;
+                    local_to_global(g, C, o, i, gx, gy, gz);
+                    const int *jm = C.jmap_local + i * NOFF;
+                    jac_row_emit<DIM>(g, P, dt, coef, gx, gy, gz, [&](int e, int comp, double v) {
+                        const int p = jm[e];
+                        if (p >= 0) reinterpret_cast<double *>(rb + p * 32)[comp] += v;
+                    });
+                }
+                for (int t = 0; t < d; ++t) {
+                    const int k = C.col[r0 + t];
+                    const double4 dk = A[C.pos[C.diag[k]]];   // row k: finished, inverted diagonal
+                    const double4 ak = rb[t * 32];
+                    const Blk L = mul({ak.x, ak.y, ak.z, ak.w}, {dk.x, dk.y, dk.z, dk.w});
+                    rb[t * 32] = make_double4(L.a, L.b, L.c, L.d);
+                    const int u1 = C.upd_ptr[r0 + t + 1];
+                    for (int u0 = C.upd_ptr[r0 + t]; u0 < u1; u0 += UB) {
+                        double4 us[UB];
+                        int dl[UB];
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) {
+                            const bool ok = u0 + b < u1;
+                            dl[b] = ok ? C.upd_dl[u0 + b] : 0;
+                            us[b] = ok ? A[C.upd[u0 + b].x] : make_double4(0.0, 0.0, 0.0, 0.0);
+                        }
+#pragma unroll
+                        for (int b = 0; b < UB; ++b)
+                            if (u0 + b < u1) {
+                                const Blk m = mul(L, {us[b].x, us[b].y, us[b].z, us[b].w});
+                                double4 v = rb[dl[b] * 32];
+                                v.x -= m.a;
+                                v.y -= m.b;
+                                v.z -= m.c;
+                                v.w -= m.d;
+                                rb[dl[b] * 32] = v;
+                            }
+                    }
+                }
+                // diagonal block: scalar pivots as the reference's factor_inplace sees them
+                const double4 D = rb[d * 32];
+                const double p0 = D.x;
+                const double p1 = D.w - (D.z / D.x) * D.y;
+                int bad = -1;
+                if (fabs(p0) < 1e-300) bad = 2 * i;
+                else if (fabs(p1) < 1e-300) bad = 2 * i + 1;
+                if (bad >= 0) atomicMin(bad_row + s, bad);
+                const double det = D.x * D.w - D.y * D.z;
+                rb[d * 32] = make_double4(D.w / det, -D.y / det, -D.z / det, D.x / det);
+                for (int j = 0; j < len; ++j) A[C.pos[r0 + j]] = rb[j * 32];
+            }
+            __syncwarp();   // this level's rows are visible to the next level's lanes
+        }
     }
 }
 
@@ -1149,9 +1244,18 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
             const int *f = std::lower_bound(b, e, lt);
             C.jmap[(size_t)l * noff + q] = (int)(f - C.col.data());
         }
+    C.jmap_local.assign(C.jmap.size(), -1);
+    for (int l = 0; l < nloc; ++l)
+        for (int q = 0; q < noff; ++q) {
+            const int j = C.jmap[(size_t)l * noff + q];
+            if (j >= 0) C.jmap_local[(size_t)l * noff + q] = j - C.rowptr[l];
+        }
+    C.rmax = 0;
+    for (int i = 0; i < nloc; ++i) C.rmax = std::max(C.rmax, C.rowptr[i + 1] - C.rowptr[i]);
     // IKJ update lists: for lower entry t=(i,k), pairs (U entry (k,j), entry (i,j))
     C.upd_ptr.assign(C.nnzb + 1, 0);
     C.upd.clear();
+    C.upd_dl.clear();
     std::vector<int> where(nloc, -1);
     for (int i = 0; i < nloc; ++i) {
         for (int t = C.rowptr[i]; t < C.rowptr[i + 1]; ++t) where[C.col[t]] = t;
@@ -1160,7 +1264,10 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
             if (k < i) {
                 for (int u = C.diag[k] + 1; u < C.rowptr[k + 1]; ++u) {
                     const int w = where[C.col[u]];
-                    if (w >= 0) C.upd.push_back(make_int2(u, w));
+                    if (w >= 0) {
+                        C.upd.push_back(make_int2(u, w));
+                        C.upd_dl.push_back(w - C.rowptr[i]);
+                    }
                 }
             }
             C.upd_ptr[t + 1] = (int)C.upd.size();
@@ -1334,6 +1441,8 @@ acch_status upload_class(ClassHost &C)
     const size_t o_meta = add(C.meta.size());
     const size_t o_lin = add(sizeof(int) * C.lin.size());
     const size_t o_own = add(sizeof(int) * std::max<size_t>(1, C.own_list.size()));
+    const size_t o_jml = add(sizeof(int) * C.jmap_local.size());
+    const size_t o_udl = add(sizeof(int) * std::max<size_t>(1, C.upd_dl.size()));
     ACCH_CUDA(cudaMalloc(&C.dev_mem, total));
     std::vector<unsigned char> h(total, 0);
     auto put = [&](size_t o, const void *src, size_t bytes) { if (bytes) memcpy(h.data() + o, src, bytes); };
@@ -1366,6 +1475,8 @@ acch_status upload_class(ClassHost &C)
     put(o_meta, C.meta.data(), C.meta.size());
     put(o_lin, C.lin.data(), sizeof(int) * C.lin.size());
     put(o_own, C.own_list.data(), sizeof(int) * C.own_list.size());
+    put(o_jml, C.jmap_local.data(), sizeof(int) * C.jmap_local.size());
+    put(o_udl, C.upd_dl.data(), sizeof(int) * C.upd_dl.size());
     ACCH_CUDA(cudaMemcpy(C.dev_mem, h.data(), total, cudaMemcpyHostToDevice));
     unsigned char *b = (unsigned char *)C.dev_mem;
     ClassDev &d = C.dev;
@@ -1406,6 +1517,9 @@ acch_status upload_class(ClassHost &C)
     d.lin = (const int *)(b + o_lin);
     d.own_list = (const int *)(b + o_own);
     d.n_owned = (int)C.own_list.size();
+    d.jmap_local = (const int *)(b + o_jml);
+    d.upd_dl = (const int *)(b + o_udl);
+    d.rmax = C.rmax;
     d.meta_bytes = (int)C.meta.size();
     d.m_fbs = C.m_off[1];
     d.m_bptr = C.m_off[2];
@@ -1454,6 +1568,7 @@ struct acch_precond {
     int tma_mode = 0;      // apply_tma_kernel (TMA ring) in use
     // class-group solver (apply_group_kernel): groups of <= group_nw subdomains of one class
     int group_mode = 0, group_nw = 8, group_per_warp = 1, meta_max = 0, y_stride = 0;
+    int factor_warp = 0, factor_rstride = 0;   // factor_warp_kernel (opt-in: ACCH_FACTOR_WARP=1)
     int dbg = 0;   // ACCH_APPLY_DBG (timing experiments only; results are wrong): 1 no factor loads, 2 loads only
     size_t group_smem = 0;
     std::vector<int4> groups;
@@ -1833,6 +1948,23 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
                     pc->meta_max, pc->group_smem, occ);
         }
     }
+    {
+        // warp factorisation: 4 warps x 32 row buffers of the longest row must fit
+        int rmax = 0;
+        for (const auto &C : pc->classes) rmax = std::max(rmax, C.rmax);
+        pc->factor_rstride = rmax;
+        const size_t sm = (size_t)4 * 32 * rmax * sizeof(double4);
+        // opt-in (ACCH_FACTOR_WARP=1): 4.1x less DRAM traffic than the CTA
+        // kernel (55 vs 226 GB at 256^3) but latency-bound at 8 warps/SM and
+        // measured slower (158 vs 124 ms; profiles/r01_factor.txt)
+        pc->factor_warp = 0;
+        if (const char *e = getenv("ACCH_FACTOR_WARP")) pc->factor_warp = sm <= 200 * 1024 && atoi(e) != 0;
+        if (pc->factor_warp) {
+            const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+            PC_CUDA(cudaFuncSetAttribute(factor_warp_kernel<3, 4>, attr, smem_optin()));
+            PC_CUDA(cudaFuncSetAttribute(factor_warp_kernel<2, 4>, attr, smem_optin()));
+        }
+    }
 #undef PC_CUDA
     *out = pc;
     return ACCH_OK;
@@ -1868,14 +2000,25 @@ extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef,
     acch_ctx *ctx = pc->ctx;
     ACCH_CUDA(cudaMemsetAsync(pc->d_bad, 0x7f, sizeof(int) * pc->nsub, ctx->stream));
     ProfScope prof_scope(ctx, PC_FACTOR, 32.0 * pc->total_nnzb + 56.0 * pc->total_ext);
-    if (pc->dim == 3)
+    if (pc->factor_warp) {
+        constexpr int NW = 4;
+        const unsigned nb = (unsigned)((pc->nsub + NW - 1) / NW);
+        const size_t sm = (size_t)NW * 32 * pc->factor_rstride * sizeof(double4);
+        if (pc->dim == 3)
+            factor_warp_kernel<3, NW><<<nb, NW * 32, sm, ctx->stream>>>(ctx->g, ctx->p, dt, coef, pc->d_classes,
+                pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, pc->d_bad, pc->nsub, pc->factor_rstride);
+        else
+            factor_warp_kernel<2, NW><<<nb, NW * 32, sm, ctx->stream>>>(ctx->g, ctx->p, dt, coef, pc->d_classes,
+                pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, pc->d_bad, pc->nsub, pc->factor_rstride);
+    } else if (pc->dim == 3) {
         factor_kernel<3><<<(unsigned)pc->nsub, kFactorThreads, 0, ctx->stream>>>(
             ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals,
             pc->d_bad);
-    else
+    } else {
         factor_kernel<2><<<(unsigned)pc->nsub, kFactorThreads, 0, ctx->stream>>>(
             ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals,
             pc->d_bad);
+    }
     ACCH_LAUNCHED(ctx);
     std::vector<int> bad(pc->nsub);
     ACCH_CUDA(cudaMemcpyAsync(bad.data(), pc->d_bad, sizeof(int) * pc->nsub, cudaMemcpyDeviceToHost, ctx->stream));

@@ -349,3 +349,25 @@ def test_group_solver_interior_boxes_bitwise_equal_warp_solver(variant, monkeypa
     po.update(Jo)
     ref = po.apply(host(r))
     assert np.max(np.abs(outs["1"] - ref)) <= 1e-10 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("solver", ["ilu0", "ilu1", "lu"])
+@pytest.mark.parametrize("bc", [BoundaryCondition.PERIODIC, BoundaryCondition.NEUMANN])
+def test_warp_factorisation_bitwise_equal_cta_factorisation(solver, bc, monkeypatch):
+    """The warp-per-subdomain factorisation (row buffers in shared memory)
+    performs the CTA kernel's operations in the same order: the factors, and
+    so the applies, must agree bitwise."""
+    rng = np.random.default_rng(9)
+    g = Grid((12, 12, 12), (1.0, 1.0, 1.0), bc)
+    uo, vo = 0.5 + rng.uniform(-0.05, 0.05, g.array_shape), rng.uniform(-0.05, 0.05, g.array_shape)
+    un, vn = uo + rng.uniform(-0.01, 0.01, g.array_shape), vo + rng.uniform(-0.01, 0.01, g.array_shape)
+    prob = StepProblem.create(g, PARAMS, st(g, uo, vo), 1e-3)
+    J = assemble_jacobian(prob, st(g, un, vn))
+    r = torch.tensor(rng.standard_normal(2 * g.n_cells), device=DEV)
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ACCH_FACTOR_WARP", mode)
+        pre = SchwarzPreconditioner(partition(g, 8, 1), SchwarzVariant.LEFT_RAS, SubdomainSolverSpec.from_string(solver))
+        pre.update(J)
+        outs[mode] = host(pre.apply(r))
+    assert np.array_equal(outs["1"], outs["0"])
