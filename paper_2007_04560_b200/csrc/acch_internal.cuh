@@ -85,7 +85,7 @@ struct acch_ctx {
     double *d_work = nullptr;         // 3 * 2N: z (precond out), r, t
     double *d_h = nullptr;            // small device array for Hessenberg column
     double *d_mvtmp = nullptr;        // two-pass matvec intermediate (dG_u, eta), 2 * nstore
-    int matvec_mode = 1;              // 1 two-pass (default, measured faster), 0 fused z-marching kernel (ACCH_MATVEC=fused)
+    int matvec_mode = 2;              // 2 z-marching one-barrier kernel (3D default), 1 two-pass (2D), 0 older fused kernel
     long long launches = 0;
     ProfState prof;
     // slab decomposition: rank topology and the host hooks that move ghost

@@ -193,7 +193,7 @@ acch_status acch_ctx_create(const acch_grid_desc *grid, const acch_params *param
         acch_ctx_destroy(ctx);
         return acch_cuda_fail(e, "acch_ctx_create allocation");
     }
-    if (const char *e = getenv("ACCH_MATVEC")) ctx->matvec_mode = strcmp(e, "fused") == 0 ? 0 : 1;
+    ctx->matvec_mode = ctx->g.dim == 3 ? 2 : 1;   // re-read per call (launch_matvec)
     *out = ctx;
     return ACCH_OK;
 }

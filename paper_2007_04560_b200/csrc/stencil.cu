@@ -16,6 +16,7 @@
 // (G_u, or dG_u; tile + 1 halo) in shared memory, so every input byte is read
 // from HBM once per sweep and the expensive entropy chords are evaluated only
 // on the tile + 1 halo.
+#include <stdlib.h>
 #include <string.h>
 
 #include "acch_internal.cuh"
@@ -494,6 +495,240 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
 }
 
 // ---------------------------------------------------------------------------
+// z-marching fused matvec, one barrier per plane (3D default).
+//
+// CTA = TX x TY threads over an x-y tile, marching a z range.  Every input
+// byte comes from HBM once per sweep (halo re-reads are L2 hits):
+//   * w: 3-slot smem ring of tile+2 planes, cp.async one plane ahead;
+//   * the tile+1 "columns" (TX*TY centre columns, one per thread, plus the
+//     2 GX + 2 TY ring columns owned by the first threads) carry
+//     dG_u = (-alpha/2 + S) w_u + D w_v - gamma/2 lap w_u and
+//     eta = (c_u w_u + c_v w_v)/2, computed once per column and plane into a
+//     3-slot smem ring B = {(dG_u, cbar), (eta, G_u)};
+//   * coefficient planes are prefetched one plane ahead into registers; the
+//     z-neighbours of a column's w_u stay in the owning thread's registers.
+// Iteration k: wait W(k+2), barrier, issue W(k+3), compute B(k+1), emit y(k)
+// from B(k) (written before the barrier) and the own column's B(k+-1).
+// All per-thread offsets are computed once; the z loop is loads + flops.
+// ---------------------------------------------------------------------------
+
+template <int TX, int TY>
+struct ZmSmem {
+    static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2;
+    static constexpr int NW = HX * HY, NB = GX * GY, NRING = 2 * GX + 2 * TY;
+    static constexpr size_t bytes = sizeof(double2) * (3 * NW + 2 * 3 * NB);
+};
+
+template <int TX, int TY, int MINB>
+__global__ void __launch_bounds__(TX *TY, MINB)
+mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef, const double2 *__restrict__ w_g,
+             double2 *__restrict__ yout, int nchunk)
+{
+    using L = ZmSmem<TX, TY>;
+    constexpr int HX = L::HX, GX = L::GX, NW = L::NW, NB = L::NB, NRING = L::NRING, NT = TX * TY;
+    constexpr int NWR = (NW + NT - 1) / NT;
+    static_assert(NRING <= NT, "ring columns must fit one per thread");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2 *sW = reinterpret_cast<double2 *>(smem_raw);      // [3][NW]   w
+    double2 *sB1 = sW + 3 * NW;                                  // [3][NB]   (dG_u, cbar)
+    double2 *sB2 = sB1 + 3 * NB;                                 // [3][NB]   (eta, G_u)
+
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int nx = g.nx, ny = g.ny;
+    const long long nxy = (long long)nx * ny;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    // z range of this chunk: chunks split nz as evenly as possible
+    const int zb = (int)(((long long)blockIdx.z * g.nz) / nchunk);
+    const int ze = (int)(((long long)(blockIdx.z + 1) * g.nz) / nchunk);
+    const long long N = g.nstore;
+    const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
+    const double hg = 0.5 * P.gamma, ha = -0.5 * P.alpha, hb = -0.5 * P.beta;
+    const double idt = 1.0 / dt, irho = 1.0 / P.rho;
+
+    // w tile+2 copy offsets (plane-relative)
+    int woff[NWR];
+#pragma unroll
+    for (int r = 0; r < NWR; ++r) {
+        const int i = tid + r * NT;
+        const int hx = i % HX, hy = i / HX;
+        woff[r] = (i < NW) ? wrap_coord(y0 + hy - 2, ny, g.periodic) * nx + wrap_coord(x0 + hx - 2, nx, g.periodic) : 0;
+    }
+    // owned columns: j = 0 centre (tx, ty); j = 1 ring column tid (tid < NRING)
+    const bool has_ring = tid < NRING;
+    int cx[2], cy[2];
+    cx[0] = tx;
+    cy[0] = ty;
+    {
+        // ring of the tile+1 region in tile coordinates (-1 .. TX, -1 .. TY)
+        int r = has_ring ? tid : 0;
+        if (r < GX) { cx[1] = r - 1; cy[1] = -1; }
+        else if (r < 2 * GX) { cx[1] = r - GX - 1; cy[1] = TY; }
+        else if (r < 2 * GX + TY) { cx[1] = -1; cy[1] = r - 2 * GX; }
+        else { cx[1] = TX; cy[1] = r - 2 * GX - TY; }
+    }
+    int hc[2], gc[2], coff[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        hc[j] = (cy[j] + 2) * HX + (cx[j] + 2);
+        gc[j] = (cy[j] + 1) * GX + (cx[j] + 1);
+        coff[j] = wrap_coord(y0 + cy[j], ny, g.periodic) * nx + wrap_coord(x0 + cx[j], nx, g.periodic);
+    }
+    const int x = x0 + tx, y = y0 + ty;
+    const bool active = x < nx && y < ny;
+    const bool per = g.periodic != 0;
+    const bool fxl = per || x > 0, fxh = per || x < nx - 1, fyl = per || y > 0, fyh = per || y < ny - 1;
+    const int jn = has_ring ? 2 : 1;
+
+    auto load_w = [&](int kk, int slot) {
+        const double2 *src = w_g + zplane(g, kk) * nxy;
+        double2 *dst = sW + slot * NW + tid;
+#pragma unroll
+        for (int r = 0; r < NWR; ++r)
+            if (r < NWR - 1 || tid + r * NT < NW) cp_async16(dst + r * NT, src + woff[r]);
+        cp_async_commit();
+    };
+
+    double cS[2], cD[2], cU[2], cV[2], cC[2], cG[2];
+    auto prefetch = [&](int kk) {
+        const double *base = coef + zplane(g, kk) * nxy;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (j < jn) {
+                const double *p = base + coff[j];
+                cS[j] = __ldg(p + CO_S * N);
+                cD[j] = __ldg(p + CO_D * N);
+                cU[j] = __ldg(p + CO_CU * N);
+                cV[j] = __ldg(p + CO_CV * N);
+                cC[j] = __ldg(p + CO_CBAR * N);
+                cG[j] = __ldg(p + CO_GU * N);
+            }
+        }
+    };
+
+    // column values carried across planes
+    double wuz[2];                 // w_u of column j at the plane below the one being built
+    double2 wk = make_double2(0.0, 0.0), wk1 = wk;   // centre w at planes k, k+1
+    double wvm = 0.0;                                 // centre w_v at plane k-1
+    double lxy_k = 0.0, lxy_k1 = 0.0;                 // centre xy-lap(w_v) at planes k, k+1
+    double Sk = 0.0, Dk = 0.0, Sk1 = 0.0, Dk1 = 0.0;  // centre S, D at planes k, k+1
+
+    // build B(kk) from W(kk) (slot s1) and W(kk+1) (slot s2); wuz = w_u(kk-1)
+    auto build = [&](int kk, int s1, int s2, int sb) {
+        const double2 *W1 = sW + s1 * NW, *W2 = sW + s2 * NW;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (j < jn) {
+                const int h = hc[j];
+                const double2 w0 = W1[h], xm = W1[h - 1], xp = W1[h + 1], ym = W1[h - HX], yp = W1[h + HX];
+                const double zp = W2[h].x;
+                double lap = (xp.x - 2.0 * w0.x + xm.x) * ihx;
+                lap += (yp.x - 2.0 * w0.x + ym.x) * ihy;
+                lap += (zp - 2.0 * w0.x + wuz[j]) * ihz;
+                const double dG = (ha + cS[j]) * w0.x + cD[j] * w0.y - hg * lap;
+                const double et = 0.5 * (cU[j] * w0.x + cV[j] * w0.y);
+                sB1[sb * NB + gc[j]] = make_double2(dG, cC[j]);
+                sB2[sb * NB + gc[j]] = make_double2(et, cG[j]);
+                wuz[j] = w0.x;
+                if (j == 0) {
+                    wk1 = w0;
+                    lxy_k1 = (xp.y - 2.0 * w0.y + xm.y) * ihx + (yp.y - 2.0 * w0.y + ym.y) * ihy;
+                    Sk1 = cS[0];
+                    Dk1 = cD[0];
+                }
+            }
+        }
+        (void)kk;
+    };
+
+    // ring slots: W planes kk -> (kk - zb + 3) % 3 tracked by rotation
+    int sw1, sw2;                    // slots of W(k+1), W(k+2) at the top of iteration k
+    int sb0, sb1, sb2;               // slots of B(k-1), B(k), B(k+1)
+
+    // prologue: B(zb-1) and B(zb) are built before iteration zb; W(zb-2) is
+    // needed only as the z-neighbour w_u(zb-2) of each column (a register)
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+        if (j < jn) wuz[j] = __ldg(&w_g[zplane(g, zb - 2) * nxy + coff[j]].x);
+    load_w(zb - 1, 0);
+    load_w(zb, 1);
+    prefetch(zb - 1);
+    cp_async_wait_all();
+    __syncthreads();
+    load_w(zb + 1, 2);
+    build(zb - 1, 0, 1, 0);      // B(zb-1) -> slot 0; needs W(zb) centre = slot 1
+    wvm = wk1.y;
+    prefetch(zb);
+    cp_async_wait_all();
+    __syncthreads();
+    // now W(zb) slot 1, W(zb+1) slot 2; slot 0 (W(zb-1)) is free
+    load_w(zb + 2, 0);
+    build(zb, 1, 2, 1);          // B(zb) -> slot 1
+    wk = wk1;
+    lxy_k = lxy_k1;
+    Sk = Sk1;
+    Dk = Dk1;
+    prefetch(zb + 1);
+    double gvk = active ? __ldg(coef + CO_GV * N + zplane(g, zb) * nxy + coff[0]) : 0.0;
+    // W slots: W(k+1) = 2, W(k+2) = 0 at k = zb
+    sw1 = 2;
+    sw2 = 0;
+    sb0 = 0;
+    sb1 = 1;
+    sb2 = 2;
+    for (int k = zb; k < ze; ++k) {
+        cp_async_wait_all();
+        __syncthreads();
+        // the W slot of plane k is free (W(k) lives in registers): W(k+3) into it
+        const int swf = 3 - sw1 - sw2;
+        if (k + 3 <= ze + 1) load_w(k + 3, swf);
+        build(k + 1, sw1, sw2, sb2);
+        double gvn = 0.0;
+        if (k + 2 <= ze) prefetch(k + 2);
+        if (active && k + 1 < ze) gvn = __ldg(coef + CO_GV * N + zplane(g, k + 1) * nxy + coff[0]);
+        if (active) {
+            const double2 *B1 = sB1 + sb1 * NB, *B2 = sB2 + sb1 * NB;
+            const int c0 = gc[0];
+            const double2 a0 = B1[c0], e0 = B2[c0];
+            const double dG0 = a0.x, C0 = a0.y, E0 = e0.x, G0 = e0.y;
+            double d1 = 0.0, d2 = 0.0;
+            auto face = [&](const double2 &an, const double2 &en, double ih, bool lo_ok, bool hi_ok,
+                            const double2 &am, const double2 &em) {
+                if (hi_ok) {
+                    d1 += 0.5 * (C0 + an.y) * (an.x - dG0) * ih;
+                    d2 += 0.5 * (E0 + en.x) * (en.y - G0) * ih;
+                }
+                if (lo_ok) {
+                    d1 -= 0.5 * (C0 + am.y) * (dG0 - am.x) * ih;
+                    d2 -= 0.5 * (E0 + em.x) * (G0 - em.y) * ih;
+                }
+            };
+            face(B1[c0 + 1], B2[c0 + 1], ihx, fxl, fxh, B1[c0 - 1], B2[c0 - 1]);
+            face(B1[c0 + GX], B2[c0 + GX], ihy, fyl, fyh, B1[c0 - GX], B2[c0 - GX]);
+            face(sB1[sb2 * NB + c0], sB2[sb2 * NB + c0], ihz, zstep_ok(g, k, -1), zstep_ok(g, k, +1),
+                 sB1[sb0 * NB + c0], sB2[sb0 * NB + c0]);
+            const double lapv = lxy_k + (wk1.y - 2.0 * wk.y + wvm) * ihz;
+            double2 out;
+            out.x = wk.x * idt - d1 - d2;
+            out.y = wk.y * idt + (C0 * irho) * (Dk * wk.x + (hb + Sk) * wk.y - hg * lapv) + (gvk * irho) * E0;
+            yout[zplane(g, k) * nxy + coff[0]] = out;
+        }
+        // rotate
+        wvm = wk.y;
+        wk = wk1;
+        lxy_k = lxy_k1;
+        Sk = Sk1;
+        Dk = Dk1;
+        gvk = gvn;
+        sw1 = sw2;
+        sw2 = swf;
+        const int tb = sb0;
+        sb0 = sb1;
+        sb1 = sb2;
+        sb2 = tb;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Two-pass matrix-free matvec (thread per cell, neighbours through L1/L2):
 //   pass 1: T = (dG_u, eta) per cell                 reads w, S, D, c_u, c_v
 //   pass 2: y from T, cbar, G_u (7-point), w, S, D, G_v
@@ -834,17 +1069,68 @@ static acch_status launch_matvec_twopass(acch_ctx *ctx, const double *coef, doub
     return ACCH_OK;
 }
 
+// z chunks for a z-marching kernel: minimise waves x (planes per chunk + the
+// pipeline start-up), given the resident CTAs per SM of the kernel
+static int choose_zchunks(int tiles, int nz, int per_sm, int sms, double startup)
+{
+    const long long slots = (long long)per_sm * sms;
+    int best = 1;
+    double best_cost = 1e300;
+    for (int c = 1; c <= nz; ++c) {
+        const long long items = (long long)tiles * c;
+        const long long waves = (items + slots - 1) / slots;
+        const double cost = (double)waves * ((double)nz / c + startup);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = c;
+        }
+    }
+    return best;
+}
+
+template <int MINB>
+static acch_status launch_matvec_zm_t(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
+{
+    constexpr int TX = 32, TY = 8;
+    using L = ZmSmem<TX, TY>;
+    auto kern = mv_zm_kernel<TX, TY, MINB>;
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        acch_status st = set_smem(kern, L::bytes);
+        if (st != ACCH_OK) return st;
+        ACCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TX * TY, L::bytes));
+        ACCH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        if (per_sm < 1) per_sm = 1;
+    }
+    const GridDev &g = ctx->g;
+    const int gx = (g.nx + TX - 1) / TX, gy = (g.ny + TY - 1) / TY;
+    const int nchunk = choose_zchunks(gx * gy, g.nz, per_sm, sms, 3.0);
+    kern<<<dim3(gx, gy, nchunk), dim3(TX, TY), L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
+                                                                       (double2 *)y, nchunk);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+static acch_status launch_matvec_zm(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
+{
+    const char *e = getenv("ACCH_ZM_MINB");
+    if (e && atoi(e) == 3) return launch_matvec_zm_t<3>(ctx, coef, dt, w, y);
+    return launch_matvec_zm_t<2>(ctx, coef, dt, w, y);
+}
+
 acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
-    // ACCH_MATVEC=fused selects the z-marching kernel (read per call so tests
-    // can exercise both forms on one context)
+    // ACCH_MATVEC = zm (3D default) | twopass (2D default) | fused (read per
+    // call so tests can exercise every form on one context)
     const char *mode = getenv("ACCH_MATVEC");
-    ctx->matvec_mode = (mode && strcmp(mode, "fused") == 0) ? 0 : 1;
-    if (ctx->matvec_mode == 1) {
-        ProfScope prof_scope(ctx, PC_MATVEC, 88.0 * ctx->g.n);
-        return launch_matvec_twopass(ctx, coef, dt, w, y);
-    }
+    int m = ctx->g.dim == 3 ? 2 : 1;
+    if (mode && strcmp(mode, "fused") == 0) m = 0;
+    if (mode && strcmp(mode, "twopass") == 0) m = 1;
+    if (mode && strcmp(mode, "zm") == 0 && ctx->g.dim == 3) m = 2;
+    ctx->matvec_mode = m;
     ProfScope prof_scope(ctx, PC_MATVEC, 88.0 * ctx->g.n);
+    if (m == 2) return launch_matvec_zm(ctx, coef, dt, w, y);
+    if (m == 1) return launch_matvec_twopass(ctx, coef, dt, w, y);
     const GridDev &g = ctx->g;
     const dim3 block(MTX, MTY / MRPT);
     if (g.dim == 3) {

@@ -73,7 +73,7 @@ def test_residual_matches_reference(tag):
     assert np.max(np.abs(F0 - z["F0"])) <= 1e-12 * np.max(np.abs(z["F0"]))
 
 
-@pytest.mark.parametrize("form", ["twopass", "fused"])
+@pytest.mark.parametrize("form", ["zm", "twopass", "fused"])
 @pytest.mark.parametrize("tag", STENCIL)
 def test_jacobian_matvec_matches_reference(tag, form, monkeypatch):
     monkeypatch.setenv("ACCH_MATVEC", form)
