@@ -40,8 +40,38 @@ struct ParamsDev {
     double c2[ACCH_MAX_ORDER];   // 1 / (2s+1)
 };
 
-// coefficient planes of the matrix-free Jacobian, SoA, each N doubles
+// Coefficients of the matrix-free Jacobian: 7 doubles per stored cell in
+// three cell-major arrays, so a stencil kernel fetches a cell's coefficients
+// with one 32-byte and one 16-byte load:
+//   A[c]  = (S, D, c_u, c_v)   double4 at coef + 4c
+//   B[c]  = (cbar, G_u)        double2 at coef + 4N + 2c
+//   Gv[c]                      double  at coef + 6N + c
 enum { CO_S = 0, CO_D, CO_CBAR, CO_GU, CO_CU, CO_CV, CO_GV, CO_NFIELDS };
+__host__ __device__ __forceinline__ long long co_index(int f, long long N, long long c)
+{
+    switch (f) {
+    case CO_S: return 4 * c;
+    case CO_D: return 4 * c + 1;
+    case CO_CU: return 4 * c + 2;
+    case CO_CV: return 4 * c + 3;
+    case CO_CBAR: return 4 * N + 2 * c;
+    case CO_GU: return 4 * N + 2 * c + 1;
+    default: return 6 * N + c;
+    }
+}
+#ifdef __CUDACC__
+// one 256-bit read-only load (LDG.E.256 on sm_100); not volatile, so the
+// compiler may schedule it like any other load
+__device__ __forceinline__ double4 ldg256(const double4 *p)
+{
+    double4 v;
+    asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w) : "l"(p));
+    return v;
+}
+#endif
+__host__ __device__ __forceinline__ const double4 *co_A(const double *coef) { return reinterpret_cast<const double4 *>(coef); }
+__host__ __device__ __forceinline__ const double2 *co_B(const double *coef, long long N) { return reinterpret_cast<const double2 *>(coef + 4 * N); }
+__host__ __device__ __forceinline__ const double *co_Gv(const double *coef, long long N) { return coef + 6 * N; }
 
 // ---------------------------------------------------------------------------
 // Host-side context

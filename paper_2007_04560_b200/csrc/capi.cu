@@ -380,7 +380,9 @@ acch_status acch_jacobian_prepare(acch_ctx *ctx, const double *x_old, double dt,
     TRY(comm_halo(ctx, x, 2, 1));
     TRY(launch_jacobian_prepare(ctx, x_old, dt, x, coef));
     // the factorisation reads coefficients one plane beyond an overlapping box
-    for (int f = 0; f < CO_NFIELDS; ++f) TRY(comm_halo(ctx, coef + f * ctx->g.nstore, 1, 2));
+    TRY(comm_halo(ctx, coef, 4, 2));
+    TRY(comm_halo(ctx, coef + 4 * ctx->g.nstore, 2, 2));
+    TRY(comm_halo(ctx, coef + 6 * ctx->g.nstore, 1, 2));
     return ACCH_OK;
 }
 

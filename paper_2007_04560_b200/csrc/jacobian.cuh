@@ -53,7 +53,7 @@ __device__ __forceinline__ void jac_row_emit(const GridDev &g, const ParamsDev &
         r[a] = a == 2 ? q[a] + s : wrap_coord(q[a] + s, nn[a], g.periodic);
     };
     const long long c0 = cid(cc);
-    const double cb0 = coef[CO_CBAR * N + c0], gu0 = coef[CO_GU * N + c0];
+    const double cb0 = coef[co_index(CO_CBAR, N, c0)], gu0 = coef[co_index(CO_GU, N, c0)];
     // weights of dG_u(m) and eta(m) in row c of the u equation
     double wdg[7], weta[7];
     int mo[3 * 7];   // relative offsets of m
@@ -67,8 +67,8 @@ __device__ __forceinline__ void jac_row_emit(const GridDev &g, const ParamsDev &
             int q[3];
             shifted(cc, a, s, q);
             const long long cn = cid(q);
-            const double K = 0.5 * (cb0 + coef[CO_CBAR * N + cn]) * g.ih2[a];
-            const double dGn = coef[CO_GU * N + cn] - gu0;
+            const double K = 0.5 * (cb0 + coef[co_index(CO_CBAR, N, cn)]) * g.ih2[a];
+            const double dGn = coef[co_index(CO_GU, N, cn)] - gu0;
             ktot += K;
             wdg[nm] = -K;
             weta[nm] = -0.5 * dGn * g.ih2[a];
@@ -99,15 +99,15 @@ __device__ __forceinline__ void jac_row_emit(const GridDev &g, const ParamsDev &
             }
         }
         const int om = offid(mo[3 * j], mo[3 * j + 1], mo[3 * j + 2]);
-        const double A = -0.5 * P.alpha + coef[CO_S * N + cm] + hg * lsum;
-        emit(om, 0, wdg[j] * A + weta[j] * 0.5 * coef[CO_CU * N + cm]);
-        emit(om, 1, wdg[j] * coef[CO_D * N + cm] + weta[j] * 0.5 * coef[CO_CV * N + cm]);
+        const double A = -0.5 * P.alpha + coef[co_index(CO_S, N, cm)] + hg * lsum;
+        emit(om, 0, wdg[j] * A + weta[j] * 0.5 * coef[co_index(CO_CU, N, cm)]);
+        emit(om, 1, wdg[j] * coef[co_index(CO_D, N, cm)] + weta[j] * 0.5 * coef[co_index(CO_CV, N, cm)]);
     }
     const int o0 = offid(0, 0, 0);
     emit(o0, 0, 1.0 / dt);
     // v row
     const double cr = cb0 / P.rho;
-    const double S0 = coef[CO_S * N + c0], D0 = coef[CO_D * N + c0], Gv0 = coef[CO_GV * N + c0];
+    const double S0 = coef[co_index(CO_S, N, c0)], D0 = coef[co_index(CO_D, N, c0)], Gv0 = coef[co_index(CO_GV, N, c0)];
     double lsum0 = 0.0;
     for (int a = 0; a < g.dim; ++a) {
         for (int s = -1; s <= 1; s += 2) {
@@ -117,8 +117,8 @@ __device__ __forceinline__ void jac_row_emit(const GridDev &g, const ParamsDev &
             emit(o, 3, -hg * cr * g.ih2[a]);
         }
     }
-    emit(o0, 2, cr * D0 + Gv0 * coef[CO_CU * N + c0] / (2.0 * P.rho));
-    emit(o0, 3, 1.0 / dt + cr * (-0.5 * P.beta + S0) + hg * cr * lsum0 + Gv0 * coef[CO_CV * N + c0] / (2.0 * P.rho));
+    emit(o0, 2, cr * D0 + Gv0 * coef[co_index(CO_CU, N, c0)] / (2.0 * P.rho));
+    emit(o0, 3, 1.0 / dt + cr * (-0.5 * P.beta + S0) + hg * cr * lsum0 + Gv0 * coef[co_index(CO_CV, N, c0)] / (2.0 * P.rho));
 }
 
 template <int DIM>

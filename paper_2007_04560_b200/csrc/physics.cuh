@@ -96,6 +96,19 @@ __device__ __forceinline__ int zplane(const GridDev &g, int z)
     return z + g.zg;
 }
 
+// zplane() for -nz <= z < 2 nz without integer division (z-marching kernels)
+__device__ __forceinline__ int zplane_near(const GridDev &g, int z)
+{
+    if (g.zg == 0) {
+        if (z < 0) return g.periodic ? z + g.nz : 0;
+        if (z >= g.nz) return g.periodic ? z - g.nz : g.nz - 1;
+        return z;
+    }
+    if (z < 0 && g.zwall_lo) z = 0;
+    if (z >= g.nz && g.zwall_hi) z = g.nz - 1;
+    return z + g.zg;
+}
+
 // can a stencil step from local plane z to z + s (no physical wall crossed)?
 __device__ __forceinline__ bool zstep_ok(const GridDev &g, int z, int s)
 {

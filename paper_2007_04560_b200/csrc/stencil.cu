@@ -53,7 +53,14 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem));
 }
+// bulk L2 prefetch of [p, p + bytes) (16-byte granules)
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, unsigned bytes)
+{
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Chord for the residual's hot loop: same branch predicates as
@@ -270,13 +277,17 @@ __global__ void jac_prepare_kernel(GridDev g, ParamsDev P, const double2 *__rest
     entropy_chord<true>(n0.x + n0.y, o0.x + o0.y, P, 0, phi, dp);
     entropy_chord<true>(n0.x - n0.y, o0.x - o0.y, P, 0, psi, dq);
     const long long N = g.nstore;
-    coef[CO_S * N + c] = P.theta * (dp + dq);
-    coef[CO_D * N + c] = P.theta * (dp - dq);
-    coef[CO_CBAR * N + c] = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
-    coef[CO_GU * N + c] = -0.5 * P.alpha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) - 0.5 * P.gamma * (lun + luo);
-    coef[CO_CU * N + c] = (1.0 - 2.0 * n0.x) * (0.25 - n0.y * n0.y);    // physics.py:133-135
-    coef[CO_CV * N + c] = -2.0 * n0.y * n0.x * (1.0 - n0.x);
-    coef[CO_GV * N + c] = -0.5 * P.beta * (n0.y + o0.y) + P.theta * (phi - psi) - 0.5 * P.gamma * (lvn + lvo);
+    double4 a;
+    a.x = P.theta * (dp + dq);                                   // S
+    a.y = P.theta * (dp - dq);                                   // D
+    a.z = (1.0 - 2.0 * n0.x) * (0.25 - n0.y * n0.y);             // c_u  (physics.py:133-135)
+    a.w = -2.0 * n0.y * n0.x * (1.0 - n0.x);                     // c_v
+    reinterpret_cast<double4 *>(coef)[c] = a;
+    double2 b;
+    b.x = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));   // cbar
+    b.y = -0.5 * P.alpha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) - 0.5 * P.gamma * (lun + luo);   // G_u
+    reinterpret_cast<double2 *>(coef + 4 * N)[c] = b;
+    coef[6 * N + c] = -0.5 * P.beta * (n0.y + o0.y) + P.theta * (phi - psi) - 0.5 * P.gamma * (lvn + lvo);   // G_v
 }
 
 // ---------------------------------------------------------------------------
@@ -310,13 +321,9 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
     double *sGu = sCb + R * GX * GY;
 
     const long long N = g.nstore;
-    const double *__restrict__ cS = coef + CO_S * N;
-    const double *__restrict__ cD = coef + CO_D * N;
-    const double *__restrict__ cC = coef + CO_CBAR * N;
-    const double *__restrict__ cG = coef + CO_GU * N;
-    const double *__restrict__ cU = coef + CO_CU * N;
-    const double *__restrict__ cV = coef + CO_CV * N;
-    const double *__restrict__ cGv = coef + CO_GV * N;
+    const double4 *__restrict__ cA = co_A(coef);
+    const double2 *__restrict__ cB = co_B(coef, N);
+    const double *__restrict__ cGv = co_Gv(coef, N);
 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
@@ -352,12 +359,14 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
                 const int ex = wrap_coord(x0 + i % GX - 1, nx, g.periodic);
                 const int ey = wrap_coord(y0 + i / GX - 1, ny, g.periodic);
                 const long long c = ((long long)gz * ny + ey) * nx + ex;
-                pS[j] = __ldg(cS + c);
-                pD[j] = __ldg(cD + c);
-                pU[j] = __ldg(cU + c);
-                pV[j] = __ldg(cV + c);
-                pC[j] = __ldg(cC + c);
-                pG[j] = __ldg(cG + c);
+                const double4 a = ldg256(cA + c);
+                const double2 b = __ldg(cB + c);
+                pS[j] = a.x;
+                pD[j] = a.y;
+                pU[j] = a.z;
+                pV[j] = a.w;
+                pC[j] = b.x;
+                pG[j] = b.y;
             }
         }
     };
@@ -430,7 +439,8 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
         double lapv = lxy;
         if (DIM == 3) lapv += (wvp - 2.0 * w0.y + wvm) * ihz;
         const long long c = cell_at(g, x, y, zplane(g, k));
-        const double S = __ldg(cS + c), D = __ldg(cD + c), Gv = __ldg(cGv + c);
+        const double4 a = ldg256(cA + c);
+        const double S = a.x, D = a.y, Gv = __ldg(cGv + c);
         double2 out;
         // reciprocals as in the reference's assembled blocks (idt = 1/dt,
         // scheme.py:471); 1/rho once per thread instead of two divisions per cell
@@ -516,10 +526,10 @@ template <int TX, int TY>
 struct ZmSmem {
     static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2;
     static constexpr int NW = HX * HY, NB = GX * GY, NRING = 2 * GX + 2 * TY;
-    static constexpr size_t bytes = sizeof(double2) * (3 * NW + 2 * 3 * NB);
+    static constexpr size_t bytes = sizeof(double2) * (4 * NW + 2 * 3 * NB);
 };
 
-template <int TX, int TY, int MINB>
+template <int TX, int TY, int MINB, bool PER>
 __global__ void __launch_bounds__(TX *TY, MINB)
 mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef, const double2 *__restrict__ w_g,
              double2 *__restrict__ yout, int nchunk)
@@ -529,8 +539,8 @@ mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
     constexpr int NWR = (NW + NT - 1) / NT;
     static_assert(NRING <= NT, "ring columns must fit one per thread");
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *sW = reinterpret_cast<double2 *>(smem_raw);      // [3][NW]   w
-    double2 *sB1 = sW + 3 * NW;                                  // [3][NB]   (dG_u, cbar)
+    double2 *sW = reinterpret_cast<double2 *>(smem_raw);      // [4][NW]   w
+    double2 *sB1 = sW + 4 * NW;                                  // [3][NB]   (dG_u, cbar)
     double2 *sB2 = sB1 + 3 * NB;                                 // [3][NB]   (eta, G_u)
 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
@@ -541,7 +551,12 @@ mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
     const int zb = (int)(((long long)blockIdx.z * g.nz) / nchunk);
     const int ze = (int)(((long long)(blockIdx.z + 1) * g.nz) / nchunk);
     const long long N = g.nstore;
+    const double4 *__restrict__ cA = co_A(coef);
+    const double2 *__restrict__ cB = co_B(coef, N);
+    const double *__restrict__ cGv = co_Gv(coef, N);
     const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
+    // flux weights 0.5/h^2: 0.5 (C0 + Cn) (Gn - G0) / h^2 == (C0 + Cn) (Gn - G0) (0.5/h^2) bitwise
+    const double fhx = 0.5 * ihx, fhy = 0.5 * ihy, fhz = 0.5 * ihz;
     const double hg = 0.5 * P.gamma, ha = -0.5 * P.alpha, hb = -0.5 * P.beta;
     const double idt = 1.0 / dt, irho = 1.0 / P.rho;
 
@@ -575,32 +590,31 @@ mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
     }
     const int x = x0 + tx, y = y0 + ty;
     const bool active = x < nx && y < ny;
-    const bool per = g.periodic != 0;
-    const bool fxl = per || x > 0, fxh = per || x < nx - 1, fyl = per || y > 0, fyh = per || y < ny - 1;
+    const bool fxl = PER || x > 0, fxh = PER || x < nx - 1, fyl = PER || y > 0, fyh = PER || y < ny - 1;
     const int jn = has_ring ? 2 : 1;
 
-    auto load_w = [&](int kk, int slot) {
-        const double2 *src = w_g + zplane(g, kk) * nxy;
+    // cp.async of one w plane (tile+2) into a ring slot; the caller commits
+    auto load_w = [&](long long poff, int slot) {
+        const double2 *src = w_g + poff;
         double2 *dst = sW + slot * NW + tid;
 #pragma unroll
         for (int r = 0; r < NWR; ++r)
             if (r < NWR - 1 || tid + r * NT < NW) cp_async16(dst + r * NT, src + woff[r]);
-        cp_async_commit();
     };
 
     double cS[2], cD[2], cU[2], cV[2], cC[2], cG[2];
-    auto prefetch = [&](int kk) {
-        const double *base = coef + zplane(g, kk) * nxy;
+    auto prefetch = [&](long long poff) {
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             if (j < jn) {
-                const double *p = base + coff[j];
-                cS[j] = __ldg(p + CO_S * N);
-                cD[j] = __ldg(p + CO_D * N);
-                cU[j] = __ldg(p + CO_CU * N);
-                cV[j] = __ldg(p + CO_CV * N);
-                cC[j] = __ldg(p + CO_CBAR * N);
-                cG[j] = __ldg(p + CO_GU * N);
+                const double4 a = ldg256(cA + poff + coff[j]);
+                const double2 b = __ldg(cB + poff + coff[j]);
+                cS[j] = a.x;
+                cD[j] = a.y;
+                cU[j] = a.z;
+                cV[j] = a.w;
+                cC[j] = b.x;
+                cG[j] = b.y;
             }
         }
     };
@@ -613,7 +627,7 @@ mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
     double Sk = 0.0, Dk = 0.0, Sk1 = 0.0, Dk1 = 0.0;  // centre S, D at planes k, k+1
 
     // build B(kk) from W(kk) (slot s1) and W(kk+1) (slot s2); wuz = w_u(kk-1)
-    auto build = [&](int kk, int s1, int s2, int sb) {
+    auto build = [&](int s1, int s2, int sb) {
         const double2 *W1 = sW + s1 * NW, *W2 = sW + s2 * NW;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
@@ -637,80 +651,87 @@ mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
                 }
             }
         }
-        (void)kk;
     };
 
-    // ring slots: W planes kk -> (kk - zb + 3) % 3 tracked by rotation
-    int sw1, sw2;                    // slots of W(k+1), W(k+2) at the top of iteration k
-    int sb0, sb1, sb2;               // slots of B(k-1), B(k), B(k+1)
+    // storage offsets of planes k .. k+3 (rolled once per plane, no division)
+    int z0 = zplane_near(g, zb), z1 = zplane_near(g, zb + 1), z2 = zplane_near(g, zb + 2), z3 = zplane_near(g, zb + 3);
+    auto poff = [&](int zs) { return (long long)zs * nxy; };
 
     // prologue: B(zb-1) and B(zb) are built before iteration zb; W(zb-2) is
-    // needed only as the z-neighbour w_u(zb-2) of each column (a register)
+    // needed only as the z-neighbour w_u(zb-2) of each column (a register).
+    // w planes are copied two iterations ahead (4-slot ring, one commit group
+    // per plane).
+    {
+        const long long pm2 = zplane_near(g, zb - 2) * nxy, pm1 = zplane_near(g, zb - 1) * nxy;
 #pragma unroll
-    for (int j = 0; j < 2; ++j)
-        if (j < jn) wuz[j] = __ldg(&w_g[zplane(g, zb - 2) * nxy + coff[j]].x);
-    load_w(zb - 1, 0);
-    load_w(zb, 1);
-    prefetch(zb - 1);
+        for (int j = 0; j < 2; ++j)
+            if (j < jn) wuz[j] = __ldg(&w_g[pm2 + coff[j]].x);
+        load_w(pm1, 0);
+        load_w(poff(z0), 1);
+        cp_async_commit();
+        prefetch(pm1);
+    }
     cp_async_wait_all();
     __syncthreads();
-    load_w(zb + 1, 2);
-    build(zb - 1, 0, 1, 0);      // B(zb-1) -> slot 0; needs W(zb) centre = slot 1
+    load_w(poff(z1), 2);
+    cp_async_commit();
+    load_w(poff(z2), 3);
+    cp_async_commit();
+    build(0, 1, 0);              // B(zb-1) -> slot 0; needs W(zb) centre = slot 1
     wvm = wk1.y;
-    prefetch(zb);
-    cp_async_wait_all();
+    prefetch(poff(z0));
+    cp_async_wait_group<1>();    // W(zb+1) landed, W(zb+2) may still be in flight
     __syncthreads();
-    // now W(zb) slot 1, W(zb+1) slot 2; slot 0 (W(zb-1)) is free
-    load_w(zb + 2, 0);
-    build(zb, 1, 2, 1);          // B(zb) -> slot 1
+    // now W(zb) slot 1, W(zb+1) slot 2, W(zb+2) slot 3; slot 0 (W(zb-1)) is free
+    load_w(poff(z3), 0);
+    cp_async_commit();
+    build(1, 2, 1);              // B(zb) -> slot 1
     wk = wk1;
     lxy_k = lxy_k1;
     Sk = Sk1;
     Dk = Dk1;
-    prefetch(zb + 1);
-    double gvk = active ? __ldg(coef + CO_GV * N + zplane(g, zb) * nxy + coff[0]) : 0.0;
-    // W slots: W(k+1) = 2, W(k+2) = 0 at k = zb
-    sw1 = 2;
-    sw2 = 0;
-    sb0 = 0;
-    sb1 = 1;
-    sb2 = 2;
+    prefetch(poff(z1));
+    double gvk = active ? __ldg(cGv + poff(z0) + coff[0]) : 0.0;
+    int sw1 = 2, sw2 = 3, sw3 = 0;   // slots of W(k+1), W(k+2), W(k+3) at the top of iteration k
+    int sb0 = 0, sb1 = 1, sb2 = 2;   // slots of B(k-1), B(k), B(k+1)
+    int z4 = zplane_near(g, zb + 4);
     for (int k = zb; k < ze; ++k) {
-        cp_async_wait_all();
+        cp_async_wait_group<1>();    // W(k+2) landed (W(k+3) may be in flight)
         __syncthreads();
-        // the W slot of plane k is free (W(k) lives in registers): W(k+3) into it
-        const int swf = 3 - sw1 - sw2;
-        if (k + 3 <= ze + 1) load_w(k + 3, swf);
-        build(k + 1, sw1, sw2, sb2);
+        // the W slot of plane k is free (W(k) lives in registers): W(k+4) into it
+        const int swf = 6 - sw1 - sw2 - sw3;
+        if (k + 4 <= ze + 1) load_w(poff(z4), swf);
+        cp_async_commit();           // possibly empty: keeps one group per plane
+        build(sw1, sw2, sb2);    // B(k+1)
         double gvn = 0.0;
-        if (k + 2 <= ze) prefetch(k + 2);
-        if (active && k + 1 < ze) gvn = __ldg(coef + CO_GV * N + zplane(g, k + 1) * nxy + coff[0]);
+        if (k + 2 <= ze) prefetch(poff(z2));
+        if (active && k + 1 < ze) gvn = __ldg(cGv + poff(z1) + coff[0]);
         if (active) {
             const double2 *B1 = sB1 + sb1 * NB, *B2 = sB2 + sb1 * NB;
             const int c0 = gc[0];
             const double2 a0 = B1[c0], e0 = B2[c0];
             const double dG0 = a0.x, C0 = a0.y, E0 = e0.x, G0 = e0.y;
             double d1 = 0.0, d2 = 0.0;
-            auto face = [&](const double2 &an, const double2 &en, double ih, bool lo_ok, bool hi_ok,
+            auto face = [&](const double2 &an, const double2 &en, double fh, bool lo_ok, bool hi_ok,
                             const double2 &am, const double2 &em) {
                 if (hi_ok) {
-                    d1 += 0.5 * (C0 + an.y) * (an.x - dG0) * ih;
-                    d2 += 0.5 * (E0 + en.x) * (en.y - G0) * ih;
+                    d1 += (C0 + an.y) * (an.x - dG0) * fh;
+                    d2 += (E0 + en.x) * (en.y - G0) * fh;
                 }
                 if (lo_ok) {
-                    d1 -= 0.5 * (C0 + am.y) * (dG0 - am.x) * ih;
-                    d2 -= 0.5 * (E0 + em.x) * (G0 - em.y) * ih;
+                    d1 -= (C0 + am.y) * (dG0 - am.x) * fh;
+                    d2 -= (E0 + em.x) * (G0 - em.y) * fh;
                 }
             };
-            face(B1[c0 + 1], B2[c0 + 1], ihx, fxl, fxh, B1[c0 - 1], B2[c0 - 1]);
-            face(B1[c0 + GX], B2[c0 + GX], ihy, fyl, fyh, B1[c0 - GX], B2[c0 - GX]);
-            face(sB1[sb2 * NB + c0], sB2[sb2 * NB + c0], ihz, zstep_ok(g, k, -1), zstep_ok(g, k, +1),
+            face(B1[c0 + 1], B2[c0 + 1], fhx, fxl, fxh, B1[c0 - 1], B2[c0 - 1]);
+            face(B1[c0 + GX], B2[c0 + GX], fhy, fyl, fyh, B1[c0 - GX], B2[c0 - GX]);
+            face(sB1[sb2 * NB + c0], sB2[sb2 * NB + c0], fhz, PER || zstep_ok(g, k, -1), PER || zstep_ok(g, k, +1),
                  sB1[sb0 * NB + c0], sB2[sb0 * NB + c0]);
             const double lapv = lxy_k + (wk1.y - 2.0 * wk.y + wvm) * ihz;
             double2 out;
             out.x = wk.x * idt - d1 - d2;
             out.y = wk.y * idt + (C0 * irho) * (Dk * wk.x + (hb + Sk) * wk.y - hg * lapv) + (gvk * irho) * E0;
-            yout[zplane(g, k) * nxy + coff[0]] = out;
+            yout[poff(z0) + coff[0]] = out;
         }
         // rotate
         wvm = wk.y;
@@ -720,11 +741,17 @@ mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
         Dk = Dk1;
         gvk = gvn;
         sw1 = sw2;
-        sw2 = swf;
+        sw2 = sw3;
+        sw3 = swf;
         const int tb = sb0;
         sb0 = sb1;
         sb1 = sb2;
         sb2 = tb;
+        z0 = z1;
+        z1 = z2;
+        z2 = z3;
+        z3 = z4;
+        z4 = zplane_near(g, k + 5);
     }
 }
 
@@ -768,9 +795,9 @@ mv_pass1_kernel(GridDev g, ParamsDev P, const double *__restrict__ coef, const d
         lap += (__ldg(w + cell_at(g, x, y, zplane(g, z + 1))).x - 2.0 * w0.x +
                 __ldg(w + cell_at(g, x, y, zplane(g, z - 1))).x) * g.ih2[2];
     double2 t;
-    t.x = (-0.5 * P.alpha + __ldg(coef + CO_S * N + c)) * w0.x + __ldg(coef + CO_D * N + c) * w0.y -
-          0.5 * P.gamma * lap;
-    t.y = 0.5 * (__ldg(coef + CO_CU * N + c) * w0.x + __ldg(coef + CO_CV * N + c) * w0.y);
+    const double4 a = ldg256(co_A(coef) + c);
+    t.x = (-0.5 * P.alpha + a.x) * w0.x + a.y * w0.y - 0.5 * P.gamma * lap;
+    t.y = 0.5 * (a.z * w0.x + a.w * w0.y);
     T[c] = t;
 }
 
@@ -785,17 +812,18 @@ mv_pass2_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ co
     const int zs = zplane(g, z);
     const long long c = cell_at(g, x, y, zs);
     const long long N = g.nstore;
-    const double *__restrict__ cC = coef + CO_CBAR * N;
-    const double *__restrict__ cG = coef + CO_GU * N;
+    const double2 *__restrict__ cB = co_B(coef, N);
     const double2 t0 = __ldg(T + c), w0 = __ldg(w + c);
-    const double C0 = __ldg(cC + c), G0 = __ldg(cG + c);
+    const double2 b0 = __ldg(cB + c);
+    const double C0 = b0.x, G0 = b0.y;
     const bool per = g.periodic != 0;
     double d1 = 0.0, d2 = 0.0, lapv = 0.0;
     auto face = [&](long long cn, double ih, bool ok, double sgn) {
         // sgn = +1 for the upper face (n - c), -1 for the lower face (c - n)
         if (!ok) return;
         const double2 tn = __ldg(T + cn);
-        const double Cn = __ldg(cC + cn), Gn = __ldg(cG + cn);
+        const double2 bn = __ldg(cB + cn);
+        const double Cn = bn.x, Gn = bn.y;
         d1 += 0.5 * (C0 + Cn) * (tn.x - t0.x) * ih;
         d2 += 0.5 * (t0.y + tn.y) * (Gn - G0) * ih;
         (void)sgn;
@@ -817,7 +845,8 @@ mv_pass2_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ co
         face(czm, g.ih2[2], zstep_ok(g, z, -1), -1.0);
         lapv += (__ldg(w + czp).y - 2.0 * w0.y + __ldg(w + czm).y) * g.ih2[2];
     }
-    const double S = __ldg(coef + CO_S * N + c), D = __ldg(coef + CO_D * N + c), Gv = __ldg(coef + CO_GV * N + c);
+    const double2 sd = __ldg(reinterpret_cast<const double2 *>(coef) + 2 * c);   // (S, D) half of A[c]
+    const double S = sd.x, D = sd.y, Gv = __ldg(co_Gv(coef, N) + c);
     const double hg = 0.5 * P.gamma;
     double2 out;
     const double idt = 1.0 / dt, irho = 1.0 / P.rho;   // reciprocals (see matvec_kernel)
@@ -1076,7 +1105,8 @@ static int choose_zchunks(int tiles, int nz, int per_sm, int sms, double startup
     const long long slots = (long long)per_sm * sms;
     int best = 1;
     double best_cost = 1e300;
-    for (int c = 1; c <= nz; ++c) {
+    // chunks of at least 2 planes (the start-up reads planes up to zb + 3)
+    for (int c = 1; c <= (nz >= 4 ? nz / 2 : 1); ++c) {
         const long long items = (long long)tiles * c;
         const long long waves = (items + slots - 1) / slots;
         const double cost = (double)waves * ((double)nz / c + startup);
@@ -1088,12 +1118,12 @@ static int choose_zchunks(int tiles, int nz, int per_sm, int sms, double startup
     return best;
 }
 
-template <int MINB>
+template <int MINB, bool PER>
 static acch_status launch_matvec_zm_t(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
     constexpr int TX = 32, TY = 8;
     using L = ZmSmem<TX, TY>;
-    auto kern = mv_zm_kernel<TX, TY, MINB>;
+    auto kern = mv_zm_kernel<TX, TY, MINB, PER>;
     static int per_sm = 0, sms = 0;
     if (!per_sm) {
         acch_status st = set_smem(kern, L::bytes);
@@ -1114,8 +1144,10 @@ static acch_status launch_matvec_zm_t(acch_ctx *ctx, const double *coef, double 
 static acch_status launch_matvec_zm(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
     const char *e = getenv("ACCH_ZM_MINB");
-    if (e && atoi(e) == 3) return launch_matvec_zm_t<3>(ctx, coef, dt, w, y);
-    return launch_matvec_zm_t<2>(ctx, coef, dt, w, y);
+    const bool per = ctx->g.periodic != 0;
+    if (e && atoi(e) == 3)
+        return per ? launch_matvec_zm_t<3, true>(ctx, coef, dt, w, y) : launch_matvec_zm_t<3, false>(ctx, coef, dt, w, y);
+    return per ? launch_matvec_zm_t<2, true>(ctx, coef, dt, w, y) : launch_matvec_zm_t<2, false>(ctx, coef, dt, w, y);
 }
 
 acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
@@ -1127,6 +1159,7 @@ acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const do
     if (mode && strcmp(mode, "fused") == 0) m = 0;
     if (mode && strcmp(mode, "twopass") == 0) m = 1;
     if (mode && strcmp(mode, "zm") == 0 && ctx->g.dim == 3) m = 2;
+    if (m == 2 && ctx->g.nz < 3) m = 1;   // the z-marching kernel's plane map assumes nz >= 3
     ctx->matvec_mode = m;
     ProfScope prof_scope(ctx, PC_MATVEC, 88.0 * ctx->g.n);
     if (m == 2) return launch_matvec_zm(ctx, coef, dt, w, y);

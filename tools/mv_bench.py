@@ -64,12 +64,14 @@ def main():
     out["residual"] = {"ms": round(t, 4), "frac": round(48 * N / t / 1e6 / peak, 4)}
     ys = {}
     for form in args.forms.split(","):
-        name, _, minb = form.partition(":")
+        # form[:minb[:pfd]]
+        name, *opt = form.split(":")
         os.environ["ACCH_MATVEC"] = name
-        if minb:
-            os.environ["ACCH_ZM_MINB"] = minb
-        else:
-            os.environ.pop("ACCH_ZM_MINB", None)
+        for key, val in zip(("ACCH_ZM_MINB", "ACCH_ZM_PFD"), opt + [""] * 2):
+            if val:
+                os.environ[key] = val
+            else:
+                os.environ.pop(key, None)
         y = torch.empty_like(w)
         t = timeit(lambda: J.matvec_into(w, y), args.reps)
         ys[form] = y
