@@ -529,10 +529,22 @@ struct ZmSmem {
     static constexpr size_t bytes = sizeof(double2) * (4 * NW + 2 * 3 * NB);
 };
 
+// host-computed constants of the matvec (kernel parameters, i.e. constant-bank
+// operands, so they cost no registers in the plane loop)
+struct MvConst {
+    const double4 *A;
+    const double2 *B;
+    const double *Gv;
+    double ihx, ihy, ihz;    // 1/h^2
+    double fhx, fhy, fhz;    // 0.5/h^2 (flux weights)
+    double hg, ha, hb;       // gamma/2, -alpha/2, -beta/2
+    double idt, irho;        // 1/dt, 1/rho
+};
+
 template <int TX, int TY, int MINB, bool PER>
 __global__ void __launch_bounds__(TX *TY, MINB)
-mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef, const double2 *__restrict__ w_g,
-             double2 *__restrict__ yout, int nchunk)
+mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g, double2 *__restrict__ yout,
+             int nchunk)
 {
     using L = ZmSmem<TX, TY>;
     constexpr int HX = L::HX, GX = L::GX, NW = L::NW, NB = L::NB, NRING = L::NRING, NT = TX * TY;
@@ -550,15 +562,14 @@ mv_zm_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
     // z range of this chunk: chunks split nz as evenly as possible
     const int zb = (int)(((long long)blockIdx.z * g.nz) / nchunk);
     const int ze = (int)(((long long)(blockIdx.z + 1) * g.nz) / nchunk);
-    const long long N = g.nstore;
-    const double4 *__restrict__ cA = co_A(coef);
-    const double2 *__restrict__ cB = co_B(coef, N);
-    const double *__restrict__ cGv = co_Gv(coef, N);
-    const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
+    const double4 *__restrict__ cA = mc.A;
+    const double2 *__restrict__ cB = mc.B;
+    const double *__restrict__ cGv = mc.Gv;
+    const double &ihx = mc.ihx, &ihy = mc.ihy, &ihz = mc.ihz;
     // flux weights 0.5/h^2: 0.5 (C0 + Cn) (Gn - G0) / h^2 == (C0 + Cn) (Gn - G0) (0.5/h^2) bitwise
-    const double fhx = 0.5 * ihx, fhy = 0.5 * ihy, fhz = 0.5 * ihz;
-    const double hg = 0.5 * P.gamma, ha = -0.5 * P.alpha, hb = -0.5 * P.beta;
-    const double idt = 1.0 / dt, irho = 1.0 / P.rho;
+    const double &fhx = mc.fhx, &fhy = mc.fhy, &fhz = mc.fhz;
+    const double &hg = mc.hg, &ha = mc.ha, &hb = mc.hb;
+    const double &idt = mc.idt, &irho = mc.irho;
 
     // w tile+2 copy offsets (plane-relative)
     int woff[NWR];
@@ -1135,8 +1146,22 @@ static acch_status launch_matvec_zm_t(acch_ctx *ctx, const double *coef, double 
     const GridDev &g = ctx->g;
     const int gx = (g.nx + TX - 1) / TX, gy = (g.ny + TY - 1) / TY;
     const int nchunk = choose_zchunks(gx * gy, g.nz, per_sm, sms, 3.0);
-    kern<<<dim3(gx, gy, nchunk), dim3(TX, TY), L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
-                                                                       (double2 *)y, nchunk);
+    MvConst mc;
+    mc.A = co_A(coef);
+    mc.B = co_B(coef, g.nstore);
+    mc.Gv = co_Gv(coef, g.nstore);
+    mc.ihx = g.ih2[0];
+    mc.ihy = g.ih2[1];
+    mc.ihz = g.ih2[2];
+    mc.fhx = 0.5 * g.ih2[0];
+    mc.fhy = 0.5 * g.ih2[1];
+    mc.fhz = 0.5 * g.ih2[2];
+    mc.hg = 0.5 * ctx->p.gamma;
+    mc.ha = -0.5 * ctx->p.alpha;
+    mc.hb = -0.5 * ctx->p.beta;
+    mc.idt = 1.0 / dt;
+    mc.irho = 1.0 / ctx->p.rho;
+    kern<<<dim3(gx, gy, nchunk), dim3(TX, TY), L::bytes, ctx->stream>>>(g, mc, (const double2 *)w, (double2 *)y, nchunk);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
 }
