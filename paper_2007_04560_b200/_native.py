@@ -17,7 +17,7 @@ import torch
 from .exceptions import (InadmissibleStateError, PartitionError, ZeroPivotError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libacch_b200.so")
+LIB_PATH = os.environ.get("ACCH_LIB_PATH") or os.path.join(_HERE, "libacch_b200.so")   # override: experiments only
 
 ACCH_OK = 0
 ACCH_ERR_INVALID_ARG = 1

@@ -71,6 +71,10 @@ struct ClassDev {
     // the row's CSR pattern, update target -> index within row i's pattern
     const int *jmap_local, *upd_dl;
     int rmax;   // longest pattern row
+    // row-sequential batched solver (apply_rs_kernel): shared-memory image
+    // lenL[nloc] | lenU[nloc] | own[nloc] (uint8) | colL[nL] | colU[nU] (uint16) | rel x,y,z (int)
+    const unsigned char *rs_meta;
+    int rs_meta_bytes, rs_m_lenU, rs_m_own, rs_m_colL, rs_m_colU, rs_m_rel, rs_nL, rs_ring, rs_far;
     int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
 };
 
@@ -85,6 +89,14 @@ struct ClassHost {
     std::vector<unsigned char> owned;
     std::vector<unsigned char> meta;   // ClassDev::meta image
     std::vector<int> lin, own_list, jmap_local, upd_dl;
+    // CSR-entry forms of jmap / upd (before the slot layout is applied) and
+    // the row-sequential layout: forward rows ascending (L entries), then
+    // backward rows descending ([inv D_i] + U entries)
+    std::vector<int> jmap_csr;
+    std::vector<int2> upd_csr;
+    std::vector<int> rs_pos;
+    std::vector<unsigned char> rs_meta;
+    int rs_ok = 0, rs_ring = 0, rs_nL = 0, rs_far = 0, rs_m[5] = {0};
     int rmax = 0;
     int m_off[13] = {0};
     int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
@@ -109,6 +121,13 @@ struct Blk {
     double a, b, c, d;   // [[a, b], [c, d]]
 };
 
+// a subdomain's factor slots: slot p at base[p * stride]
+struct StridedBlocks {
+    double4 *base;
+    int stride;
+    __device__ __forceinline__ double4 &operator[](long long p) const { return base[p * stride]; }
+};
+
 __device__ __forceinline__ Blk mul(const Blk &x, const Blk &y)
 {
     return {x.a * y.a + x.b * y.c, x.a * y.b + x.b * y.d, x.c * y.a + x.d * y.c, x.c * y.b + x.d * y.d};
@@ -118,13 +137,14 @@ template <int DIM>
 __global__ void __launch_bounds__(kFactorThreads)
 factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef, const ClassDev *__restrict__ classes,
               const int *__restrict__ sub_class, const int4 *__restrict__ sub_origin,
-              const long long *__restrict__ sub_off, double4 *__restrict__ vals, int *__restrict__ bad_row)
+              const long long *__restrict__ sub_off, double4 *__restrict__ vals, int *__restrict__ bad_row, int ss)
 {
+    // slot p of this subdomain lives at A[p * ss] (ss = 8: row-sequential batches)
     constexpr int NOFF = DIM == 3 ? 25 : 13;
     const int s = blockIdx.x;
     const ClassDev C = classes[sub_class[s]];
     const int4 o = sub_origin[s];
-    double4 *A = vals + sub_off[s];
+    StridedBlocks A{vals + sub_off[s], ss};
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int t = tid; t < C.ell_total; t += nt) A[t] = make_double4(0.0, 0.0, 0.0, 0.0);
     __syncthreads();
@@ -197,7 +217,7 @@ __global__ void __launch_bounds__(NW * 32)
 factor_warp_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
                    const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
                    const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
-                   double4 *__restrict__ vals, int *__restrict__ bad_row, long long nsub, int rstride)
+                   double4 *__restrict__ vals, int *__restrict__ bad_row, long long nsub, int rstride, int ss)
 {
     constexpr int NOFF = DIM == 3 ? 25 : 13;
     constexpr int UB = 8;
@@ -207,7 +227,7 @@ factor_warp_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__
     if (s >= nsub) return;
     const ClassDev &C = classes[sub_class[s]];
     const int4 o = sub_origin[s];
-    double4 *A = vals + sub_off[s];
+    StridedBlocks A{vals + sub_off[s], ss};
     // row buffer: entry j of the lane's row at rb[j * 32] (conflict-free across lanes)
     double4 *rb = reinterpret_cast<double4 *>(smem_raw) + (size_t)warp * 32 * rstride + lane;
     for (int lev = 0; lev < C.nlev; ++lev) {
@@ -863,6 +883,284 @@ apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *
 }
 
 // ---------------------------------------------------------------------------
+// Row-sequential batched solver (opt-in: ACCH_RS=1; measured slower than the
+// class-group solver at the bench size, kept as a tested alternative).
+//
+// A warp solves 8 subdomains of ONE class at once, row after row, with no
+// level schedule: lane = 8 q + b works on subdomain b and on the blocks
+// t = q, q + 4, q + 8 of the current row (rows have <= 12 blocks), and the
+// four partial sums of a row are combined by two shuffles.  Because the 8
+// subdomains share the class's pattern, every lane runs the same row at the
+// same time, and the factor blocks of a batch are stored slot-major and
+// subdomain-minor (slot p of subdomain b at batch_base + 8 p + b), so one
+// row's blocks are one contiguous, fully coalesced 1 KB stream per warp step.
+// Blocks are loaded RS_D rows ahead into registers; the solution values a
+// row reads (<= max|i - j| rows back / ahead) live in a per-warp shared
+// memory ring; the forward result y is kept in an L2-resident scratch
+// (one slot per resident warp, indexed by %smid) for the backward sweep.
+// ---------------------------------------------------------------------------
+
+constexpr int RS_B = 8;       // subdomains per warp
+#ifndef ACCH_RS_D
+#define ACCH_RS_D 3
+#endif
+constexpr int RS_D = ACCH_RS_D;   // rows of factor blocks in flight per warp
+constexpr int RS_PITCH = 9;   // ring row pitch in double2 (8 subdomains + 1: conflict-free gathers)
+
+// volatile: issued where written (RS_D rows ahead of its use), never sunk
+// toward the consuming FMA by the scheduler
+__device__ __forceinline__ double4 ldg_stream(const double4 *p, uint64_t pol)
+{
+    double4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+        : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+        : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ unsigned smid()
+{
+    unsigned r;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+    return r;
+}
+
+template <int VARIANT, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+apply_rs_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *__restrict__ items,
+                const int4 *__restrict__ batches, const long long *__restrict__ batch_base,
+                const int *__restrict__ members, const int4 *__restrict__ sub_origin,
+                const long long *__restrict__ sub_ext_off, const double4 *__restrict__ vals,
+                const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
+                double2 *__restrict__ scratch, int meta_pad, int ring_stride, int max_nloc, int pf_rows)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int4 it = items[blockIdx.x];   // (class, first batch, batches, -)
+    const ClassDev &C = classes[it.x];
+    {
+        const uint4 *__restrict__ src = reinterpret_cast<const uint4 *>(C.rs_meta);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem_raw);
+        for (int i = threadIdx.x; i < C.rs_meta_bytes / 16; i += NW * 32) dst[i] = __ldg(src + i);
+    }
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp >= it.z) return;
+    const unsigned char *lenL = smem_raw, *lenU = smem_raw + C.rs_m_lenU, *own = smem_raw + C.rs_m_own;
+    const unsigned short *colL = reinterpret_cast<const unsigned short *>(smem_raw + C.rs_m_colL);
+    const unsigned short *colU = reinterpret_cast<const unsigned short *>(smem_raw + C.rs_m_colU);
+    const int *relx = reinterpret_cast<const int *>(smem_raw + C.rs_m_rel);
+    const int lx = C.len[0], ly = C.len[1], lz = C.len[2];
+    const int *rely = relx + lx, *relz = rely + ly;
+    const int nloc = C.nloc, R = C.rs_ring, nL = C.rs_nL;
+    const bool any_far = C.rs_far != 0;
+
+    const int4 bt = batches[it.y + warp];   // (first member, count, -, -)
+    const int b = lane & 7, q = lane >> 3;
+    const bool bval = b < bt.y;
+    const int s = members[bt.x + (bval ? b : 0)];
+    const int4 o = sub_origin[s];
+    const double4 *__restrict__ A = vals + batch_base[it.y + warp] + b;     // slot p at A[8 p]
+    double2 *ring = reinterpret_cast<double2 *>(smem_raw + meta_pad) + (size_t)warp * ring_stride + b;
+    double2 *scr = scratch + ((size_t)smid() * NW + warp) * (size_t)max_nloc * RS_B + b;   // row i at scr[8 i]
+    const uint64_t pol = evict_first_policy();
+
+    // column code -> operand index: ring element (>= 0) or, for a far
+    // column, ~(scratch element) (< 0)
+    auto operand = [&](unsigned code) -> int {
+        return (code & 0x8000u) ? ~(int)((code & 0x7fffu) * RS_B) : (int)code * RS_PITCH;
+    };
+    // sum over this lane's blocks of a row: acc -= blk * x[col]; blocks
+    // 12.. of a long row (block t at slot off + t, column code col[t]) are
+    // loaded here
+    auto row_sum = [&](double2 &acc, const double4 (&f)[3], const int (&c)[3], int len, bool far, int off,
+                       const unsigned short *col) {
+        if (!far) {
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+                if (4 * u + q < len) blk_sub(acc, f[u], ring[c[u]]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 3; ++u)
+                if (4 * u + q < len) blk_sub(acc, f[u], c[u] >= 0 ? ring[c[u]] : scr[~c[u]]);
+        }
+        for (int t = 12 + q; t < len; t += 4) {
+            const int cu = operand(col[t]);
+            blk_sub(acc, ldg_stream(A + (size_t)(off + t) * RS_B, pol), cu >= 0 ? ring[cu] : scr[~cu]);
+        }
+    };
+
+    // storage index of local cell (ix, iy, iz) of this lane's subdomain
+    auto cell = [&](int ix, int iy, int iz) -> long long {
+        int gx = o.x + relx[ix];
+        if (gx >= g.nx) gx -= g.nx;
+        int gy = o.y + rely[iy];
+        if (gy >= g.ny) gy -= g.ny;
+        int gz = 0;
+        if (g.dim == 3) {
+            gz = o.z + relz[iz];
+            if (g.zg == 0) gz = gz >= g.nz ? gz - g.nz : gz;
+            else gz += g.zg;
+        }
+        return ((long long)gz * g.ny + gy) * g.nx + gx;
+    };
+
+    // ---------------- forward sweep: y_i = r_i - sum_j L_ij y_j ----------------
+    double4 F[RS_D][3];
+    int Cc[RS_D][3];
+    double2 Rv[RS_D];
+    int ld_i = 0, ld_off = 0, lx_ = 0, ly_ = 0, lz_ = 0;
+    // every lane issues the same number of loads per row (a block past the
+    // row's end re-reads its last block), so the compiler can wait for a
+    // row's loads by count while the later rows' loads stay in flight
+    auto issue_fwd = [&](double4 (&f)[3], int (&c)[3], double2 &rv) {
+        if (ld_i < nloc) {
+            const int len = lenL[ld_i] & 0x7f;
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int t = 4 * u + q;
+                if (t < len) {   // (blocks 12.. of a long row: row_sum)
+                    f[u] = ldg_stream(A + (size_t)(ld_off + t) * RS_B, pol);
+                    c[u] = operand(colL[ld_off + t]);
+                }
+            }
+            const bool keep = VARIANT != 2 || own[ld_i];
+            rv = (bval && keep) ? r[cell(lx_, ly_, lz_)] : make_double2(0.0, 0.0);
+            ld_off += len;
+            ++ld_i;
+            if (++lx_ == lx) {
+                lx_ = 0;
+                if (++ly_ == ly) {
+                    ly_ = 0;
+                    ++lz_;
+                }
+            }
+        }
+    };
+    // the TMA engine pulls the batch's blocks pf_rows rows ahead into L2, so
+    // the register loads RS_D rows ahead hit L2
+    const char *Abatch = reinterpret_cast<const char *>(A - b);
+    int pf_i = 0, pf_off = 0;
+    auto prefetch_fwd = [&]() {
+        if (pf_i < nloc) {
+            const int len = lenL[pf_i] & 0x7f;
+            if (lane == 0 && len) prefetch_l2(Abatch + (size_t)pf_off * RS_B * 32, (unsigned)len * RS_B * 32);
+            pf_off += len;
+            ++pf_i;
+        }
+    };
+    for (int k = 0; k < pf_rows; ++k) prefetch_fwd();
+#pragma unroll
+    for (int st = 0; st < RS_D; ++st) issue_fwd(F[st], Cc[st], Rv[st]);
+    int ri = 0, off_c = 0;
+    for (int i0 = 0; i0 < nloc; i0 += RS_D) {
+#pragma unroll
+        for (int st = 0; st < RS_D; ++st) {
+            const int i = i0 + st;
+            if (i < nloc) {
+                const int lv = lenL[i];
+                double2 acc = make_double2(0.0, 0.0);
+                row_sum(acc, F[st], Cc[st], lv & 0x7f, (lv & 0x80) != 0, off_c, colL + off_c);
+                off_c += lv & 0x7f;
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+                const double2 yi = make_double2(Rv[st].x + acc.x, Rv[st].y + acc.y);
+                if (q == 0) {
+                    ring[ri * RS_PITCH] = yi;
+                    scr[(size_t)i * RS_B] = yi;
+                }
+                ri = ri + 1 == R ? 0 : ri + 1;
+                issue_fwd(F[st], Cc[st], Rv[st]);
+                prefetch_fwd();
+                __syncwarp();
+            }
+        }
+    }
+
+    // ------------- backward sweep: x_i = inv(D_i) (y_i - sum_j U_ij x_j) -------------
+    double4 Di[RS_D];
+    double2 Yv[RS_D];
+    int bl_i = nloc - 1, bl_off = nL, bl_offu = 0;
+    auto issue_bwd = [&](double4 (&f)[3], int (&c)[3], double4 &di, double2 &yv) {
+        if (bl_i >= 0) {
+            const int len = lenU[bl_i] & 0x7f;
+            di = ldg_stream(A + (size_t)bl_off * RS_B, pol);
+#pragma unroll
+            for (int u = 0; u < 3; ++u) {
+                const int t = 4 * u + q;
+                if (t < len) {
+                    f[u] = ldg_stream(A + (size_t)(bl_off + 1 + t) * RS_B, pol);
+                    c[u] = operand(colU[bl_offu + t]);
+                }
+            }
+            yv = scr[(size_t)bl_i * RS_B];   // coherent load: written by this warp above
+            bl_off += 1 + len;
+            bl_offu += len;
+            --bl_i;
+        }
+    };
+    int pb_i = nloc - 1, pb_off = nL;
+    auto prefetch_bwd = [&]() {
+        if (pb_i >= 0) {
+            const int len = 1 + (lenU[pb_i] & 0x7f);
+            if (lane == 0) prefetch_l2(Abatch + (size_t)pb_off * RS_B * 32, (unsigned)len * RS_B * 32);
+            pb_off += len;
+            --pb_i;
+        }
+    };
+    for (int k = 0; k < pf_rows; ++k) prefetch_bwd();
+#pragma unroll
+    for (int st = 0; st < RS_D; ++st) issue_bwd(F[st], Cc[st], Di[st], Yv[st]);
+    ri = (nloc - 1) % R;
+    int cx = lx - 1, cy = ly - 1, cz = lz - 1, offb_c = nL, offu_c = 0;
+    const long long eoff = VARIANT != 1 ? sub_ext_off[s] : 0;
+    for (int k0 = 0; k0 < nloc; k0 += RS_D) {
+#pragma unroll
+        for (int st = 0; st < RS_D; ++st) {
+            const int i = nloc - 1 - (k0 + st);
+            if (i >= 0) {
+                const int lv = lenU[i];
+                double2 acc = make_double2(0.0, 0.0);
+                // U block t of row i: slot offb_c + 1 + t, code colU[offu_c + t]
+                row_sum(acc, F[st], Cc[st], lv & 0x7f, (lv & 0x80) != 0, offb_c + 1, colU + offu_c);
+                offb_c += 1 + (lv & 0x7f);
+                offu_c += lv & 0x7f;
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
+                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
+                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
+                const double2 v = make_double2(Yv[st].x + acc.x, Yv[st].y + acc.y);
+                const double4 d = Di[st];
+                const double2 xi = make_double2(d.x * v.x + d.y * v.y, d.z * v.x + d.w * v.y);
+                if (q == 0) {
+                    ring[ri * RS_PITCH] = xi;
+                    if (any_far) scr[(size_t)i * RS_B] = xi;   // far columns of later rows read x here
+                    if (bval) {
+                        if (VARIANT == 1) {
+                            if (own[i]) z[cell(cx, cy, cz)] = xi;
+                        } else {
+                            ext_out[eoff + i] = xi;
+                        }
+                    }
+                }
+                ri = ri == 0 ? R - 1 : ri - 1;
+                if (--cx < 0) {
+                    cx = lx - 1;
+                    if (--cy < 0) {
+                        cy = ly - 1;
+                        --cz;
+                    }
+                }
+                issue_bwd(F[st], Cc[st], Di[st], Yv[st]);
+                prefetch_bwd();
+                __syncwarp();
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // TMA-streamed warp solver.  Same sweeps as apply_warp_kernel, but each
 // level's factor slots and column ids are brought into a per-warp
 // shared-memory ring by cp.async.bulk (TMA) several levels ahead, completion
@@ -1274,6 +1572,74 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
         }
         for (int t = C.rowptr[i]; t < C.rowptr[i + 1]; ++t) where[C.col[t]] = -1;
     }
+    C.jmap_csr = C.jmap;
+    C.upd_csr = C.upd;
+    // row-sequential layout (apply_rs_kernel): eligible when every L / U row
+    // has <= 24 blocks (blocks 0..11 of a row are prefetched, 3 per lane of a
+    // 4-lane row group; the wrapped layer of a periodic box makes some rows
+    // longer, whose tail blocks are loaded when the row is solved).  A column within
+    // 255 rows of its row is read from the per-warp ring of the last R rows;
+    // a farther one (the wrapped layer of a periodic box sorts to the other
+    // end of the local order) from the warp's y / x scratch in L2.
+    {
+        C.rs_pos.assign(C.nnzb, -1);
+        int slot = 0, near = 0, maxlen = 0;
+        for (int i = 0; i < nloc; ++i) {
+            for (int t = C.rowptr[i]; t < C.diag[i]; ++t) C.rs_pos[t] = slot++;
+            maxlen = std::max(maxlen, C.diag[i] - C.rowptr[i]);
+            for (int t = C.rowptr[i]; t < C.rowptr[i + 1]; ++t) {
+                const int d = std::abs(C.col[t] - i);
+                if (d <= 255) near = std::max(near, d);
+            }
+        }
+        C.rs_nL = slot;
+        for (int i = nloc - 1; i >= 0; --i) {
+            for (int t = C.diag[i]; t < C.rowptr[i + 1]; ++t) C.rs_pos[t] = slot++;
+            maxlen = std::max(maxlen, C.rowptr[i + 1] - C.diag[i] - 1);
+        }
+        const int R = near + 1;
+        C.rs_ring = R;
+        C.rs_ok = maxlen <= 24 && nloc <= 32767;
+        const int nL = C.rs_nL, nU = C.nnzb - nloc - nL;
+        size_t at = 0;
+        auto seg = [&](size_t bytes) { size_t o = at; at += (bytes + 15) / 16 * 16; return (int)o; };
+        seg(nloc);
+        C.rs_m[0] = seg(nloc);                     // lenU
+        C.rs_m[1] = seg(nloc);                     // own
+        C.rs_m[2] = seg(2 * (size_t)nL);           // colL (uint16)
+        C.rs_m[3] = seg(2 * (size_t)std::max(nU, 1));   // colU (uint16)
+        C.rs_m[4] = seg(sizeof(int) * (lx + ly + lz));
+        C.rs_meta.assign(at, 0);
+        unsigned char *m = C.rs_meta.data();
+        unsigned short *cl = reinterpret_cast<unsigned short *>(m + C.rs_m[2]);
+        unsigned short *cu = reinterpret_cast<unsigned short *>(m + C.rs_m[3]);
+        // entry code: ring slot j mod R (near) or 0x8000 | j (far); bit 7 of a
+        // row length flags a row with a far entry
+        auto code = [&](int i, int j, bool &far) -> unsigned short {
+            if (std::abs(j - i) < R) return (unsigned short)(j % R);
+            far = true;
+            return (unsigned short)(0x8000 | j);
+        };
+        int kl = 0, ku = 0;
+        C.rs_far = 0;
+        for (int i = 0; i < nloc; ++i) {
+            bool far = false;
+            for (int t = C.rowptr[i]; t < C.diag[i]; ++t) cl[kl++] = code(i, C.col[t], far);
+            m[i] = (unsigned char)((C.diag[i] - C.rowptr[i]) | (far ? 0x80 : 0));
+            C.rs_far |= far;
+        }
+        for (int i = nloc - 1; i >= 0; --i) {
+            bool far = false;
+            for (int t = C.diag[i] + 1; t < C.rowptr[i + 1]; ++t) cu[ku++] = code(i, C.col[t], far);
+            m[C.rs_m[0] + i] = (unsigned char)((C.rowptr[i + 1] - C.diag[i] - 1) | (far ? 0x80 : 0));
+            C.rs_far |= far;
+        }
+        int *rl = reinterpret_cast<int *>(m + C.rs_m[4]);
+        for (int a = 0, k = 0; a < 3; ++a) {
+            const int la = a == 0 ? lx : (a == 1 ? ly : lz);
+            for (int i = 0; i < la; ++i) rl[k++] = a < dim ? rel[a][i] : 0;
+        }
+    }
     // level schedules from the factor DAG
     std::vector<int> lev(nloc, 0), levb(nloc, 0);
     int nlev = 0, nlevb = 0;
@@ -1369,7 +1735,18 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
         C.owned[l] = own ? 1 : 0;
         if (own) C.own_list.push_back(l);
     }
+    for (int l = 0; l < nloc; ++l) C.rs_meta[C.rs_m[1] + l] = C.owned[l];
     return true;
+}
+
+// switch a class to the row-sequential slot layout (factor kernels address
+// slots through pos / jmap / upd)
+void use_rs_layout(ClassHost &C)
+{
+    C.pos = C.rs_pos;
+    for (size_t k = 0; k < C.jmap.size(); ++k) C.jmap[k] = C.jmap_csr[k] >= 0 ? C.pos[C.jmap_csr[k]] : -1;
+    for (size_t u = 0; u < C.upd.size(); ++u) C.upd[u] = make_int2(C.pos[C.upd_csr[u].x], C.pos[C.upd_csr[u].y]);
+    C.ell_total = C.nnzb;
 }
 
 template <typename T>
@@ -1443,6 +1820,7 @@ acch_status upload_class(ClassHost &C)
     const size_t o_own = add(sizeof(int) * std::max<size_t>(1, C.own_list.size()));
     const size_t o_jml = add(sizeof(int) * C.jmap_local.size());
     const size_t o_udl = add(sizeof(int) * std::max<size_t>(1, C.upd_dl.size()));
+    const size_t o_rsm = add(C.rs_meta.size());
     ACCH_CUDA(cudaMalloc(&C.dev_mem, total));
     std::vector<unsigned char> h(total, 0);
     auto put = [&](size_t o, const void *src, size_t bytes) { if (bytes) memcpy(h.data() + o, src, bytes); };
@@ -1477,6 +1855,7 @@ acch_status upload_class(ClassHost &C)
     put(o_own, C.own_list.data(), sizeof(int) * C.own_list.size());
     put(o_jml, C.jmap_local.data(), sizeof(int) * C.jmap_local.size());
     put(o_udl, C.upd_dl.data(), sizeof(int) * C.upd_dl.size());
+    put(o_rsm, C.rs_meta.data(), C.rs_meta.size());
     ACCH_CUDA(cudaMemcpy(C.dev_mem, h.data(), total, cudaMemcpyHostToDevice));
     unsigned char *b = (unsigned char *)C.dev_mem;
     ClassDev &d = C.dev;
@@ -1520,6 +1899,16 @@ acch_status upload_class(ClassHost &C)
     d.jmap_local = (const int *)(b + o_jml);
     d.upd_dl = (const int *)(b + o_udl);
     d.rmax = C.rmax;
+    d.rs_meta = b + o_rsm;
+    d.rs_meta_bytes = (int)C.rs_meta.size();
+    d.rs_m_lenU = C.rs_m[0];
+    d.rs_m_own = C.rs_m[1];
+    d.rs_m_colL = C.rs_m[2];
+    d.rs_m_colU = C.rs_m[3];
+    d.rs_m_rel = C.rs_m[4];
+    d.rs_nL = C.rs_nL;
+    d.rs_ring = C.rs_ring;
+    d.rs_far = C.rs_far;
     d.meta_bytes = (int)C.meta.size();
     d.m_fbs = C.m_off[1];
     d.m_bptr = C.m_off[2];
@@ -1577,6 +1966,15 @@ struct acch_precond {
     TmaSmem tl{};
     int pf_depth = 2;      // levels prefetched ahead into L2 (ACCH_PREFETCH_DEPTH overrides; 2 measured best for the group solver)
     WarpSmem wl{0, 0, 0};
+    // row-sequential batched solver (apply_rs_kernel)
+    int rs_mode = 0, rs_nw = 0, rs_meta_pad = 0, rs_ring_stride = 0, slot_stride = 1, rs_pf_rows = 8;
+    size_t rs_smem = 0;
+    std::vector<int4> rs_items, rs_batches;
+    std::vector<long long> rs_batch_base;
+    int4 *d_rs_items = nullptr, *d_rs_batches = nullptr;
+    long long *d_rs_batch_base = nullptr;
+    int *d_rs_members = nullptr;
+    double2 *d_rs_scratch = nullptr;
 };
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is process-wide per kernel, so
@@ -1606,6 +2004,11 @@ static void free_precond(acch_precond *pc)
     cudaFree(pc->d_cell_src);
     cudaFree(pc->d_groups);
     cudaFree(pc->d_grp_sub);
+    cudaFree(pc->d_rs_items);
+    cudaFree(pc->d_rs_batches);
+    cudaFree(pc->d_rs_batch_base);
+    cudaFree(pc->d_rs_members);
+    cudaFree(pc->d_rs_scratch);
 }
 
 extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t overlap, const int64_t *owned_lo,
@@ -1705,17 +2108,81 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         }
         pc->sub_origin.push_back(make_int4(lo3[0], lo3[1], lo3[2], nowrap));
     }
+    // row-sequential batched solver (opt-in, ACCH_RS=1) when every class
+    // qualifies and the shared-memory image + rings of >= 2 warps fit.  At
+    // 256^3 / 8^3 boxes it measured 7.8 ms per apply against the group
+    // solver's 5.0 (profiles/r01_apply_rs.txt): 2000 dependent row steps per
+    // batch at 6 warps / SM stay latency-bound.
+    {
+        int ok = 0, ring = 0;
+        if (const char *e = getenv("ACCH_RS")) ok = atoi(e) != 0;
+        size_t meta = 0;
+        for (const auto &C : pc->classes) {
+            ok = ok && C.rs_ok;
+            ring = std::max(ring, C.rs_ring);
+            meta = std::max(meta, C.rs_meta.size());
+        }
+        const size_t limit = 227 * 1024;
+        pc->rs_meta_pad = (int)((meta + 127) / 128 * 128);
+        pc->rs_ring_stride = ring * RS_PITCH;
+        const size_t per_warp = sizeof(double2) * (size_t)pc->rs_ring_stride;
+        int nw = 8;
+        while (nw > 2 && pc->rs_meta_pad + nw * per_warp > limit) --nw;
+        if (const char *e = getenv("ACCH_RS_WARPS")) nw = std::min(nw, std::max(2, atoi(e)));
+        if (const char *e = getenv("ACCH_RS_PF")) pc->rs_pf_rows = std::max(0, atoi(e));
+        if (getenv("ACCH_DEBUG")) {
+            int nok = 0;
+            for (const auto &C : pc->classes) nok += C.rs_ok;
+            fprintf(stderr, "[acch] row-sequential: %d/%zu classes eligible, ring %d rows, meta %zu B, %d warps -> %zu B\n",
+                    nok, pc->classes.size(), ring, meta, nw, pc->rs_meta_pad + nw * per_warp);
+        }
+        ok = ok && pc->rs_meta_pad + nw * per_warp <= limit;
+        if (ok) {
+            pc->rs_mode = 1;
+            pc->rs_nw = nw;
+            // one resident CTA per SM (the scratch slot is indexed by %smid)
+            pc->rs_smem = std::max<size_t>(pc->rs_meta_pad + nw * per_warp, 116 * 1024);
+            pc->slot_stride = RS_B;
+            for (auto &C : pc->classes) use_rs_layout(C);
+        }
+    }
     // offsets
     long long vo = 0, eo = 0;
     int max_nloc = 0;
+    pc->sub_off.assign(n_sub, 0);
     for (long long s = 0; s < n_sub; ++s) {
         const ClassHost &C = pc->classes[pc->sub_class[s]];
-        pc->sub_off.push_back(vo);
+        if (!pc->rs_mode) {
+            pc->sub_off[s] = vo;
+            vo += C.ell_total;
+        }
         pc->sub_ext_off.push_back(eo);
-        vo += C.ell_total;
         eo += C.nloc;
         pc->total_nnzb += C.nnzb;
         max_nloc = std::max(max_nloc, C.nloc);
+    }
+    std::vector<int> rs_members;
+    if (pc->rs_mode) {
+        // batches of RS_B subdomains of one class; items of <= rs_nw batches of one class
+        std::vector<std::vector<int>> members(pc->classes.size());
+        for (long long s = 0; s < n_sub; ++s) members[pc->sub_class[s]].push_back((int)s);
+        for (size_t c = 0; c < members.size(); ++c) {
+            const int first_batch = (int)pc->rs_batches.size();
+            for (size_t i = 0; i < members[c].size(); i += RS_B) {
+                const int cnt = (int)std::min<size_t>(RS_B, members[c].size() - i);
+                pc->rs_batches.push_back(make_int4((int)rs_members.size(), cnt, 0, 0));
+                pc->rs_batch_base.push_back(vo);
+                for (int b = 0; b < cnt; ++b) {
+                    const int s = members[c][i + b];
+                    rs_members.push_back(s);
+                    pc->sub_off[s] = vo + b;
+                }
+                vo += (long long)RS_B * pc->classes[c].ell_total;
+            }
+            const int nb = (int)pc->rs_batches.size() - first_batch;
+            for (int k = 0; k < nb; k += pc->rs_nw)
+                pc->rs_items.push_back(make_int4((int)c, first_batch + k, std::min(pc->rs_nw, nb - k), 0));
+        }
     }
     int max_width = 0;
     for (const auto &C : pc->classes) max_width = std::max(max_width, std::max(C.max_fwidth, C.max_bwidth));
@@ -1801,6 +2268,35 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
     PC_CUDA(cudaMalloc(&pc->d_sub_ext_off, sizeof(long long) * n_sub));
     PC_CUDA(cudaMemcpy(pc->d_sub_ext_off, pc->sub_ext_off.data(), sizeof(long long) * n_sub, cudaMemcpyHostToDevice));
     PC_CUDA(cudaMalloc(&pc->d_vals, sizeof(double4) * std::max<long long>(1, pc->total_blocks)));
+    if (pc->rs_mode) {
+        PC_CUDA(cudaMalloc(&pc->d_rs_items, sizeof(int4) * pc->rs_items.size()));
+        PC_CUDA(cudaMemcpy(pc->d_rs_items, pc->rs_items.data(), sizeof(int4) * pc->rs_items.size(), cudaMemcpyHostToDevice));
+        PC_CUDA(cudaMalloc(&pc->d_rs_batches, sizeof(int4) * pc->rs_batches.size()));
+        PC_CUDA(cudaMemcpy(pc->d_rs_batches, pc->rs_batches.data(), sizeof(int4) * pc->rs_batches.size(),
+                           cudaMemcpyHostToDevice));
+        PC_CUDA(cudaMalloc(&pc->d_rs_batch_base, sizeof(long long) * pc->rs_batch_base.size()));
+        PC_CUDA(cudaMemcpy(pc->d_rs_batch_base, pc->rs_batch_base.data(), sizeof(long long) * pc->rs_batch_base.size(),
+                           cudaMemcpyHostToDevice));
+        PC_CUDA(cudaMalloc(&pc->d_rs_members, sizeof(int) * rs_members.size()));
+        PC_CUDA(cudaMemcpy(pc->d_rs_members, rs_members.data(), sizeof(int) * rs_members.size(), cudaMemcpyHostToDevice));
+        // forward-sweep scratch: one slot per (SM id, warp); SM ids may exceed the SM count
+        int dev = 0, nsm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        const size_t slots = (size_t)std::max(256, 2 * nsm) * pc->rs_nw;
+        PC_CUDA(cudaMalloc(&pc->d_rs_scratch, sizeof(double2) * slots * (size_t)max_nloc * RS_B));
+        const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        const int optin = smem_optin();
+#define RS_ATTR(NW)                                                        \
+        PC_CUDA(cudaFuncSetAttribute(apply_rs_kernel<0, NW>, attr, optin)); \
+        PC_CUDA(cudaFuncSetAttribute(apply_rs_kernel<1, NW>, attr, optin)); \
+        PC_CUDA(cudaFuncSetAttribute(apply_rs_kernel<2, NW>, attr, optin));
+        RS_ATTR(2) RS_ATTR(3) RS_ATTR(4) RS_ATTR(5) RS_ATTR(6) RS_ATTR(7) RS_ATTR(8)
+#undef RS_ATTR
+        if (getenv("ACCH_DEBUG"))
+            fprintf(stderr, "[acch] row-sequential solver: %zu batches, %zu items, %d warps/CTA, smem %zu B\n",
+                    pc->rs_batches.size(), pc->rs_items.size(), pc->rs_nw, pc->rs_smem);
+    }
     PC_CUDA(cudaMalloc(&pc->d_bad, sizeof(int) * n_sub));
     const bool need_ext = variant != 1 || !pc->use_smem;
     if (need_ext) PC_CUDA(cudaMalloc(&pc->d_ext_out, sizeof(double2) * std::max<long long>(1, pc->total_ext)));
@@ -1897,7 +2393,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         for (const auto &C : pc->classes) meta_max = std::max(meta_max, (int)C.meta.size());
         pc->meta_max = (meta_max + 15) / 16 * 16;
         pc->y_stride = (int)((sizeof(double2) * (size_t)max_nloc + 15) / 16 * 16);
-        int enable = pc->warp_mode && !pc->tma_mode;
+        int enable = pc->warp_mode && !pc->tma_mode && !pc->rs_mode;
         if (const char *e = getenv("ACCH_GROUP")) enable = enable && atoi(e) != 0;
         int nw = 8;
         if (const char *e = getenv("ACCH_GROUP_WARPS")) nw = atoi(e) <= 4 ? 4 : 8;
@@ -2006,18 +2502,20 @@ extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef,
         const size_t sm = (size_t)NW * 32 * pc->factor_rstride * sizeof(double4);
         if (pc->dim == 3)
             factor_warp_kernel<3, NW><<<nb, NW * 32, sm, ctx->stream>>>(ctx->g, ctx->p, dt, coef, pc->d_classes,
-                pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, pc->d_bad, pc->nsub, pc->factor_rstride);
+                pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, pc->d_bad, pc->nsub, pc->factor_rstride,
+                pc->slot_stride);
         else
             factor_warp_kernel<2, NW><<<nb, NW * 32, sm, ctx->stream>>>(ctx->g, ctx->p, dt, coef, pc->d_classes,
-                pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, pc->d_bad, pc->nsub, pc->factor_rstride);
+                pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, pc->d_bad, pc->nsub, pc->factor_rstride,
+                pc->slot_stride);
     } else if (pc->dim == 3) {
         factor_kernel<3><<<(unsigned)pc->nsub, kFactorThreads, 0, ctx->stream>>>(
             ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals,
-            pc->d_bad);
+            pc->d_bad, pc->slot_stride);
     } else {
         factor_kernel<2><<<(unsigned)pc->nsub, kFactorThreads, 0, ctx->stream>>>(
             ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals,
-            pc->d_bad);
+            pc->d_bad, pc->slot_stride);
     }
     ACCH_LAUNCHED(ctx);
     std::vector<int> bad(pc->nsub);
@@ -2094,7 +2592,28 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     apply_tma_kernel<V><<<(unsigned)pc->nsub, 32, pc->tl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,             \
         pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
         (double2 *)z, pc->d_ext_out, pc->tl, pc->nsub)
-    if (pc->group_mode) {
+#define RSAPPLY_W(V, NW)                                                                                        \
+    apply_rs_kernel<V, NW><<<(unsigned)pc->rs_items.size(), NW * 32, pc->rs_smem, ctx->stream>>>(ctx->g, pc->d_classes, \
+        pc->d_rs_items, pc->d_rs_batches, pc->d_rs_batch_base, pc->d_rs_members, pc->d_sub_origin, pc->d_sub_ext_off,  \
+        pc->d_vals, (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->d_rs_scratch, pc->rs_meta_pad,              \
+        pc->rs_ring_stride, pc->max_nloc, pc->rs_pf_rows)
+#define RSAPPLY(V)                                 \
+    do {                                           \
+        switch (pc->rs_nw) {                       \
+        case 2: RSAPPLY_W(V, 2); break;            \
+        case 3: RSAPPLY_W(V, 3); break;            \
+        case 4: RSAPPLY_W(V, 4); break;            \
+        case 5: RSAPPLY_W(V, 5); break;            \
+        case 6: RSAPPLY_W(V, 6); break;            \
+        case 7: RSAPPLY_W(V, 7); break;            \
+        default: RSAPPLY_W(V, 8); break;           \
+        }                                          \
+    } while (0)
+    if (pc->rs_mode) {
+        if (pc->variant == 1) RSAPPLY(1);
+        else if (pc->variant == 0) RSAPPLY(0);
+        else RSAPPLY(2);
+    } else if (pc->group_mode) {
         if (pc->variant == 1) GAPPLY(1);
         else if (pc->variant == 0) GAPPLY(0);
         else GAPPLY(2);
@@ -2116,6 +2635,8 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         else APPLY(2, 128);
     }
 #undef APPLY
+#undef RSAPPLY
+#undef RSAPPLY_W
 #undef WAPPLY
 #undef WAPPLY_D
 #undef GAPPLY

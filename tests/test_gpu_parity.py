@@ -351,6 +351,35 @@ def test_group_solver_interior_boxes_bitwise_equal_warp_solver(variant, monkeypa
     assert np.max(np.abs(outs["1"] - ref)) <= 1e-10 * np.max(np.abs(ref))
 
 
+@pytest.mark.parametrize("variant", [SchwarzVariant.LEFT_RAS, SchwarzVariant.RIGHT_RAS, SchwarzVariant.CLASSICAL])
+@pytest.mark.parametrize("bc", [BoundaryCondition.PERIODIC, BoundaryCondition.NEUMANN])
+def test_row_sequential_solver_matches_oracle(variant, bc, monkeypatch):
+    """The opt-in row-sequential batched solver (ACCH_RS=1; factor slots in
+    row order, 8 subdomains per warp, ring + scratch for the solution) on a
+    grid whose periodic boxes wrap in z (far columns through the scratch),
+    with partial batches, against the oracle, and the factorisation in its
+    strided layout."""
+    from oracle import acch_oracle as O
+    monkeypatch.setenv("ACCH_RS", "1")
+    rng = np.random.default_rng(13)
+    counts = (20, 20, 20)
+    g = Grid(counts, (1.0, 1.0, 1.0), bc)
+    uo, vo = 0.5 + rng.uniform(-0.05, 0.05, g.array_shape), rng.uniform(-0.05, 0.05, g.array_shape)
+    un, vn = uo + rng.uniform(-0.01, 0.01, g.array_shape), vo + rng.uniform(-0.01, 0.01, g.array_shape)
+    prob = StepProblem.create(g, PARAMS, st(g, uo, vo), 1e-3)
+    J = assemble_jacobian(prob, st(g, un, vn))
+    r = rng.standard_normal(2 * g.n_cells)
+    pre = SchwarzPreconditioner(partition(g, 125, 1), variant, SubdomainSolverSpec.from_string("ilu0"))
+    pre.update(J)
+    out = host(pre.apply(torch.tensor(r, device=DEV)))
+    m = O.Mesh(counts, (1.0, 1.0, 1.0), bc == BoundaryCondition.PERIODIC)
+    Jo = O.Step(m, O.Coeffs(), uo, vo, 1e-3).jacobian(O.pack(un, vn)).assemble_fast()
+    po = O.SchwarzOracle(O.decompose(m, 125, 1), variant.value, "ilu0")
+    po.update(Jo)
+    ref = po.apply(r)
+    assert np.max(np.abs(out - ref)) <= 1e-10 * np.max(np.abs(ref))
+
+
 @pytest.mark.parametrize("solver", ["ilu0", "ilu1", "lu"])
 @pytest.mark.parametrize("bc", [BoundaryCondition.PERIODIC, BoundaryCondition.NEUMANN])
 def test_warp_factorisation_bitwise_equal_cta_factorisation(solver, bc, monkeypatch):
