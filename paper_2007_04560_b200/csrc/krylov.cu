@@ -108,8 +108,10 @@ __host__ __device__ __forceinline__ int gslot(int s) { return (s / MG) * (MG + 1
 template <int NS>
 __global__ void __launch_bounds__(kRedThreads)
 mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ h, double *__restrict__ w,
-               long long n, double *partials, unsigned int *counter, double *result, int h_grouped, int zero)
+               long long n, double *partials, unsigned int *counter, double *result, int h_grouped, double div)
 {
+    // w <- (w - V h) / div when div != 0 (the Arnoldi normalisation fused
+    // into the last update pass), else w <- w - V h
     __shared__ double sh[NS];
     if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? h[h_grouped ? gslot(threadIdx.x) : threadIdx.x] : 0.0;
     __syncthreads();
@@ -127,6 +129,10 @@ mupdate_kernel(const double *__restrict__ V, long long ld, int m, const double *
                 wi.x -= sh[s] * v.x;
                 wi.y -= sh[s] * v.y;
             }
+        if (div != 0.0) {
+            wi.x /= div;
+            wi.y /= div;
+        }
         w2[i] = wi;
         acc += wi.x * wi.x + wi.y * wi.y;
     }
@@ -361,13 +367,13 @@ static acch_status mdot_to(acch_ctx *ctx, const double *V, long long ld, int m, 
 }
 
 static acch_status mupdate_to(acch_ctx *ctx, const double *V, long long ld, int m, const double *h, double *w,
-                              long long n, double *out, int h_grouped = 1)
+                              long long n, double *out, int h_grouped = 1, double div = 0.0)
 {
     ProfScope prof_scope(ctx, PC_KUPDATE, 8.0 * (m + 2) * n);
     const int G = rgrid(n);
 #define MUP_CASE(NS) \
     mupdate_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, m, h, w, n, ctx->d_partials, ctx->d_counter, out, \
-                                                           h_grouped, 0);
+                                                           h_grouped, div);
     if (m <= 4) { MUP_CASE(4) }
     else if (m <= 8) { MUP_CASE(8) }
     else if (m <= 16) { MUP_CASE(16) }
@@ -551,6 +557,7 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
             double *w = col(j + 1);
             TRY(matvec(zj, w));
             double norm_before, norm_after;
+            bool normalised = false;   // w already divided by norm_after
             if (ortho == 1) {
                 // pass 1: h1 = V^T w (+ ||w||^2); w -= V h1 fused with the
                 // second pass's projections h2 = V^T w (+ ||w||^2), which are
@@ -570,12 +577,27 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                 norm_before = sqrt(tmp[ns - 1]);
                 norm_after = sqrt(tmp[64]);
                 if (norm_after < 0.5 * norm_before) {
-                    TRY(mupdate_to(ctx, V + off, nv, m, d2 + 1, w + off, ni, dh + 40, 0));
-                    double t40;
-                    if (multi) TRY(reduce_dots(&t40, dh + 40, 1, false));
-                    else TRY(fetch(ctx, &t40, dh + 40, 1));
+                    // second pass.  ||w - V h2||^2 = ||w||^2 - ||h2||^2 (h2 are the
+                    // projections of w on the orthonormal basis; no cancellation:
+                    // ||h2|| is at rounding level), so the pass can write the
+                    // normalised vector directly -- one sweep fewer than update +
+                    // norm + scale.  (If the identity is not usable, the norm is
+                    // measured as before.)
+                    double hh = 0.0;
+                    for (int i = 0; i <= j; ++i) hh += tmp[65 + i] * tmp[65 + i];
+                    const double n2 = tmp[64] - hh;
                     for (int i = 0; i <= j; ++i) h(i, j) += tmp[65 + i];
-                    norm_after = sqrt(t40);
+                    if (n2 > 0.0 && hh <= 1e-6 * tmp[64]) {
+                        norm_after = sqrt(n2);
+                        TRY(mupdate_to(ctx, V + off, nv, m, d2 + 1, w + off, ni, dh + 40, 0, norm_after));
+                        normalised = true;
+                    } else {
+                        TRY(mupdate_to(ctx, V + off, nv, m, d2 + 1, w + off, ni, dh + 40, 0));
+                        double t40;
+                        if (multi) TRY(reduce_dots(&t40, dh + 40, 1, false));
+                        else TRY(fetch(ctx, &t40, dh + 40, 1));
+                        norm_after = sqrt(t40);
+                    }
                 }
             } else {
                 TRY(dot_to(ctx, w + off, w + off, ni, dh + 40));
@@ -626,7 +648,7 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                 breakdown = true;
                 break;
             }
-            TRY(scale_by(ctx, norm_after, w, w, nv));
+            if (!normalised) TRY(scale_by(ctx, norm_after, w, w, nv));
             if (fabs(gv[j]) <= tol) break;
         }
         if (j > 0) {
