@@ -68,6 +68,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // two logs of ln z - ln(1-z) merged into one log of z/(1-z), reciprocals
 // shared between the log argument and the series ratios, and FMA Horner.
 // Agrees with the reference formula to a few ulps of the O(1) terms.
+// ORDER > 0: the series order as a compile-time constant (fully unrolled
+// Horner on constant coefficients 1/((2s+1)2s), correctly rounded exactly as
+// the host computes them); ORDER = 0: P.order at run time.
+template <int ORDER>
 __device__ __forceinline__ double chord_fast(double a, double b, const ParamsDev &P)
 {
     const double zeta = 0.5 * (a + b);
@@ -75,13 +79,28 @@ __device__ __forceinline__ double chord_fast(double a, double b, const ParamsDev
     const double w = 1.0 - zeta;
     if (sigma == 0.0) return log(zeta / w);
     if (fabs(sigma) <= 0.4 * fmin(zeta, w)) {
-        const double iz = 1.0 / zeta, iw = 1.0 / w;
+        const double r = 1.0 / (zeta * w);            // one reciprocal for 1/zeta and 1/w
+        const double iz = w * r, iw = zeta * r;
         const double rz = sigma * iz, rw = sigma * iw;
         const double tz = rz * rz, tw = rw * rw;
-        double pz = P.c1[P.order - 1], pw = P.c1[P.order - 1];
-        for (int s = P.order - 2; s >= 0; --s) {
-            pz = fma(pz, tz, P.c1[s]);
-            pw = fma(pw, tw, P.c1[s]);
+        double pz, pw;
+        if (ORDER > 0) {
+            constexpr double cl = 1.0 / ((2.0 * ORDER + 1.0) * 2.0 * ORDER);
+            pz = cl;
+            pw = cl;
+#pragma unroll
+            for (int s = ORDER - 1; s >= 1; --s) {
+                const double c = 1.0 / ((2.0 * s + 1.0) * 2.0 * s);
+                pz = fma(pz, tz, c);
+                pw = fma(pw, tw, c);
+            }
+        } else {
+            pz = P.c1[P.order - 1];
+            pw = P.c1[P.order - 1];
+            for (int s = P.order - 2; s >= 0; --s) {
+                pz = fma(pz, tz, P.c1[s]);
+                pw = fma(pw, tw, P.c1[s]);
+            }
         }
         return log(zeta * iw) - pz * tz + pw * tw;
     }
@@ -154,8 +173,8 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
                 luo += (ozp.x - 2.0 * o0.x + ozm.x) * ihz;
                 lvo += (ozp.y - 2.0 * o0.y + ozm.y) * ihz;
             }
-            const double phi = chord_fast(n0.x + n0.y, o0.x + o0.y, P);
-            const double psi = chord_fast(n0.x - n0.y, o0.x - o0.y, P);
+            const double phi = chord_fast<0>(n0.x + n0.y, o0.x + o0.y, P);
+            const double psi = chord_fast<0>(n0.x - n0.y, o0.x - o0.y, P);
             const int idx = s0 * GX * GY + i;
             sGu[idx] = -0.5 * P.alpha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) - 0.5 * P.gamma * (lun + luo);
             sGv[idx] = -0.5 * P.beta * (n0.y + o0.y) + P.theta * (phi - psi) - 0.5 * P.gamma * (lvn + lvo);
@@ -236,6 +255,238 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
             if (k + 3 <= ze + 1) load_plane(k + 3);
             if (active) output(k, n0, o0);
         }
+    }
+    double v[2] = {acc_norm, acc_gap};
+    const int ops[2] = {RED_SUM, RED_MIN};
+    reduce_finish<2>(v, ops, partials, counter, result);
+}
+
+// ---------------------------------------------------------------------------
+// z-marching residual, one barrier per plane (3D default) -- the matvec's
+// pipeline (mv_zm_kernel below) with the discrete variational derivative:
+//   * both states U', U^n: 4-slot smem rings of tile+2 planes, cp.async two
+//     planes ahead;
+//   * every tile+1 column (centre columns one per thread + the ring columns
+//     of the first threads) evaluates G_u, G_v, cbar once per plane
+//     (scheme.py:270-287, entropy chords included) into a 3-slot smem ring
+//     B = (G_u, cbar); the centre keeps G_v and its states in registers;
+//   * the z-neighbours of a column's states stay in the owning thread's
+//     registers; all offsets are computed once.
+// ||F||^2 and the admissibility gap are fused (deterministic grid reduction).
+// ---------------------------------------------------------------------------
+
+template <int TX, int TY>
+struct RzmSmem {
+    static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2;
+    static constexpr int NW = HX * HY, NB = GX * GY, NRING = 2 * GX + 2 * TY;
+    static constexpr size_t bytes = sizeof(double2) * (2 * 4 * NW + 3 * NB);
+};
+
+template <int TX, int TY, int MINB, bool PER, bool RW, int ORDER>
+__global__ void __launch_bounds__(TX *TY + (RW ? 32 * ((2 * TX + 4 * TY + 4 + 31) / 32) : 0), MINB)
+res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__restrict__ xo_g,
+              const double2 *__restrict__ xn_g, double2 *__restrict__ F, double *partials, unsigned int *counter,
+              double *result, int nchunk)
+{
+    using L = RzmSmem<TX, TY>;
+    constexpr int HX = L::HX, GX = L::GX, NW = L::NW, NB = L::NB, NRING = L::NRING, NT = TX * TY;
+    // RW: the ring columns get their own warps (every thread owns one column,
+    // the centre warps also emit the outputs), else the first NRING centre
+    // threads own a ring column too
+    constexpr int NTA = NT + (RW ? 32 * ((NRING + 31) / 32) : 0);
+    constexpr int NWR = (NW + NTA - 1) / NTA;
+    static_assert(NRING <= NT, "ring columns must fit one per thread");
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    double2 *sN = reinterpret_cast<double2 *>(smem_raw);   // [4][NW]   U'
+    double2 *sO = sN + 4 * NW;                               // [4][NW]   U^n
+    double2 *sB = sO + 4 * NW;                               // [3][NB]   (G_u, cbar)
+
+    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+    const bool centre = !RW || tid < NT;
+    const int tx = tid % TX, ty = centre ? tid / TX : 0;
+    const int nx = g.nx, ny = g.ny;
+    const long long nxy = (long long)nx * ny;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int zb = (int)(((long long)blockIdx.z * g.nz) / nchunk);
+    const int ze = (int)(((long long)(blockIdx.z + 1) * g.nz) / nchunk);
+    const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
+
+    int woff[NWR];
+#pragma unroll
+    for (int r = 0; r < NWR; ++r) {
+        const int i = tid + r * NTA;
+        const int hx = i % HX, hy = i / HX;
+        woff[r] = (i < NW) ? wrap_coord(y0 + hy - 2, ny, g.periodic) * nx + wrap_coord(x0 + hx - 2, nx, g.periodic) : 0;
+    }
+    const bool has_ring = !RW && tid < NRING;
+    int cx[2], cy[2];
+    cx[0] = tx;
+    cy[0] = ty;
+    {
+        int r = has_ring ? tid : 0;
+        if (RW && !centre) r = min(tid - NT, NRING - 1);   // spare lanes repeat the last ring column
+        if (r < GX) { cx[1] = r - 1; cy[1] = -1; }
+        else if (r < 2 * GX) { cx[1] = r - GX - 1; cy[1] = TY; }
+        else if (r < 2 * GX + TY) { cx[1] = -1; cy[1] = r - 2 * GX; }
+        else { cx[1] = TX; cy[1] = r - 2 * GX - TY; }
+        if (RW && !centre) {
+            cx[0] = cx[1];
+            cy[0] = cy[1];
+        }
+    }
+    int hc[2], gc[2], coff[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        hc[j] = (cy[j] + 2) * HX + (cx[j] + 2);
+        gc[j] = (cy[j] + 1) * GX + (cx[j] + 1);
+        coff[j] = wrap_coord(y0 + cy[j], ny, g.periodic) * nx + wrap_coord(x0 + cx[j], nx, g.periodic);
+    }
+    const int x = x0 + tx, y = y0 + ty;
+    const bool active = centre && x < nx && y < ny;
+    const bool fxl = PER || x > 0, fxh = PER || x < nx - 1, fyl = PER || y > 0, fyh = PER || y < ny - 1;
+    const int jn = has_ring ? 2 : 1;
+
+    auto load_x = [&](long long poff, int slot) {
+        const double2 *srcn = xn_g + poff, *srco = xo_g + poff;
+        double2 *dn = sN + slot * NW + tid, *dO = sO + slot * NW + tid;
+#pragma unroll
+        for (int r = 0; r < NWR; ++r)
+            if (r < NWR - 1 || tid + r * NTA < NW) {
+                cp_async16(dn + r * NTA, srcn + woff[r]);
+                cp_async16(dO + r * NTA, srco + woff[r]);
+            }
+    };
+
+    double2 nz[2], oz[2];                     // column states at the plane below the one being built
+    double2 nk = make_double2(0.0, 0.0), ok_ = nk, nk1 = nk, ok1 = nk;   // centre states, planes k, k+1
+    double gvk = 0.0, gvk1 = 0.0;             // centre G_v, planes k, k+1
+
+    // B(kk) from X(kk) (slot s1) and X(kk+1) (slot s2); nz/oz = states at kk-1
+    auto build = [&](int s1, int s2, int sb) {
+        const double2 *N1 = sN + s1 * NW, *O1 = sO + s1 * NW, *N2 = sN + s2 * NW, *O2 = sO + s2 * NW;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (j < jn) {
+                const int h = hc[j];
+                const double2 n0 = N1[h], o0 = O1[h];
+                const double2 nxm = N1[h - 1], nxp = N1[h + 1], nym = N1[h - HX], nyp = N1[h + HX];
+                const double2 oxm = O1[h - 1], oxp = O1[h + 1], oym = O1[h - HX], oyp = O1[h + HX];
+                const double2 nzp = N2[h], ozp = O2[h];
+                // Laplacians, axes summed x, y, z (grid.py:263-271)
+                double lun = (nxp.x - 2.0 * n0.x + nxm.x) * ihx;
+                double lvn = (nxp.y - 2.0 * n0.y + nxm.y) * ihx;
+                double luo = (oxp.x - 2.0 * o0.x + oxm.x) * ihx;
+                double lvo = (oxp.y - 2.0 * o0.y + oxm.y) * ihx;
+                lun += (nyp.x - 2.0 * n0.x + nym.x) * ihy;
+                lvn += (nyp.y - 2.0 * n0.y + nym.y) * ihy;
+                luo += (oyp.x - 2.0 * o0.x + oym.x) * ihy;
+                lvo += (oyp.y - 2.0 * o0.y + oym.y) * ihy;
+                lun += (nzp.x - 2.0 * n0.x + nz[j].x) * ihz;
+                lvn += (nzp.y - 2.0 * n0.y + nz[j].y) * ihz;
+                luo += (ozp.x - 2.0 * o0.x + oz[j].x) * ihz;
+                lvo += (ozp.y - 2.0 * o0.y + oz[j].y) * ihz;
+                const double phi = chord_fast<ORDER>(n0.x + n0.y, o0.x + o0.y, P);
+                const double psi = chord_fast<ORDER>(n0.x - n0.y, o0.x - o0.y, P);
+                const double Gu = -0.5 * P.alpha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) - 0.5 * P.gamma * (lun + luo);
+                const double cb = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
+                sB[sb * NB + gc[j]] = make_double2(Gu, cb);
+                nz[j] = n0;
+                oz[j] = o0;
+                if (j == 0) {
+                    gvk1 = -0.5 * P.beta * (n0.y + o0.y) + P.theta * (phi - psi) - 0.5 * P.gamma * (lvn + lvo);
+                    nk1 = n0;
+                    ok1 = o0;
+                }
+            }
+        }
+    };
+
+    int z0 = zplane_near(g, zb), z1 = zplane_near(g, zb + 1), z2 = zplane_near(g, zb + 2), z3 = zplane_near(g, zb + 3);
+    auto poff = [&](int zs) { return (long long)zs * nxy; };
+    {
+        const long long pm2 = zplane_near(g, zb - 2) * nxy, pm1 = zplane_near(g, zb - 1) * nxy;
+#pragma unroll
+        for (int j = 0; j < 2; ++j)
+            if (j < jn) {
+                nz[j] = __ldg(xn_g + pm2 + coff[j]);
+                oz[j] = __ldg(xo_g + pm2 + coff[j]);
+            }
+        load_x(pm1, 0);
+        load_x(poff(z0), 1);
+        cp_async_commit();
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    load_x(poff(z1), 2);
+    cp_async_commit();
+    load_x(poff(z2), 3);
+    cp_async_commit();
+    build(0, 1, 0);              // B(zb-1)
+    cp_async_wait_group<1>();
+    __syncthreads();
+    load_x(poff(z3), 0);
+    cp_async_commit();
+    build(1, 2, 1);              // B(zb)
+    nk = nk1;
+    ok_ = ok1;
+    gvk = gvk1;
+    double acc_norm = 0.0, acc_gap = INFINITY;
+    int sw1 = 2, sw2 = 3, sw3 = 0;
+    int sb0 = 0, sb1 = 1, sb2 = 2;
+    int z4 = zplane_near(g, zb + 4);
+    for (int k = zb; k < ze; ++k) {
+        cp_async_wait_group<1>();
+        __syncthreads();
+        const int swf = 6 - sw1 - sw2 - sw3;
+        if (k + 4 <= ze + 1) load_x(poff(z4), swf);
+        cp_async_commit();
+        build(sw1, sw2, sb2);    // B(k+1)
+        if (active) {
+            const double2 *B = sB + sb1 * NB;
+            const int c0 = gc[0];
+            const double2 b0 = B[c0];
+            const double G0 = b0.x, C0 = b0.y;
+            double div = 0.0;
+            {
+                const double2 bp = B[c0 + 1], bm = B[c0 - 1];
+                const double fp = fxh ? 0.5 * (C0 + bp.y) * (bp.x - G0) : 0.0;
+                const double fm = fxl ? 0.5 * (C0 + bm.y) * (G0 - bm.x) : 0.0;
+                div += (fp - fm) * ihx;
+            }
+            {
+                const double2 bp = B[c0 + GX], bm = B[c0 - GX];
+                const double fp = fyh ? 0.5 * (C0 + bp.y) * (bp.x - G0) : 0.0;
+                const double fm = fyl ? 0.5 * (C0 + bm.y) * (G0 - bm.x) : 0.0;
+                div += (fp - fm) * ihy;
+            }
+            {
+                const double2 bp = sB[sb2 * NB + c0], bm = sB[sb0 * NB + c0];
+                const double fp = (PER || zstep_ok(g, k, +1)) ? 0.5 * (C0 + bp.y) * (bp.x - G0) : 0.0;
+                const double fm = (PER || zstep_ok(g, k, -1)) ? 0.5 * (C0 + bm.y) * (G0 - bm.x) : 0.0;
+                div += (fp - fm) * ihz;
+            }
+            double2 f;
+            f.x = (nk.x - ok_.x) / dt - div;
+            f.y = (nk.y - ok_.y) / dt + (C0 / P.rho) * gvk;
+            F[poff(z0) + coff[0]] = f;
+            acc_norm += f.x * f.x + f.y * f.y;
+            acc_gap = red_combine(acc_gap, cell_gap(nk.x, nk.y), RED_MIN);
+        }
+        nk = nk1;
+        ok_ = ok1;
+        gvk = gvk1;
+        sw1 = sw2;
+        sw2 = sw3;
+        sw3 = swf;
+        const int tb = sb0;
+        sb0 = sb1;
+        sb1 = sb2;
+        sb2 = tb;
+        z0 = z1;
+        z1 = z2;
+        z2 = z3;
+        z3 = z4;
+        z4 = zplane_near(g, k + 5);
     }
     double v[2] = {acc_norm, acc_gap};
     const int ops[2] = {RED_SUM, RED_MIN};
@@ -541,21 +792,27 @@ struct MvConst {
     double idt, irho;        // 1/dt, 1/rho
 };
 
-template <int TX, int TY, int MINB, bool PER>
-__global__ void __launch_bounds__(TX *TY, MINB)
+template <int TX, int TY, int MINB, bool PER, bool RW>
+__global__ void __launch_bounds__(TX *TY + (RW ? 32 * ((2 * TX + 4 * TY + 4 + 31) / 32) : 0), MINB)
 mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g, double2 *__restrict__ yout,
              int nchunk)
 {
     using L = ZmSmem<TX, TY>;
     constexpr int HX = L::HX, GX = L::GX, NW = L::NW, NB = L::NB, NRING = L::NRING, NT = TX * TY;
-    constexpr int NWR = (NW + NT - 1) / NT;
+    // RW: the ring columns get their own warps (every thread owns one column,
+    // the centre warps also emit the outputs), else the first NRING centre
+    // threads own a ring column too
+    constexpr int NTA = NT + (RW ? 32 * ((NRING + 31) / 32) : 0);
+    constexpr int NWR = (NW + NTA - 1) / NTA;
     static_assert(NRING <= NT, "ring columns must fit one per thread");
     extern __shared__ __align__(16) unsigned char smem_raw[];
     double2 *sW = reinterpret_cast<double2 *>(smem_raw);      // [4][NW]   w
     double2 *sB1 = sW + 4 * NW;                                  // [3][NB]   (dG_u, cbar)
     double2 *sB2 = sB1 + 3 * NB;                                 // [3][NB]   (eta, G_u)
 
-    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+    const bool centre = !RW || tid < NT;
+    const int tx = tid % TX, ty = centre ? tid / TX : 0;
     const int nx = g.nx, ny = g.ny;
     const long long nxy = (long long)nx * ny;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
@@ -575,7 +832,7 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
     int woff[NWR];
 #pragma unroll
     for (int r = 0; r < NWR; ++r) {
-        const int i = tid + r * NT;
+        const int i = tid + r * NTA;
         const int hx = i % HX, hy = i / HX;
         woff[r] = (i < NW) ? wrap_coord(y0 + hy - 2, ny, g.periodic) * nx + wrap_coord(x0 + hx - 2, nx, g.periodic) : 0;
     }
@@ -591,6 +848,10 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
         else if (r < 2 * GX) { cx[1] = r - GX - 1; cy[1] = TY; }
         else if (r < 2 * GX + TY) { cx[1] = -1; cy[1] = r - 2 * GX; }
         else { cx[1] = TX; cy[1] = r - 2 * GX - TY; }
+        if (RW && !centre) {
+            cx[0] = cx[1];
+            cy[0] = cy[1];
+        }
     }
     int hc[2], gc[2], coff[2];
 #pragma unroll
@@ -600,7 +861,7 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
         coff[j] = wrap_coord(y0 + cy[j], ny, g.periodic) * nx + wrap_coord(x0 + cx[j], nx, g.periodic);
     }
     const int x = x0 + tx, y = y0 + ty;
-    const bool active = x < nx && y < ny;
+    const bool active = centre && x < nx && y < ny;
     const bool fxl = PER || x > 0, fxh = PER || x < nx - 1, fyl = PER || y > 0, fyh = PER || y < ny - 1;
     const int jn = has_ring ? 2 : 1;
 
@@ -610,7 +871,7 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
         double2 *dst = sW + slot * NW + tid;
 #pragma unroll
         for (int r = 0; r < NWR; ++r)
-            if (r < NWR - 1 || tid + r * NT < NW) cp_async16(dst + r * NT, src + woff[r]);
+            if (r < NWR - 1 || tid + r * NTA < NW) cp_async16(dst + r * NTA, src + woff[r]);
     };
 
     double cS[2], cD[2], cU[2], cV[2], cC[2], cG[2];
@@ -1046,10 +1307,68 @@ int stencil_offsets(int dim, int (*off)[3])
     return n;
 }
 
+// z chunks for a z-marching kernel: minimise waves x (planes per chunk + the
+// pipeline start-up), given the resident CTAs per SM of the kernel
+static int choose_zchunks(int tiles, int nz, int per_sm, int sms, double startup)
+{
+    const long long slots = (long long)per_sm * sms;
+    int best = 1;
+    double best_cost = 1e300;
+    // chunks of at least 2 planes (the start-up reads planes up to zb + 3)
+    for (int c = 1; c <= (nz >= 4 ? nz / 2 : 1); ++c) {
+        const long long items = (long long)tiles * c;
+        const long long waves = (items + slots - 1) / slots;
+        const double cost = (double)waves * ((double)nz / c + startup);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = c;
+        }
+    }
+    return best;
+}
+
+template <int MINB, bool PER, bool RW, int ORDER>
+static acch_status launch_residual_zm_t(acch_ctx *ctx, const double *x_old, double dt, const double *x, double *F)
+{
+    constexpr int TX = 32, TY = 8;
+    using L = RzmSmem<TX, TY>;
+    constexpr int NTA = TX * TY + (RW ? 32 * ((L::NRING + 31) / 32) : 0);
+    auto kern = res_zm_kernel<TX, TY, MINB, PER, RW, ORDER>;
+    static int per_sm = 0, sms = 0;
+    if (!per_sm) {
+        acch_status st = set_smem(kern, L::bytes);
+        if (st != ACCH_OK) return st;
+        ACCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTA, L::bytes));
+        ACCH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
+        if (per_sm < 1) per_sm = 1;
+    }
+    const GridDev &g = ctx->g;
+    const int gx = (g.nx + TX - 1) / TX, gy = (g.ny + TY - 1) / TY;
+    const int nchunk = choose_zchunks(gx * gy, g.nz, per_sm, sms, 3.0);
+    kern<<<dim3(gx, gy, nchunk), dim3(NTA), L::bytes, ctx->stream>>>(
+        g, ctx->p, dt, (const double2 *)x_old, (const double2 *)x, (double2 *)F, ctx->d_partials, ctx->d_counter,
+        ctx->d_result, nchunk);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
 acch_status launch_residual(acch_ctx *ctx, const double *x_old, double dt, const double *x, double *F)
 {
     ProfScope prof_scope(ctx, PC_RESIDUAL, 48.0 * ctx->g.n);
     const GridDev &g = ctx->g;
+    // ACCH_RESIDUAL=ring selects the older 2-barrier kernel (tests compare both)
+    const char *mode = getenv("ACCH_RESIDUAL");
+    const bool zm = g.dim == 3 && g.nz >= 3 && !(mode && strcmp(mode, "ring") == 0);
+    if (zm) {
+        // ring warps (every thread one column, measured fastest); the
+        // reference's default series order 10 compiled in
+        if (ctx->p.order == 10) {
+            if (g.periodic) return launch_residual_zm_t<2, true, true, 10>(ctx, x_old, dt, x, F);
+            return launch_residual_zm_t<2, false, true, 10>(ctx, x_old, dt, x, F);
+        }
+        if (g.periodic) return launch_residual_zm_t<2, true, true, 0>(ctx, x_old, dt, x, F);
+        return launch_residual_zm_t<2, false, true, 0>(ctx, x_old, dt, x, F);
+    }
     const dim3 block(RTX, RTY);
     if (g.dim == 3) {
         using L = ResidualSmem<3, RTX, RTY>;
@@ -1109,37 +1428,18 @@ static acch_status launch_matvec_twopass(acch_ctx *ctx, const double *coef, doub
     return ACCH_OK;
 }
 
-// z chunks for a z-marching kernel: minimise waves x (planes per chunk + the
-// pipeline start-up), given the resident CTAs per SM of the kernel
-static int choose_zchunks(int tiles, int nz, int per_sm, int sms, double startup)
-{
-    const long long slots = (long long)per_sm * sms;
-    int best = 1;
-    double best_cost = 1e300;
-    // chunks of at least 2 planes (the start-up reads planes up to zb + 3)
-    for (int c = 1; c <= (nz >= 4 ? nz / 2 : 1); ++c) {
-        const long long items = (long long)tiles * c;
-        const long long waves = (items + slots - 1) / slots;
-        const double cost = (double)waves * ((double)nz / c + startup);
-        if (cost < best_cost - 1e-9) {
-            best_cost = cost;
-            best = c;
-        }
-    }
-    return best;
-}
-
-template <int MINB, bool PER>
+template <int MINB, bool PER, bool RW>
 static acch_status launch_matvec_zm_t(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
     constexpr int TX = 32, TY = 8;
     using L = ZmSmem<TX, TY>;
-    auto kern = mv_zm_kernel<TX, TY, MINB, PER>;
+    constexpr int NTA = TX * TY + (RW ? 32 * ((L::NRING + 31) / 32) : 0);
+    auto kern = mv_zm_kernel<TX, TY, MINB, PER, RW>;
     static int per_sm = 0, sms = 0;
     if (!per_sm) {
         acch_status st = set_smem(kern, L::bytes);
         if (st != ACCH_OK) return st;
-        ACCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TX * TY, L::bytes));
+        ACCH_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NTA, L::bytes));
         ACCH_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device));
         if (per_sm < 1) per_sm = 1;
     }
@@ -1161,7 +1461,7 @@ static acch_status launch_matvec_zm_t(acch_ctx *ctx, const double *coef, double 
     mc.hb = -0.5 * ctx->p.beta;
     mc.idt = 1.0 / dt;
     mc.irho = 1.0 / ctx->p.rho;
-    kern<<<dim3(gx, gy, nchunk), dim3(TX, TY), L::bytes, ctx->stream>>>(g, mc, (const double2 *)w, (double2 *)y, nchunk);
+    kern<<<dim3(gx, gy, nchunk), dim3(NTA), L::bytes, ctx->stream>>>(g, mc, (const double2 *)w, (double2 *)y, nchunk);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
 }
@@ -1170,9 +1470,12 @@ static acch_status launch_matvec_zm(acch_ctx *ctx, const double *coef, double dt
 {
     const char *e = getenv("ACCH_ZM_MINB");
     const bool per = ctx->g.periodic != 0;
+    const char *rw = getenv("ACCH_ZM_RW");
+    if (rw && atoi(rw))
+        return per ? launch_matvec_zm_t<2, true, true>(ctx, coef, dt, w, y) : launch_matvec_zm_t<2, false, true>(ctx, coef, dt, w, y);
     if (e && atoi(e) == 3)
-        return per ? launch_matvec_zm_t<3, true>(ctx, coef, dt, w, y) : launch_matvec_zm_t<3, false>(ctx, coef, dt, w, y);
-    return per ? launch_matvec_zm_t<2, true>(ctx, coef, dt, w, y) : launch_matvec_zm_t<2, false>(ctx, coef, dt, w, y);
+        return per ? launch_matvec_zm_t<3, true, false>(ctx, coef, dt, w, y) : launch_matvec_zm_t<3, false, false>(ctx, coef, dt, w, y);
+    return per ? launch_matvec_zm_t<2, true, false>(ctx, coef, dt, w, y) : launch_matvec_zm_t<2, false, false>(ctx, coef, dt, w, y);
 }
 
 acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)

@@ -62,8 +62,10 @@ def test_chord_known_answers():
 
 # --------------------------------------------------------------------------- scheme
 
+@pytest.mark.parametrize("form", ["zm", "ring"])
 @pytest.mark.parametrize("tag", STENCIL)
-def test_residual_matches_reference(tag):
+def test_residual_matches_reference(tag, form, monkeypatch):
+    monkeypatch.setenv("ACCH_RESIDUAL", form)
     z = golden(f"stencil_{tag}.npz")
     g = grid_of(z)
     prob = StepProblem.create(g, PARAMS, st(g, z["uo"], z["vo"]), float(z["dt"]))
@@ -71,6 +73,28 @@ def test_residual_matches_reference(tag):
     assert np.max(np.abs(F - z["F"])) <= 1e-12 * np.max(np.abs(z["F"]))
     F0 = host(residual_vector(prob, st(g, z["uo"], z["vo"])))
     assert np.max(np.abs(F0 - z["F0"])) <= 1e-12 * np.max(np.abs(z["F0"]))
+
+
+@pytest.mark.parametrize("order", [6, 13])
+@pytest.mark.parametrize("bc", [BoundaryCondition.PERIODIC, BoundaryCondition.NEUMANN])
+def test_residual_runtime_series_order_matches_oracle(order, bc, monkeypatch):
+    """A series order other than the compiled-in 10 (run-time Horner in the
+    z-marching residual) against the oracle, near- and exact-branch states."""
+    from oracle import acch_oracle as O
+    monkeypatch.setenv("ACCH_RESIDUAL", "zm")
+    rng = np.random.default_rng(21)
+    counts = (12, 10, 9)
+    g = Grid(counts, (1.0, 1.0, 1.0), bc)
+    params = Params(4.0, 2.0, 0.005, 0.1, 0.001, order)
+    uo, vo = 0.5 + rng.uniform(-0.05, 0.05, g.array_shape), rng.uniform(-0.05, 0.05, g.array_shape)
+    un, vn = uo + rng.uniform(-0.02, 0.02, g.array_shape), vo + rng.uniform(-0.02, 0.02, g.array_shape)
+    prob = StepProblem.create(g, params, st(g, uo, vo), 1e-3)
+    m = O.Mesh(counts, (1.0, 1.0, 1.0), bc == BoundaryCondition.PERIODIC)
+    so = O.Step(m, O.Coeffs(series_order=order), uo, vo, 1e-3)
+    for a, b in ((un, vn), (uo, vo)):
+        F = host(residual_vector(prob, st(g, a, b)))
+        Fo = so.residual(O.pack(a, b))
+        assert np.max(np.abs(F - Fo)) <= 1e-12 * np.max(np.abs(Fo))
 
 
 @pytest.mark.parametrize("form", ["zm", "twopass", "fused"])

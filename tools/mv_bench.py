@@ -42,6 +42,7 @@ def main():
     ap.add_argument("--bc", default="periodic")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--forms", default="zm,twopass,fused")
+    ap.add_argument("--residual", default="zm,ring")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
@@ -59,9 +60,22 @@ def main():
     w = torch.randn(2 * N, dtype=torch.float64, device=dev, generator=g)
     F = torch.empty_like(w)
     out = {"n": args.n, "bc": args.bc, "peak_gbs": peak}
-    t = timeit(lambda: nat.lib().acch_residual(prob.ctx.bind(), nat.ptr(prob.old.x), prob.dt, nat.ptr(x),
-                                               nat.ptr(F), None, None), args.reps)
-    out["residual"] = {"ms": round(t, 4), "frac": round(48 * N / t / 1e6 / peak, 4)}
+    Fs = {}
+    for rform in args.residual.split(","):
+        name, *opt = rform.split(":")
+        os.environ["ACCH_RESIDUAL"] = name
+        if opt:
+            os.environ["ACCH_RES_MINB"] = opt[0]
+        else:
+            os.environ.pop("ACCH_RES_MINB", None)
+        Fr = torch.empty_like(w)
+        t = timeit(lambda: nat.lib().acch_residual(prob.ctx.bind(), nat.ptr(prob.old.x), prob.dt, nat.ptr(x),
+                                                   nat.ptr(Fr), None, None), args.reps)
+        Fs[rform] = Fr
+        out["residual_" + rform] = {"ms": round(t, 4), "frac": round(48 * N / t / 1e6 / peak, 4)}
+    r0 = Fs[list(Fs)[-1]]
+    out["residual_max_rel_diff"] = {f: (Fs[f] - r0).abs().max().item() / r0.abs().max().item() for f in Fs}
+    os.environ.pop("ACCH_RESIDUAL", None)
     ys = {}
     for form in args.forms.split(","):
         # form[:minb[:pfd]]
