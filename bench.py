@@ -55,7 +55,7 @@ def parse_args():
     ap.add_argument("--solver", default="ilu0")
     ap.add_argument("--variant", default="ras-left")
     ap.add_argument("--restart", type=int, default=30)
-    ap.add_argument("--ortho", default="cgs2", choices=["cgs2", "mgs"])
+    ap.add_argument("--ortho", default="dcgs2", choices=["cgs2", "dcgs2", "mgs"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--verbose", action="store_true")

@@ -188,7 +188,7 @@ acch_status acch_ctx_create(const acch_grid_desc *grid, const acch_params *param
         (e = cudaMalloc(&ctx->d_counter, 16 * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMemset(ctx->d_counter, 0, 16 * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMalloc(&ctx->d_result, sizeof(double) * 64)) != cudaSuccess ||
-        (e = cudaMalloc(&ctx->d_h, sizeof(double) * 128)) != cudaSuccess ||
+        (e = cudaMalloc(&ctx->d_h, sizeof(double) * 256)) != cudaSuccess ||
         (e = cudaMallocHost(&ctx->h_result, sizeof(double) * 128)) != cudaSuccess) {
         acch_ctx_destroy(ctx);
         return acch_cuda_fail(e, "acch_ctx_create allocation");

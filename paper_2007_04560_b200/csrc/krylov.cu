@@ -283,6 +283,181 @@ mupdate_mdot32_kernel(const double *__restrict__ V, long long ld, int m, const d
     if (threadIdx.x == 0) *counter = 0u;
 }
 
+// Lagged second pass (ortho = 2).  Column j holds u_j, the pass-1 vector of
+// the previous step (v_j = (u_j - V_<j h2) / beta, h2 = its pass-2
+// projections, known), column j+1 holds w^ = A M^-1 u_j.  One sweep:
+//   v_j = (u_j - sum_s h2_s V_s) / beta                 -> column j (final)
+//   x   = (w^ - sum_s p_s V_s - p_j v_j) / beta           -> column j+1 (= u_{j+1})
+// with p the projections of w^ on v_0..v_j, and the pass-2 projections of x
+// and ||x||^2 in the same sweep.  result[0] = ||x||^2, result[1 + s] =
+// <V_s, x> (s < J), result[NS] = <v_j, x>.  h2: J values, p: J + 1.
+// p from the multi-dot d (gslot layout): p_s = d_s (s < J), p_J = <v_j, w^> =
+// (d_J - sum_s h2_s d_s) / beta, formed identically by every CTA
+__device__ __forceinline__ void lag_coeffs(int J, const double *__restrict__ h2, const double *__restrict__ d,
+                                           double beta, double *sh, double *sp, int cap)
+{
+    if (threadIdx.x < cap) {
+        sh[threadIdx.x] = threadIdx.x < J ? h2[threadIdx.x] : 0.0;
+        sp[threadIdx.x] = threadIdx.x < J ? d[gslot(threadIdx.x)] : 0.0;
+    }
+    if (threadIdx.x == 0) {
+        double t = d[gslot(J)];
+        for (int s = 0; s < J; ++s) t -= h2[s] * d[gslot(s)];
+        sp[J] = t / beta;
+    }
+}
+
+template <int NS>
+__global__ void __launch_bounds__(kRedThreads)
+lagupd_kernel(const double *__restrict__ V, long long ld, int J, const double *__restrict__ h2,
+              const double *__restrict__ d, double beta, double *__restrict__ U, double *__restrict__ W, long long n,
+              double *partials, unsigned int *counter, double *result, int zero)
+{
+    __shared__ double sh[NS], sp[NS];
+    lag_coeffs(J, h2, d, beta, sh, sp, NS);
+    __syncthreads();
+    double acc[NS + 1];
+#pragma unroll
+    for (int s = 0; s <= NS; ++s) acc[s] = 0.0;
+    const long long n2 = n >> 1;
+    double2 *__restrict__ u2 = reinterpret_cast<double2 *>(U);
+    double2 *__restrict__ w2 = reinterpret_cast<double2 *>(W);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        double2 v[NS - 1];
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s) v[s] = ldg2_pred(reinterpret_cast<const double2 *>(V + s * ld) + i, s < J);
+        double2 u = u2[i], x = w2[i];
+        const int a0 = NS > 1 ? anchor(v[NS > 1 ? NS - 2 : 0], zero) : 0;
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s)
+            if (s < J) {
+                const double hs = sh[s + (s == 0 ? a0 : 0)];
+                u.x -= hs * v[s].x;
+                u.y -= hs * v[s].y;
+            }
+        u.x /= beta;
+        u.y /= beta;
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s)
+            if (s < J) {
+                x.x -= sp[s] * v[s].x;
+                x.y -= sp[s] * v[s].y;
+            }
+        const double pj = sp[J];
+        x.x -= pj * u.x;
+        x.y -= pj * u.y;
+        x.x /= beta;
+        x.y /= beta;
+        u2[i] = u;
+        w2[i] = x;
+        acc[0] += x.x * x.x + x.y * x.y;
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s)
+            if (s < J) acc[1 + s] += v[s].x * x.x + v[s].y * x.y;
+        acc[NS] += u.x * x.x + u.y * x.y;   // <v_j, x>
+    }
+    int ops[NS + 1];
+#pragma unroll
+    for (int s = 0; s <= NS; ++s) ops[s] = RED_SUM;
+    reduce_finish<NS + 1>(acc, ops, partials, counter, result);
+}
+
+// The lagged pass for 16 < J + 1 <= 32 with an element per lane pair (as
+// mupdate_mdot32_kernel): the even lane holds V_0..V_15, the odd V_16..;
+// the halves of V h2 and V p are exchanged by shuffles.  <v_j, x> is
+// returned in result[32].
+__global__ void __launch_bounds__(kRedThreads, 2)
+lagupd32_kernel(const double *__restrict__ V, long long ld, int J, const double *__restrict__ h2,
+                const double *__restrict__ d, double beta, double *__restrict__ U, double *__restrict__ W, long long n,
+                double *partials, unsigned int *counter, double *result, int zero)
+{
+    constexpr int H = 16, NV = 2 * H + 1;   // norm + 32 dots
+    __shared__ double sh[2 * H + 1], sp[2 * H + 1];
+    __shared__ double red[kRedThreads / 32][2][H + 1];
+    __shared__ bool is_last;
+    lag_coeffs(J, h2, d, beta, sh, sp, 2 * H + 1);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = threadIdx.x & 1;
+    const int s0 = half * H;
+    double acc[H + 1];
+#pragma unroll
+    for (int k = 0; k <= H; ++k) acc[k] = 0.0;
+    const long long n2 = n >> 1;
+    double2 *__restrict__ u2 = reinterpret_cast<double2 *>(U);
+    double2 *__restrict__ w2 = reinterpret_cast<double2 *>(W);
+    const long long pairs = (long long)gridDim.x * (blockDim.x >> 1);
+    for (long long base = blockIdx.x * (long long)(blockDim.x >> 1) + warp * 16; base < n2; base += pairs) {
+        const long long i = base + (lane >> 1);
+        const bool ok = i < n2;
+        double2 v[H];
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+            v[k] = ldg2_pred(reinterpret_cast<const double2 *>(V + (s0 + k) * ld) + i, ok && s0 + k < J);
+        double2 u = ok ? u2[i] : make_double2(0.0, 0.0), x = ok ? w2[i] : make_double2(0.0, 0.0);
+        const int a0 = anchor(v[H - 1], zero);
+        double2 ph = make_double2(0.0, 0.0), pp = make_double2(0.0, 0.0);   // halves of V h2, V p
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+            if (s0 + k < J) {
+                const double hs = sh[s0 + k + (k == 0 ? a0 : 0)], ps = sp[s0 + k];
+                ph.x += hs * v[k].x;
+                ph.y += hs * v[k].y;
+                pp.x += ps * v[k].x;
+                pp.y += ps * v[k].y;
+            }
+        double2 oh, op;
+        oh.x = __shfl_xor_sync(0xffffffffu, ph.x, 1);
+        oh.y = __shfl_xor_sync(0xffffffffu, ph.y, 1);
+        op.x = __shfl_xor_sync(0xffffffffu, pp.x, 1);
+        op.y = __shfl_xor_sync(0xffffffffu, pp.y, 1);
+        const double2 hlo = half == 0 ? ph : oh, hhi = half == 0 ? oh : ph;
+        const double2 plo = half == 0 ? pp : op, phi = half == 0 ? op : pp;
+        u.x = ((u.x - hlo.x) - hhi.x) / beta;
+        u.y = ((u.y - hlo.y) - hhi.y) / beta;
+        const double pj = sp[J];
+        x.x = (((x.x - plo.x) - phi.x) - pj * u.x) / beta;
+        x.y = (((x.y - plo.y) - phi.y) - pj * u.y) / beta;
+        if (half == 1 && ok) {
+            u2[i] = u;
+            w2[i] = x;
+        }
+        if (half == 1) acc[0] += x.x * x.x + x.y * x.y;   // 0 when !ok
+#pragma unroll
+        for (int k = 0; k < H; ++k)
+            if (s0 + k < J) acc[1 + k] += v[k].x * x.x + v[k].y * x.y;
+        if (half == 1) acc[H] += u.x * x.x + u.y * x.y;   // <v_j, x> -> result[2H] (V_31's slot, unused: J <= 31)
+    }
+#pragma unroll
+    for (int off = 16; off >= 2; off >>= 1)
+#pragma unroll
+        for (int k = 0; k <= H; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
+    if (lane < 2)
+#pragma unroll
+        for (int k = 0; k <= H; ++k) red[warp][lane][k] = acc[k];
+    __syncthreads();
+    const long long nb = gridDim.x;
+    if (threadIdx.x < NV) {
+        const int j = threadIdx.x;
+        const int hh = j == 0 ? 1 : (j - 1) / H, kk = j == 0 ? 0 : 1 + (j - 1) % H;
+        double t = 0.0;
+        for (int q = 0; q < kRedThreads / 32; ++q) t += red[q][hh][kk];
+        partials[j * nb + blockIdx.x] = t;
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(counter, 1u) == (unsigned int)(nb - 1);
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    if (threadIdx.x < NV) {
+        double t = 0.0;
+        for (long long b = 0; b < nb; ++b) t += __ldcg(partials + threadIdx.x * nb + b);
+        result[threadIdx.x] = t;
+    }
+    if (threadIdx.x == 0) *counter = 0u;
+}
+
 template <int NS>
 __global__ void combine_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ y,
                                double *__restrict__ t, long long n)
@@ -401,6 +576,29 @@ static acch_status mupdate_mdot_to(acch_ctx *ctx, const double *V, long long ld,
                                                                    out, 0);
     } else { acch_set_error("mupdate_mdot: too many vectors"); return ACCH_ERR_INVALID_ARG; }
 #undef MUD_CASE
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+// lagged pass: see lagupd_kernel.  out[0] = ||x||^2, out[1 + s] = <V_s, x>
+// (s < J), out[*vslot] = <v_j, x>
+static acch_status lagupd_to(acch_ctx *ctx, const double *V, long long ld, int J, const double *h2, const double *d,
+                             double beta, double *U, double *W, long long n, double *out, int *vslot)
+{
+    ProfScope prof_scope(ctx, PC_KUPDATE, 8.0 * (J + 4) * n);
+    const int G = rgrid(n);
+#define LAG_CASE(NS) \
+    lagupd_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, J, h2, d, beta, U, W, n, ctx->d_partials, \
+                                                          ctx->d_counter, out, 0);
+    if (J + 1 <= 4) { LAG_CASE(4) *vslot = 4; }
+    else if (J + 1 <= 8) { LAG_CASE(8) *vslot = 8; }
+    else if (J + 1 <= 16) { LAG_CASE(16) *vslot = 16; }
+    else if (J + 1 <= 32) {
+        *vslot = 32;
+        lagupd32_kernel<<<G, kRedThreads, 0, ctx->stream>>>(V, ld, J, h2, d, beta, U, W, n, ctx->d_partials,
+                                                             ctx->d_counter, out, 0);
+    } else { acch_set_error("lagged update: too many vectors"); return ACCH_ERR_INVALID_ARG; }
+#undef LAG_CASE
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
 }
@@ -530,6 +728,12 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
     int total = 0;
     std::vector<double> H((restart + 1) * restart), cs(restart), sn(restart), gv(restart + 1), y(restart);
     auto h = [&](int i, int j) -> double & { return H[i * restart + j]; };
+    // ortho = 2 (lagged second pass): the unrotated Hessenberg matrix, and
+    // the pending correction of the newest column (v_j = (u_j - V h2) / beta)
+    std::vector<double> Hr((restart + 1) * restart), h2p(restart + 1, 0.0);
+    auto hr = [&](int i, int j) -> double & { return Hr[i * restart + j]; };
+    double beta_p = 1.0;
+    double *dh2 = dh + 160;   // device copy of h2p
 
     for (;;) {
         if (res_norm <= tol) {
@@ -546,6 +750,8 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
         std::fill(gv.begin(), gv.end(), 0.0);
         TRY(scale_by(ctx, res_norm, R, col(0), nv));
         gv[0] = res_norm;
+        std::fill(Hr.begin(), Hr.end(), 0.0);
+        beta_p = 1.0;   // v_0 is final
         int j = 0;
         bool breakdown = false;
         while (j < restart && total < max_it) {
@@ -558,7 +764,74 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
             TRY(matvec(zj, w));
             double norm_before, norm_after;
             bool normalised = false;   // w already divided by norm_after
-            if (ortho == 1) {
+            if (ortho == 2) {
+                // Lagged CGS2 (one multi-dot + one fused update per step).
+                // Column j holds u_j with v_j = (u_j - V_<j h2p) / beta_p; w^ =
+                // A M^-1 u_j.  A M^-1 v_j = (w^ - sum_i h2p_i A M^-1 v_i) / beta_p
+                // and A M^-1 v_i = V Hr[:, i] (Arnoldi), so column j of the
+                // Hessenberg matrix is (V^T w^ - c) / beta_p, c_k = sum_i h2p_i
+                // Hr[k, i]; the fused pass writes v_j and
+                // u_{j+1} = (w^ - V (V^T w^)) / beta_p, and returns the pass-2
+                // projections of u_{j+1}, applied one step later.  The second
+                // pass is thus always taken (the reference takes it when
+                // ||w|| < ||w_0|| / 2, i.e. nearly always here; otherwise it
+                // changes the basis at rounding level only).
+                int ns = 0, vslot = 0;
+                const int m = j + 1;
+                TRY(mdot_to(ctx, V + off, nv, m, w + off, ni, dh, &ns));
+                if (multi) TRY(reduce_dots(tmp, dh, 4 * (MG + 1), true));
+                TRY(lagupd_to(ctx, V + off, nv, j, dh2, dh, beta_p, col(j) + off, w + off, ni, dh + 64, &vslot));
+                if (multi) {
+                    TRY(reduce_dots(tmp + 64, dh + 64, 33, false));
+                } else {
+                    TRY(fetch(ctx, tmp, dh, 64 + 33));
+                }
+                // Hessenberg column j (unrotated)
+                double pj = tmp[gslot(j)];
+                for (int s2 = 0; s2 < j; ++s2) pj -= h2p[s2] * tmp[gslot(s2)];
+                pj /= beta_p;
+                for (int k = 0; k <= j; ++k) {
+                    double c = 0.0;
+                    for (int i2 = std::max(k - 1, 0); i2 < j; ++i2) c += h2p[i2] * hr(k, i2);
+                    const double pk = k < j ? tmp[gslot(k)] : pj;
+                    hr(k, j) = (pk - c) / beta_p;
+                }
+                // pending pass 2 of u_{j+1}
+                double hh = 0.0;
+                std::vector<double> h2n(j + 1);
+                for (int k = 0; k <= j; ++k) {
+                    h2n[k] = k < j ? tmp[65 + k] : tmp[64 + vslot];
+                    hh += h2n[k] * h2n[k];
+                    hr(k, j) += h2n[k];
+                }
+                const double xx = tmp[64];
+                norm_before = sqrt(xx);
+                if (xx - hh > 0.0 && hh <= 1e-6 * xx) {
+                    norm_after = sqrt(xx - hh);
+                    for (int k = 0; k <= j; ++k) h2p[k] = h2n[k];
+                    beta_p = norm_after;
+                    ACCH_CUDA(cudaMemcpyAsync(dh2, h2p.data(), sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
+                                              ctx->stream));
+                } else {
+                    // orthogonality lost beyond rounding level: finish u_{j+1}
+                    // explicitly (update, measured norm, scale) -- column j+1 final
+                    ACCH_CUDA(cudaMemcpyAsync(dh2, h2n.data(), sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
+                                              ctx->stream));
+                    TRY(mupdate_to(ctx, V + off, nv, j + 1, dh2, w + off, ni, dh + 40, 0));
+                    double t40;
+                    if (multi) TRY(reduce_dots(&t40, dh + 40, 1, false));
+                    else TRY(fetch(ctx, &t40, dh + 40, 1));
+                    norm_after = sqrt(t40);
+                    if (norm_after > 0.0) TRY(scale_by(ctx, norm_after, w, w, nv));
+                    std::fill(h2p.begin(), h2p.end(), 0.0);
+                    ACCH_CUDA(cudaMemcpyAsync(dh2, h2p.data(), sizeof(double) * (j + 1), cudaMemcpyHostToDevice,
+                                              ctx->stream));
+                    beta_p = 1.0;
+                }
+                hr(j + 1, j) = norm_after;
+                for (int k = 0; k <= j; ++k) h(k, j) = hr(k, j);
+                normalised = true;   // column j+1 stays as u_{j+1} (or was finished above)
+            } else if (ortho == 1) {
                 // pass 1: h1 = V^T w (+ ||w||^2); w -= V h1 fused with the
                 // second pass's projections h2 = V^T w (+ ||w||^2), which are
                 // used only when the reference's cancellation test fires

@@ -66,7 +66,7 @@ class SolverSpec:
     max_newton: int = 50
     gmres_restart: int = 30
     max_linear_iterations: int = 500
-    orthogonalization: str = "cgs2"
+    orthogonalization: str = "dcgs2"
 
 
 @dataclass(frozen=True)

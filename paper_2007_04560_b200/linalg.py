@@ -294,19 +294,21 @@ class GmresResult:
     residual_norm: float
 
 
-ORTHO = {"mgs": 0, "cgs2": 1}
+ORTHO = {"mgs": 0, "cgs2": 1, "dcgs2": 2}
 
 
 def gmres(matvec, b, precond=None, rel_tol: float = 1e-8, abs_tol: float = 1e-14, restart: int = 30,
-          max_iterations: int = 500, x0=None, ortho: str = "cgs2") -> GmresResult:
+          max_iterations: int = 500, x0=None, ortho: str = "dcgs2") -> GmresResult:
     """Restarted right-preconditioned GMRES (linalg.py:411-506).
 
     ``matvec`` must be a JacobianOperator (or its bound ``matvec``) and
     ``precond`` None or a SchwarzPreconditioner; the whole solve then runs in
     libacch_b200.  ``ortho='mgs'`` reproduces the reference's modified
-    Gram-Schmidt operation order; ``'cgs2'`` (default) is classical
+    Gram-Schmidt operation order; ``'cgs2'`` is classical
     Gram-Schmidt with the reference's conditional second pass, fused into two
-    sweeps over the basis.  Stopping and restarts follow the reference: the
+    sweeps over the basis; ``'dcgs2'`` lags the second pass by one Arnoldi
+    step (always taken) so that one multi-dot and one fused update sweep the
+    basis per step (default).  Stopping and restarts follow the reference: the
     recomputed true residual decides convergence."""
     from .scheme import JacobianOperator
     op = matvec

@@ -205,7 +205,7 @@ def test_apply_before_update_raises():
         pre.apply(torch.zeros(128, dtype=torch.float64, device=DEV))
 
 
-@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2", "dcgs2"])
 def test_gmres_matches_reference(ortho):
     z = golden("gmres.npz")
     g = Grid((16, 12), (1.0, 1.0), BoundaryCondition.PERIODIC)
@@ -237,7 +237,7 @@ NEWTON = {
 
 
 @pytest.mark.parametrize("tag", sorted(NEWTON))
-@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2", "dcgs2"])
 def test_newton_matches_reference(tag, ortho):
     z = golden("newton.npz")
     counts, periodic, dt, nsub, ov, solver, kw = NEWTON[tag]
@@ -300,7 +300,7 @@ def _check_sim(z, g, res):
     assert np.max(np.abs(got[:, 4] - got[0, 4])) <= max(2.0 * ref_drift, 1e-12)
 
 
-@pytest.mark.parametrize("ortho", ["mgs", "cgs2"])
+@pytest.mark.parametrize("ortho", ["mgs", "cgs2", "dcgs2"])
 def test_simulate_config1_matches_reference(ortho):
     _check_sim(*_run_sim("c1", ortho))
 
@@ -311,6 +311,13 @@ def test_simulate_adaptive_2d_with_retries_matches_reference():
 
 def test_simulate_adaptive_3d_neumann_with_retries_matches_reference():
     _check_sim(*_run_sim("c3small"))
+
+
+@pytest.mark.parametrize("tag", ["c2small", "c3small"])
+def test_simulate_adaptive_lagged_cgs2_matches_reference(tag):
+    """The lagged second pass (dcgs2) through adaptive runs with divergence
+    retries, against the reference histories."""
+    _check_sim(*_run_sim(tag, "dcgs2"))
 
 
 @pytest.mark.parametrize("mode", ["group", "group4", "tma", "warp", "cta"])
