@@ -366,7 +366,10 @@ lagupd_kernel(const double *__restrict__ V, long long ld, int J, const double *_
 // mupdate_mdot32_kernel): the even lane holds V_0..V_15, the odd V_16..;
 // the halves of V h2 and V p are exchanged by shuffles.  <v_j, x> is
 // returned in result[32].
-__global__ void __launch_bounds__(kRedThreads, 2)
+#ifndef ACCH_LAG32_MINB
+#define ACCH_LAG32_MINB 2
+#endif
+__global__ void __launch_bounds__(kRedThreads, ACCH_LAG32_MINB)
 lagupd32_kernel(const double *__restrict__ V, long long ld, int J, const double *__restrict__ h2,
                 const double *__restrict__ d, double beta, double *__restrict__ U, double *__restrict__ W, long long n,
                 double *partials, unsigned int *counter, double *result, int zero)

@@ -15,7 +15,9 @@ CATEGORY = {"apply_group_kernel": "precond_apply", "apply_warp_kernel": "precond
             "mv_pass1_kernel": "matvec", "mv_pass2_kernel": "matvec", "matvec_kernel": "matvec",
             "residual_kernel": "residual", "factor_kernel": "precond_factor",
             "mdot_grouped_kernel": "krylov_dot", "mupdate_kernel": "krylov_update",
-            "mupdate_mdot_kernel": "krylov_update", "mupdate_mdot32_kernel": "krylov_update"}
+            "mupdate_mdot_kernel": "krylov_update", "mupdate_mdot32_kernel": "krylov_update",
+            "mv_zm_kernel": "matvec", "res_zm_kernel": "residual", "lagupd_kernel": "krylov_update",
+            "lagupd32_kernel": "krylov_update", "apply_rs_kernel": None}
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 out = {}
