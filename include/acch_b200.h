@@ -88,8 +88,9 @@ acch_status acch_residual(acch_ctx *ctx, const double *x_old, double dt, const d
                           double *F, double *gap, double *norm2);
 
 /* assemble_jacobian (scheme.py:427-484), matrix-free form: evaluates the 7
- * per-cell coefficient planes [S, D, cbar, G_u, c_u, c_v, G_v] (7N doubles,
- * caller-owned) that define J at x. */
+ * per-cell coefficients that define J at x into a caller-owned buffer of 7N
+ * doubles (N = stored cells), laid out as N records (S, D, c_u, c_v), then N
+ * records (cbar, G_u), then N values G_v.  Only this library reads it. */
 acch_status acch_jacobian_prepare(acch_ctx *ctx, const double *x_old, double dt,
                                   const double *x, double *coef);
 
@@ -142,7 +143,9 @@ acch_status acch_precond_info(acch_precond *pc, int64_t *factorizations, int64_t
  * (linalg.py:411-506) with J given by (coef, dt) and pc optional (NULL =
  * identity).  x is overwritten with the solution (initial guess 0).
  * ortho: 0 = modified Gram-Schmidt exactly as the reference, 1 = classical
- * Gram-Schmidt with the reference's conditional second pass (fused passes). */
+ * Gram-Schmidt with the reference's conditional second pass (fused passes),
+ * 2 = classical Gram-Schmidt with the second pass lagged by one step (one
+ * multi-dot and one fused update per step; the Python default). */
 acch_status acch_gmres(acch_ctx *ctx, const double *coef, double dt, acch_precond *pc,
                        const double *b, double *x, double rel_tol, double abs_tol,
                        int32_t restart, int32_t max_iterations, int32_t ortho,
