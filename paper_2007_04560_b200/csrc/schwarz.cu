@@ -76,6 +76,7 @@ struct ClassDev {
     const unsigned char *rs_meta;
     int rs_meta_bytes, rs_m_lenU, rs_m_own, rs_m_colL, rs_m_colU, rs_m_rel, rs_nL, rs_ring, rs_far;
     int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
+    int m_lin, m_ixyz, m_own, m_rel;   // gather / scatter tables in the group image
 };
 
 struct ClassHost {
@@ -98,7 +99,7 @@ struct ClassHost {
     std::vector<unsigned char> rs_meta;
     int rs_ok = 0, rs_ring = 0, rs_nL = 0, rs_far = 0, rs_m[5] = {0};
     int rmax = 0;
-    int m_off[13] = {0};
+    int m_off[17] = {0};
     int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
     void *dev_mem = nullptr;
     ClassDev dev;
@@ -777,34 +778,34 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         prefetch_l2(A + lo, (unsigned)(hi - lo) * 32u);
     };
     if (lane < pd) prefetch_level(lane);
-    // gather r into y with many independent loads in flight per lane
-    if (o.w) {
+    // gather r into y with many independent loads in flight per lane; the
+    // offset tables come from the class image in shared memory
+    const int *s_lin = reinterpret_cast<const int *>(smem_meta + C.m_lin);
+    const unsigned *s_ixyz = reinterpret_cast<const unsigned *>(smem_meta + C.m_ixyz);
+    const int *s_relx = reinterpret_cast<const int *>(smem_meta + C.m_rel);
+    const int *s_rely = s_relx + C.len[0], *s_relz = s_rely + C.len[1];
+    // storage index of local cell l of a box that wraps (rel stored mod n)
+    auto wrapped_cell = [&](int l) -> long long {
+        const unsigned p = s_ixyz[l];
+        int gx = o.x + s_relx[p & 1023u];
+        gx = gx >= g.nx ? gx - g.nx : gx;
+        int gy = o.y + s_rely[(p >> 10) & 1023u];
+        gy = gy >= g.ny ? gy - g.ny : gy;
+        int gz = 0;
+        if (g.dim == 3) {
+            gz = o.z + s_relz[p >> 20];
+            gz = g.zg ? gz + g.zg : (gz >= g.nz ? gz - g.nz : gz);
+        }
+        return ((long long)gz * g.ny + gy) * g.nx + gx;
+    };
+    {
         constexpr int GB = 16;
         for (int l0 = 0; l0 < nloc; l0 += 32 * GB) {
             double2 v[GB];
 #pragma unroll
             for (int j = 0; j < GB; ++j) {
                 const int l = l0 + j * 32 + lane;
-                if (l < nloc) v[j] = r[obase + __ldg(C.lin + l)];
-            }
-#pragma unroll
-            for (int j = 0; j < GB; ++j) {
-                const int l = l0 + j * 32 + lane;
-                if (l < nloc) y[l] = (VARIANT == 2 && !C.owned[l]) ? make_double2(0.0, 0.0) : v[j];
-            }
-        }
-    } else {
-        constexpr int GB = 4;
-        for (int l0 = 0; l0 < nloc; l0 += 32 * GB) {
-            double2 v[GB];
-#pragma unroll
-            for (int j = 0; j < GB; ++j) {
-                const int l = l0 + j * 32 + lane;
-                if (l < nloc) {
-                    int gx, gy, gz;
-                    local_to_global(g, C, o, l, gx, gy, gz);
-                    v[j] = r[cell_at(g, gx, gy, zplane(g, gz))];
-                }
+                if (l < nloc) v[j] = r[o.w ? obase + s_lin[l] : wrapped_cell(l)];
             }
 #pragma unroll
             for (int j = 0; j < GB; ++j) {
@@ -838,17 +839,10 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     }
     if (VARIANT == 1) {
         // owned cells only (left RAS), from the class's owned-cell list
+        const unsigned short *s_own = reinterpret_cast<const unsigned short *>(smem_meta + C.m_own);
         for (int k = lane; k < C.n_owned; k += 32) {
-            const int l = __ldg(C.own_list + k);
-            long long idx;
-            if (o.w) {
-                idx = obase + __ldg(C.lin + l);
-            } else {
-                int gx, gy, gz;
-                local_to_global(g, C, o, l, gx, gy, gz);
-                idx = cell_at(g, gx, gy, zplane(g, gz));
-            }
-            z[idx] = y[l];
+            const int l = s_own[k];
+            z[o.w ? obase + s_lin[l] : wrapped_cell(l)] = y[l];
         }
     } else {
         for (int l = lane; l < nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
@@ -1774,6 +1768,13 @@ void build_meta(ClassHost &C)
     m[10] = seg(sizeof(int) * C.b_jptr.size());
     m[11] = seg(2 * (C.f_joff.size() + kJoPad));
     m[12] = seg(2 * (C.b_joff.size() + kJoPad));
+    // gather / scatter: linear offsets (boxes that do not wrap), packed local
+    // coordinates + per-axis relative coordinates (boxes that wrap), owned list
+    const int lx = (int)C.rel[0].size(), ly = (int)C.rel[1].size(), lz = C.rel[2].empty() ? 1 : (int)C.rel[2].size();
+    m[13] = seg(sizeof(int) * (size_t)C.nloc);
+    m[14] = seg(sizeof(unsigned) * (size_t)C.nloc);
+    m[15] = seg(2 * std::max<size_t>(1, C.own_list.size()));
+    m[16] = seg(sizeof(int) * (size_t)(lx + ly + lz));
     C.meta.assign(at, 0);
     auto put = [&](int o, const void *src, size_t bytes) { if (bytes) memcpy(C.meta.data() + o, src, bytes); };
     put(m[0], C.lev_ptr.data(), sizeof(int) * (nlev + 1));
@@ -1793,6 +1794,19 @@ void build_meta(ClassHost &C)
     put(m[11], j16.data(), 2 * j16.size());
     j16.assign(C.b_joff.begin(), C.b_joff.end());
     put(m[12], j16.data(), 2 * j16.size());
+    put(m[13], C.lin.data(), sizeof(int) * C.lin.size());
+    std::vector<unsigned> ixyz(C.nloc);
+    for (int l = 0; l < C.nloc; ++l)
+        ixyz[l] = (unsigned)(l % lx) | ((unsigned)((l / lx) % ly) << 10) | ((unsigned)(l / (lx * ly)) << 20);
+    put(m[14], ixyz.data(), sizeof(unsigned) * ixyz.size());
+    std::vector<unsigned short> o16(C.own_list.begin(), C.own_list.end());
+    put(m[15], o16.data(), 2 * o16.size());
+    std::vector<int> rl;
+    for (int a = 0; a < 3; ++a) {
+        const int la = a == 0 ? lx : (a == 1 ? ly : lz);
+        for (int i = 0; i < la; ++i) rl.push_back(C.rel[a].empty() ? 0 : C.rel[a][i]);
+    }
+    put(m[16], rl.data(), sizeof(int) * rl.size());
 }
 
 acch_status upload_class(ClassHost &C)
@@ -1922,6 +1936,10 @@ acch_status upload_class(ClassHost &C)
     d.m_bjp = C.m_off[10];
     d.m_fjo = C.m_off[11];
     d.m_bjo = C.m_off[12];
+    d.m_lin = C.m_off[13];
+    d.m_ixyz = C.m_off[14];
+    d.m_own = C.m_off[15];
+    d.m_rel = C.m_off[16];
     d.ell_total = C.ell_total;
     d.max_fwidth = C.max_fwidth;
     d.max_bwidth = C.max_bwidth;
