@@ -77,6 +77,7 @@ struct ClassDev {
     int rs_meta_bytes, rs_m_lenU, rs_m_own, rs_m_colL, rs_m_colU, rs_m_rel, rs_nL, rs_ring, rs_far;
     int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
     int m_lin, m_ixyz, m_own, m_rel;   // gather / scatter tables in the group image
+    int jdup;   // some row has two stencil entries on one pattern position (tiny periodic axes)
 };
 
 struct ClassHost {
@@ -98,6 +99,7 @@ struct ClassHost {
     std::vector<int> rs_pos;
     std::vector<unsigned char> rs_meta;
     int rs_ok = 0, rs_ring = 0, rs_nL = 0, rs_far = 0, rs_m[5] = {0};
+    int jdup = 0;
     int rmax = 0;
     int m_off[17] = {0};
     int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
@@ -154,15 +156,22 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
         local_to_global(g, C, o, l, gx, gy, gz);
         double blk[NOFF][4];
         jac_row_blocks<DIM>(g, P, dt, coef, gx, gy, gz, blk, NOFF);
+        // when every stencil entry of a row has its own pattern position (all
+        // but tiny periodic axes, where +-2 wrap onto one cell) the blocks are
+        // stored, not accumulated: no read of the zeroed slots
         for (int q = 0; q < NOFF; ++q) {
             const int p = C.jmap[l * NOFF + q];
             if (p < 0) continue;
-            double4 v = A[p];
-            v.x += blk[q][0];
-            v.y += blk[q][1];
-            v.z += blk[q][2];
-            v.w += blk[q][3];
-            A[p] = v;
+            if (!C.jdup) {
+                A[p] = make_double4(0.0 + blk[q][0], 0.0 + blk[q][1], 0.0 + blk[q][2], 0.0 + blk[q][3]);
+            } else {
+                double4 v = A[p];
+                v.x += blk[q][0];
+                v.y += blk[q][1];
+                v.z += blk[q][2];
+                v.w += blk[q][3];
+                A[p] = v;
+            }
         }
     }
     __syncthreads();
@@ -177,16 +186,32 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
                 const double4 ak = A[pt], dk = A[C.pos[C.diag[k]]];
                 const Blk L = mul({ak.x, ak.y, ak.z, ak.w}, {dk.x, dk.y, dk.z, dk.w});
                 A[pt] = make_double4(L.a, L.b, L.c, L.d);
-                for (int u = C.upd_ptr[t]; u < C.upd_ptr[t + 1]; ++u) {
-                    const int2 sd = C.upd[u];
-                    const double4 us = A[sd.x];
-                    const Blk m = mul(L, {us.x, us.y, us.z, us.w});
-                    double4 v = A[sd.y];
-                    v.x -= m.a;
-                    v.y -= m.b;
-                    v.z -= m.c;
-                    v.w -= m.d;
-                    A[sd.y] = v;
+                // the updates of one pivot touch distinct targets and read row
+                // k's finished U blocks: batches of UB sources and targets are
+                // loaded together (one L2 round trip per batch, not per update)
+                constexpr int UB = 8;
+                const int u1 = C.upd_ptr[t + 1];
+                for (int u0 = C.upd_ptr[t]; u0 < u1; u0 += UB) {
+                    int2 sd[UB];
+                    double4 us[UB], v[UB];
+#pragma unroll
+                    for (int b = 0; b < UB; ++b) sd[b] = u0 + b < u1 ? C.upd[u0 + b] : make_int2(0, 0);
+#pragma unroll
+                    for (int b = 0; b < UB; ++b)
+                        if (u0 + b < u1) {
+                            us[b] = A[sd[b].x];
+                            v[b] = A[sd[b].y];
+                        }
+#pragma unroll
+                    for (int b = 0; b < UB; ++b)
+                        if (u0 + b < u1) {
+                            const Blk m = mul(L, {us[b].x, us[b].y, us[b].z, us[b].w});
+                            v[b].x -= m.a;
+                            v[b].y -= m.b;
+                            v[b].z -= m.c;
+                            v[b].w -= m.d;
+                            A[sd[b].y] = v[b];
+                        }
                 }
             }
             // diagonal block: scalar pivots as the reference's factor_inplace sees them
@@ -1536,6 +1561,13 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
             const int *f = std::lower_bound(b, e, lt);
             C.jmap[(size_t)l * noff + q] = (int)(f - C.col.data());
         }
+    C.jdup = 0;
+    for (int l = 0; l < nloc && !C.jdup; ++l)
+        for (int q = 0; q < noff; ++q)
+            for (int q2 = 0; q2 < q; ++q2) {
+                const int a = C.jmap[(size_t)l * noff + q], b = C.jmap[(size_t)l * noff + q2];
+                if (a >= 0 && a == b) C.jdup = 1;
+            }
     C.jmap_local.assign(C.jmap.size(), -1);
     for (int l = 0; l < nloc; ++l)
         for (int q = 0; q < noff; ++q) {
@@ -1923,6 +1955,7 @@ acch_status upload_class(ClassHost &C)
     d.rs_nL = C.rs_nL;
     d.rs_ring = C.rs_ring;
     d.rs_far = C.rs_far;
+    d.jdup = C.jdup;
     d.meta_bytes = (int)C.meta.size();
     d.m_fbs = C.m_off[1];
     d.m_bptr = C.m_off[2];

@@ -411,6 +411,32 @@ def test_row_sequential_solver_matches_oracle(variant, bc, monkeypatch):
     assert np.max(np.abs(out - ref)) <= 1e-10 * np.max(np.abs(ref))
 
 
+@pytest.mark.parametrize("counts", [(4, 10), (4, 6, 8), (6, 4, 5)])
+def test_schwarz_tiny_periodic_axis_matches_oracle(counts):
+    """A 4-cell periodic axis puts the +-2 stencil entries on one cell: the
+    factorisation must sum those Jacobian contributions (the store-only
+    assembly is for classes without such duplicates)."""
+    from oracle import acch_oracle as O
+    rng = np.random.default_rng(31)
+    g = Grid(counts, (1.0,) * len(counts), BoundaryCondition.PERIODIC)
+    uo, vo = 0.5 + rng.uniform(-0.05, 0.05, g.array_shape), rng.uniform(-0.05, 0.05, g.array_shape)
+    un, vn = uo + rng.uniform(-0.01, 0.01, g.array_shape), vo + rng.uniform(-0.01, 0.01, g.array_shape)
+    prob = StepProblem.create(g, PARAMS, st(g, uo, vo), 1e-3)
+    J = assemble_jacobian(prob, st(g, un, vn))
+    r = rng.standard_normal(2 * g.n_cells)
+    m = O.Mesh(counts, (1.0,) * len(counts), True)
+    Jo = O.Step(m, O.Coeffs(), uo, vo, 1e-3).jacobian(O.pack(un, vn)).assemble()
+    for nsub, solver in ((1, "ilu0"), (2, "ilu0"), (2, "lu")):
+        pre = SchwarzPreconditioner(partition(g, nsub, 1), SchwarzVariant.LEFT_RAS,
+                                    SubdomainSolverSpec.from_string(solver))
+        pre.update(J)
+        out = host(pre.apply(torch.tensor(r, device=DEV)))
+        po = O.SchwarzOracle(O.decompose(m, nsub, 1), "ras-left", solver)
+        po.update(Jo)
+        ref = po.apply(r)
+        assert np.max(np.abs(out - ref)) <= 1e-10 * np.max(np.abs(ref))
+
+
 @pytest.mark.parametrize("solver", ["ilu0", "ilu1", "lu"])
 @pytest.mark.parametrize("bc", [BoundaryCondition.PERIODIC, BoundaryCondition.NEUMANN])
 def test_warp_factorisation_bitwise_equal_cta_factorisation(solver, bc, monkeypatch):
