@@ -136,8 +136,11 @@ __device__ __forceinline__ Blk mul(const Blk &x, const Blk &y)
     return {x.a * y.a + x.b * y.c, x.a * y.b + x.b * y.d, x.c * y.a + x.d * y.c, x.c * y.b + x.d * y.d};
 }
 
+#ifndef ACCH_FACTOR_MINB
+#define ACCH_FACTOR_MINB 8
+#endif
 template <int DIM>
-__global__ void __launch_bounds__(kFactorThreads)
+__global__ void __launch_bounds__(kFactorThreads, ACCH_FACTOR_MINB)
 factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef, const ClassDev *__restrict__ classes,
               const int *__restrict__ sub_class, const int4 *__restrict__ sub_origin,
               const long long *__restrict__ sub_off, double4 *__restrict__ vals, int *__restrict__ bad_row, int ss)
@@ -189,7 +192,10 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
                 // the updates of one pivot touch distinct targets and read row
                 // k's finished U blocks: batches of UB sources and targets are
                 // loaded together (one L2 round trip per batch, not per update)
-                constexpr int UB = 8;
+#ifndef ACCH_FACTOR_UB
+#define ACCH_FACTOR_UB 2
+#endif
+                constexpr int UB = ACCH_FACTOR_UB;
                 const int u1 = C.upd_ptr[t + 1];
                 for (int u0 = C.upd_ptr[t]; u0 < u1; u0 += UB) {
                     int2 sd[UB];
