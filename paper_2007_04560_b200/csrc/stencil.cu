@@ -897,6 +897,9 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
     double wvm = 0.0;                                 // centre w_v at plane k-1
     double lxy_k = 0.0, lxy_k1 = 0.0;                 // centre xy-lap(w_v) at planes k, k+1
     double Sk = 0.0, Dk = 0.0, Sk1 = 0.0, Dk1 = 0.0;  // centre S, D at planes k, k+1
+    // centre column's (dG_u, cbar, eta, G_u) at planes k-1, k, k+1 (registers:
+    // the z-faces and the cell's own values need no shared-memory reads)
+    double4 bm = make_double4(0.0, 0.0, 0.0, 0.0), b0 = bm, b1 = bm;
 
     // build B(kk) from W(kk) (slot s1) and W(kk+1) (slot s2); wuz = w_u(kk-1)
     auto build = [&](int s1, int s2, int sb) {
@@ -920,6 +923,7 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
                     lxy_k1 = (xp.y - 2.0 * w0.y + xm.y) * ihx + (yp.y - 2.0 * w0.y + ym.y) * ihy;
                     Sk1 = cS[0];
                     Dk1 = cD[0];
+                    b1 = make_double4(dG, cC[0], et, cG[0]);
                 }
             }
         }
@@ -951,6 +955,7 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
     cp_async_commit();
     build(0, 1, 0);              // B(zb-1) -> slot 0; needs W(zb) centre = slot 1
     wvm = wk1.y;
+    bm = b1;
     prefetch(poff(z0));
     cp_async_wait_group<1>();    // W(zb+1) landed, W(zb+2) may still be in flight
     __syncthreads();
@@ -958,6 +963,7 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
     load_w(poff(z3), 0);
     cp_async_commit();
     build(1, 2, 1);              // B(zb) -> slot 1
+    b0 = b1;
     wk = wk1;
     lxy_k = lxy_k1;
     Sk = Sk1;
@@ -981,8 +987,7 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
         if (active) {
             const double2 *B1 = sB1 + sb1 * NB, *B2 = sB2 + sb1 * NB;
             const int c0 = gc[0];
-            const double2 a0 = B1[c0], e0 = B2[c0];
-            const double dG0 = a0.x, C0 = a0.y, E0 = e0.x, G0 = e0.y;
+            const double dG0 = b0.x, C0 = b0.y, E0 = b0.z, G0 = b0.w;
             double d1 = 0.0, d2 = 0.0;
             auto face = [&](const double2 &an, const double2 &en, double fh, bool lo_ok, bool hi_ok,
                             const double2 &am, const double2 &em) {
@@ -997,8 +1002,8 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
             };
             face(B1[c0 + 1], B2[c0 + 1], fhx, fxl, fxh, B1[c0 - 1], B2[c0 - 1]);
             face(B1[c0 + GX], B2[c0 + GX], fhy, fyl, fyh, B1[c0 - GX], B2[c0 - GX]);
-            face(sB1[sb2 * NB + c0], sB2[sb2 * NB + c0], fhz, PER || zstep_ok(g, k, -1), PER || zstep_ok(g, k, +1),
-                 sB1[sb0 * NB + c0], sB2[sb0 * NB + c0]);
+            face(make_double2(b1.x, b1.y), make_double2(b1.z, b1.w), fhz, PER || zstep_ok(g, k, -1),
+                 PER || zstep_ok(g, k, +1), make_double2(bm.x, bm.y), make_double2(bm.z, bm.w));
             const double lapv = lxy_k + (wk1.y - 2.0 * wk.y + wvm) * ihz;
             double2 out;
             out.x = wk.x * idt - d1 - d2;
@@ -1006,6 +1011,8 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
             yout[poff(z0) + coff[0]] = out;
         }
         // rotate
+        bm = b0;
+        b0 = b1;
         wvm = wk.y;
         wk = wk1;
         lxy_k = lxy_k1;
