@@ -1687,6 +1687,66 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
         levb[i] = m;
         nlevb = std::max(nlevb, m + 1);
     }
+    // Width-capped list schedules: a level wider than a warp costs the warp
+    // solvers a second round trip for its extra rows, so levels are refilled
+    // to <= 32 rows (Kahn's algorithm, ready rows taken in order of their
+    // latest feasible level).  Any topological schedule gives the same sweep
+    // results bitwise: every row is still computed from finished rows only, in
+    // its own slot order.  At 8^3 boxes: 55 levels of up to 34 rows -> 56 of
+    // up to 32.
+    {
+        constexpr int kCap = 32;
+        auto capped = [&](bool forward, std::vector<int> &lv, int &nl) {
+            // deps(i): L columns (forward) / U columns (backward); users: the reverse
+            std::vector<std::vector<int>> users(nloc);
+            std::vector<int> indeg(nloc, 0);
+            for (int i = 0; i < nloc; ++i) {
+                const int t0 = forward ? C.rowptr[i] : C.diag[i] + 1, t1 = forward ? C.diag[i] : C.rowptr[i + 1];
+                indeg[i] = t1 - t0;
+                for (int t = t0; t < t1; ++t) users[C.col[t]].push_back(i);
+            }
+            // latest level of each row in the uncapped schedule (longest path to a sink)
+            std::vector<int> tail(nloc, 0);
+            for (int k = 0; k < nloc; ++k) {
+                const int i = forward ? nloc - 1 - k : k;   // users come after i in the sweep order
+                for (int u : users[i]) tail[i] = std::max(tail[i], tail[u] + 1);
+            }
+            std::vector<std::pair<int, int>> ready;   // (-tail, row): min-heap on -tail, i.e. longest tail first
+            auto cmp = [](const std::pair<int, int> &a, const std::pair<int, int> &b) { return a > b; };
+            for (int i = 0; i < nloc; ++i)
+                if (indeg[i] == 0) ready.emplace_back(-tail[i], i);
+            std::make_heap(ready.begin(), ready.end(), cmp);
+            nl = 0;
+            std::vector<int> take, fresh;
+            while (!ready.empty()) {
+                take.clear();
+                while (!ready.empty() && (int)take.size() < kCap) {
+                    std::pop_heap(ready.begin(), ready.end(), cmp);
+                    take.push_back(ready.back().second);
+                    ready.pop_back();
+                }
+                fresh.clear();
+                for (int i : take) {
+                    lv[i] = nl;
+                    for (int u : users[i])
+                        if (--indeg[u] == 0) fresh.push_back(u);
+                }
+                for (int u : fresh) {
+                    ready.emplace_back(-tail[u], u);
+                    std::push_heap(ready.begin(), ready.end(), cmp);
+                }
+                ++nl;
+            }
+        };
+        auto width = [&](const std::vector<int> &lv, int nl) {
+            std::vector<int> w(nl, 0);
+            int m = 0;
+            for (int i = 0; i < nloc; ++i) m = std::max(m, ++w[lv[i]]);
+            return m;
+        };
+        if (width(lev, nlev) > kCap) capped(true, lev, nlev);
+        if (width(levb, nlevb) > kCap) capped(false, levb, nlevb);
+    }
     auto bucket = [&](const std::vector<int> &lv, int nl, std::vector<int> &ptr, std::vector<int> &rows) {
         ptr.assign(nl + 1, 0);
         for (int i = 0; i < nloc; ++i) ptr[lv[i] + 1]++;
