@@ -377,10 +377,13 @@ __device__ __forceinline__ void ldg4_pred(double4 &v, const double4 *p, bool pre
                  : "l"(p), "r"((unsigned)pred), "l"(pol));
 }
 
+// acc -= a y for a 2x2 block, with the rounding pinned by intrinsics
+// (product, fused second product, subtraction): every solver and code path
+// gives bitwise the same result, whatever contraction the compiler would pick
 __device__ __forceinline__ void blk_sub(double2 &acc, const double4 &a, const double2 &y)
 {
-    acc.x -= a.x * y.x + a.y * y.y;
-    acc.y -= a.z * y.x + a.w * y.y;
+    acc.x = __dsub_rn(acc.x, __fma_rn(a.y, y.y, __dmul_rn(a.x, y.x)));
+    acc.y = __dsub_rn(acc.y, __fma_rn(a.w, y.y, __dmul_rn(a.z, y.x)));
 }
 
 template <int VARIANT, int TPS, int MAXW = 12>   // VARIANT: 0 asm, 1 ras-left, 2 ras-right
@@ -752,10 +755,26 @@ __device__ __forceinline__ void sweep_level(const double4 *__restrict__ A, const
         for (int t = 0; t < MAXW; ++t)
             if (t < len1) blk_sub(acc1, a[t], y[c[t]]);
     }
-    for (int t = MAXW; __any_sync(0xffffffffu, len0 > t || len1 > t); ++t) {   // rows longer than MAXW slots
-        const int e = base + jo[t] + lane;
-        if (t < len0) blk_sub(acc0, ldg4(A + e), y[ecol[e]]);
-        if (t < len1) blk_sub(acc1, ldg4(A + e + 32), y[ecol[e + 32]]);
+    // rows longer than MAXW slots (U rows of a wrapped periodic box, <= 21):
+    // the extra slots of the first row in batches of XB loads through a[],
+    // one round trip per batch instead of one per slot
+    constexpr int XB = 4;
+    for (int t0 = MAXW; __any_sync(0xffffffffu, len0 > t0 || len1 > t0); t0 += XB) {
+#pragma unroll
+        for (int u = 0; u < XB; ++u) {
+            const int t = t0 + u;
+            const int e = base + jo[t] + lane;
+            ldg4_pred(a[u], A + e, t < len0, pol);
+            c[u] = t < len0 ? ecol[e] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < XB; ++u)
+            if (t0 + u < len0) blk_sub(acc0, a[u], y[c[u]]);
+        for (int t = t0; t < t0 + XB; ++t)
+            if (t < len1) {
+                const int e = base + jo[t] + lane + 32;
+                blk_sub(acc1, ldg4(A + e), y[ecol[e]]);
+            }
     }
     if (backward) {
         acc0 = make_double2(d0.x * acc0.x + d0.y * acc0.y, d0.z * acc0.x + d0.w * acc0.y);
