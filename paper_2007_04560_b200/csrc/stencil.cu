@@ -278,12 +278,13 @@ residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ x
 template <int TX, int TY>
 struct RzmSmem {
     static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2;
-    static constexpr int NW = HX * HY, NB = GX * GY, NRING = 2 * GX + 2 * TY;
+    // ring columns: the tile+1 border without its 4 corners (never read by the 5-point output)
+    static constexpr int NW = HX * HY, NB = GX * GY, NRING = 2 * TX + 2 * TY;
     static constexpr size_t bytes = sizeof(double2) * (2 * 4 * NW + 3 * NB);
 };
 
 template <int TX, int TY, int MINB, bool PER, bool RW, int ORDER>
-__global__ void __launch_bounds__(TX *TY + (RW ? 32 * ((2 * TX + 4 * TY + 4 + 31) / 32) : 0), MINB)
+__global__ void __launch_bounds__(TX *TY + (RW ? 32 * ((2 * TX + 2 * TY + 31) / 32) : 0), MINB)
 res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__restrict__ xo_g,
               const double2 *__restrict__ xn_g, double2 *__restrict__ F, double *partials, unsigned int *counter,
               double *result, int nchunk)
@@ -325,10 +326,10 @@ res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__re
     {
         int r = has_ring ? tid : 0;
         if (RW && !centre) r = min(tid - NT, NRING - 1);   // spare lanes repeat the last ring column
-        if (r < GX) { cx[1] = r - 1; cy[1] = -1; }
-        else if (r < 2 * GX) { cx[1] = r - GX - 1; cy[1] = TY; }
-        else if (r < 2 * GX + TY) { cx[1] = -1; cy[1] = r - 2 * GX; }
-        else { cx[1] = TX; cy[1] = r - 2 * GX - TY; }
+        if (r < TX) { cx[1] = r; cy[1] = -1; }
+        else if (r < 2 * TX) { cx[1] = r - TX; cy[1] = TY; }
+        else if (r < 2 * TX + TY) { cx[1] = -1; cy[1] = r - 2 * TX; }
+        else { cx[1] = TX; cy[1] = r - 2 * TX - TY; }
         if (RW && !centre) {
             cx[0] = cx[1];
             cy[0] = cy[1];
@@ -776,7 +777,8 @@ matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
 template <int TX, int TY>
 struct ZmSmem {
     static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2;
-    static constexpr int NW = HX * HY, NB = GX * GY, NRING = 2 * GX + 2 * TY;
+    // ring columns: the tile+1 border without its 4 corners (never read by the 5-point output)
+    static constexpr int NW = HX * HY, NB = GX * GY, NRING = 2 * TX + 2 * TY;
     static constexpr size_t bytes = sizeof(double2) * (4 * NW + 2 * 3 * NB);
 };
 
@@ -793,7 +795,7 @@ struct MvConst {
 };
 
 template <int TX, int TY, int MINB, bool PER, bool RW>
-__global__ void __launch_bounds__(TX *TY + (RW ? 32 * ((2 * TX + 4 * TY + 4 + 31) / 32) : 0), MINB)
+__global__ void __launch_bounds__(TX *TY + (RW ? 32 * ((2 * TX + 2 * TY + 31) / 32) : 0), MINB)
 mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g, double2 *__restrict__ yout,
              int nchunk)
 {
@@ -844,10 +846,10 @@ mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g,
     {
         // ring of the tile+1 region in tile coordinates (-1 .. TX, -1 .. TY)
         int r = has_ring ? tid : 0;
-        if (r < GX) { cx[1] = r - 1; cy[1] = -1; }
-        else if (r < 2 * GX) { cx[1] = r - GX - 1; cy[1] = TY; }
-        else if (r < 2 * GX + TY) { cx[1] = -1; cy[1] = r - 2 * GX; }
-        else { cx[1] = TX; cy[1] = r - 2 * GX - TY; }
+        if (r < TX) { cx[1] = r; cy[1] = -1; }
+        else if (r < 2 * TX) { cx[1] = r - TX; cy[1] = TY; }
+        else if (r < 2 * TX + TY) { cx[1] = -1; cy[1] = r - 2 * TX; }
+        else { cx[1] = TX; cy[1] = r - 2 * TX - TY; }
         if (RW && !centre) {
             cx[0] = cx[1];
             cy[0] = cy[1];
@@ -1435,10 +1437,9 @@ static acch_status launch_matvec_twopass(acch_ctx *ctx, const double *coef, doub
     return ACCH_OK;
 }
 
-template <int MINB, bool PER, bool RW>
+template <int MINB, bool PER, bool RW, int TX = 32, int TY = 8>
 static acch_status launch_matvec_zm_t(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
-    constexpr int TX = 32, TY = 8;
     using L = ZmSmem<TX, TY>;
     constexpr int NTA = TX * TY + (RW ? 32 * ((L::NRING + 31) / 32) : 0);
     auto kern = mv_zm_kernel<TX, TY, MINB, PER, RW>;
