@@ -113,6 +113,8 @@ struct acch_ctx {
     double *d_krylov = nullptr;       // (restart + 1) * 2N
     int krylov_cols = 0;
     double *d_work = nullptr;         // 3 * 2N: z (precond out), r, t
+    double *d_zbasis = nullptr;       // lagged CGS2 with a preconditioner: M^-1 u_j per step (restart columns)
+    int zbasis_cols = 0;
     double *d_h = nullptr;            // small device array for Hessenberg column
     double *d_mvtmp = nullptr;        // two-pass matvec intermediate (dG_u, eta), 2 * nstore
     int matvec_mode = 2;              // 2 z-marching one-barrier kernel (3D default), 1 two-pass (2D), 0 older fused kernel

@@ -208,6 +208,7 @@ acch_status acch_ctx_destroy(acch_ctx *ctx)
     cudaFree(ctx->d_h);
     cudaFree(ctx->d_krylov);
     cudaFree(ctx->d_work);
+    cudaFree(ctx->d_zbasis);
     cudaFree(ctx->d_mvtmp);
     if (ctx->h_result) cudaFreeHost(ctx->h_result);
     delete ctx;

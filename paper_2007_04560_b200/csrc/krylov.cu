@@ -743,6 +743,20 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
     auto hr = [&](int i, int j) -> double & { return Hr[i * restart + j]; };
     double beta_p = 1.0;
     double *dh2 = dh + 160;   // device copy of h2p
+    // ortho = 2 with a preconditioner: z_j = M^-1 u_j is kept per step, and
+    // M^-1 v_j = sum_i Tz[i, j] z_i (v_j = (u_j - V h2p) / beta_p), so the
+    // cycle's update x += M^-1 V y = Z (Tz y) needs no extra apply
+    const bool keepz = ortho == 2 && pc;
+    std::vector<double> Tz(keepz ? restart * restart : 0), yz(restart);
+    auto tz = [&](int i, int j) -> double & { return Tz[i * restart + j]; };
+    if (keepz && ctx->zbasis_cols < restart) {
+        if (ctx->d_zbasis) cudaFree(ctx->d_zbasis);
+        ctx->d_zbasis = nullptr;
+        ACCH_CUDA(cudaMalloc(&ctx->d_zbasis, sizeof(double) * nv * restart));
+        ACCH_CUDA(cudaMemsetAsync(ctx->d_zbasis, 0, sizeof(double) * nv * restart, ctx->stream));
+        ctx->zbasis_cols = restart;
+    }
+    auto zcol = [&](int j) { return ctx->d_zbasis + (long long)j * nv; };
 
     for (;;) {
         if (res_norm <= tol) {
@@ -760,12 +774,22 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
         TRY(scale_by(ctx, res_norm, R, col(0), nv));
         gv[0] = res_norm;
         std::fill(Hr.begin(), Hr.end(), 0.0);
+        std::fill(Tz.begin(), Tz.end(), 0.0);
         beta_p = 1.0;   // v_0 is final
         int j = 0;
         bool breakdown = false;
         while (j < restart && total < max_it) {
             const double *zj = col(j);
-            if (pc) {
+            if (keepz) {
+                // Tz[:, j] = (e_j - sum_i h2p_i Tz[:, i]) / beta_p
+                for (int k = 0; k <= j; ++k) {
+                    double t = k == j ? 1.0 : 0.0;
+                    for (int i2 = k; i2 < j; ++i2) t -= h2p[i2] * tz(k, i2);
+                    tz(k, j) = t / beta_p;
+                }
+                TRY(precond(col(j), zcol(j)));
+                zj = zcol(j);
+            } else if (pc) {
                 TRY(precond(col(j), Z));
                 zj = Z;
             }
@@ -940,6 +964,18 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                 for (int k = i + 1; k < j; ++k) s -= h(i, k) * y[k];
                 y[i] = s / h(i, i);
             }
+            if (keepz) {
+                for (int k = 0; k < j; ++k) {
+                    double t = 0.0;
+                    for (int i2 = k; i2 < j; ++i2) t += tz(k, i2) * y[i2];
+                    yz[k] = t;
+                }
+                ACCH_CUDA(cudaMemcpyAsync(dh, yz.data(), sizeof(double) * j, cudaMemcpyHostToDevice, ctx->stream));
+                TRY(combine(ctx, ctx->d_zbasis, nv, j, dh, T, nv));
+                TRY(launch_axpby(ctx, 1.0, T, 1.0, x, nv));
+                ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
+                goto cycle_done;
+            }
             ACCH_CUDA(cudaMemcpyAsync(dh, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, ctx->stream));
             TRY(combine(ctx, V, nv, j, dh, T, nv));
             if (pc) {
@@ -951,6 +987,7 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
             // the host array y is reused next cycle: make sure the copy landed
             ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
         }
+    cycle_done:
         TRY(matvec(x, R));
         TRY(launch_axpby(ctx, 1.0, b, -1.0, R, nv));
         TRY(dot_to(ctx, R + off, R + off, ni, dh));
