@@ -2100,7 +2100,7 @@ struct acch_precond {
     int4 *d_groups = nullptr;
     int *d_grp_sub = nullptr;
     TmaSmem tl{};
-    int pf_depth = 2;      // levels prefetched ahead into L2 (ACCH_PREFETCH_DEPTH overrides; 2 measured best for the group solver)
+    int pf_depth = 3;      // levels prefetched ahead into L2 (ACCH_PREFETCH_DEPTH overrides; 3 measured best for the group solver with capped levels)
     WarpSmem wl{0, 0, 0};
     // row-sequential batched solver (apply_rs_kernel)
     int rs_mode = 0, rs_nw = 0, rs_meta_pad = 0, rs_ring_stride = 0, slot_stride = 1, rs_pf_rows = 8;
