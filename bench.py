@@ -33,6 +33,9 @@ if ROOT not in sys.path:
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+METRIC = "NKS time steps/s (fp64, 256^3 adaptive); Jacobian-matvec GDOF/s; % of HBM roofline"
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -209,10 +212,12 @@ def run_reference(args):
         if i >= min(args.warmup, 1):
             vals.append(r["value"])
     value = sum(vals) / len(vals)
-    line = {"metric": "NKS time steps/s (fp64, 256^3 adaptive)", "value": value, "unit": "time steps/s",
+    line = {"metric": METRIC, "value": value, "unit": "time steps/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args)},
+            "config": {"workload": workload_name(args), "grid": [args.n] * args.dim, "bc": "periodic",
+                       "ic": "u0=0.5+0.01U(-1,1), v0=0.01U(-1,1), seed 1234",
+                       "parallelism": f"host CPU, {threads} threads"},
             "cpu_baseline": {"value": value, "unit": "time steps/s", "cores": threads, "kind": "port",
                              "sample": r["sample"]},
             "e2e": {"value": value, "unit": "time steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -319,6 +324,7 @@ def run_ours(args):
         log(args, f"warmup step {stepper.step}: dt={dt:.4g} newton={nn} gmres={ng} "
                   f"retries={len(stepper.events)} {time.perf_counter() - t0:.2f}s")
 
+    first_timed = stepper.step + 1
     snap = stepper.snapshot()      # the e2e pass replays exactly these K steps
     ctx.profile(True)
     ctx.profile_read()
@@ -414,7 +420,7 @@ def run_ours(args):
     if rank == 0:
         value = args.steps / elapsed
         line = {
-            "metric": "NKS time steps/s (fp64, 256^3 adaptive); Jacobian-matvec GDOF/s; % of HBM roofline",
+            "metric": METRIC,
             "value": value, "unit": "time steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -423,7 +429,7 @@ def run_ours(args):
                        "parallelism": "1 GPU" if world == 1 else
                        f"z-slabs over {world} GPUs (2 ghost planes, halo + allreduce via NCCL)",
                        "l2": "every vector 268 MB > 126 MB L2 (no flush needed)",
-                       "steps_timed": f"accepted steps {stepper.step - args.steps - (args.steps if e2e else 0) + 1}.."},
+                       "steps_timed": f"accepted steps {first_timed}..{first_timed + args.steps - 1} (after {args.warmup} warm-up steps)"},
             "solver_stats": {"newton": newton_total, "gmres": gmres_total, "retries": retries,
                              "dt": [round(x, 6) for x in dts]},
             "roofline": roofline,
