@@ -377,6 +377,19 @@ __device__ __forceinline__ void ldg4_pred(double4 &v, const double4 *p, bool pre
                  : "l"(p), "r"((unsigned)pred), "l"(pol));
 }
 
+// fp32 copy of the factor blocks (opt-in mixed-precision storage, ACCH_FACTOR_F32=1):
+// one 128-bit load per block, widened exactly to fp64 at the FMA
+__device__ __forceinline__ void ldg4_pred(float4 &v, const float4 *p, bool pred, uint64_t pol)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
+                 "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %6;\n\t}"
+                 : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
+                 : "l"(p), "r"((unsigned)pred), "l"(pol));
+}
+__device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
+__device__ __forceinline__ int anchor_bits(const double4 &a) { return __double2hiint(a.x); }
+__device__ __forceinline__ int anchor_bits(const float4 &a) { return __float_as_int(a.x); }
+
 // acc -= a y for a 2x2 block, with the rounding pinned by intrinsics
 // (product, fused second product, subtraction): every solver and code path
 // gives bitwise the same result, whatever contraction the compiler would pick
@@ -384,6 +397,10 @@ __device__ __forceinline__ void blk_sub(double2 &acc, const double4 &a, const do
 {
     acc.x = __dsub_rn(acc.x, __fma_rn(a.y, y.y, __dmul_rn(a.x, y.x)));
     acc.y = __dsub_rn(acc.y, __fma_rn(a.w, y.y, __dmul_rn(a.z, y.x)));
+}
+__device__ __forceinline__ void blk_sub(double2 &acc, const float4 &a, const double2 &y)
+{
+    blk_sub(acc, make_double4(a.x, a.y, a.z, a.w), y);
 }
 
 template <int VARIANT, int TPS, int MAXW = 12>   // VARIANT: 0 asm, 1 ras-left, 2 ras-right
@@ -705,17 +722,17 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
 // load's result (masked by `zero`, a runtime 0 the compiler cannot fold), so
 // ptxas cannot start consuming loads 0..5 before it has issued loads 6..11 --
 // the interleaving that otherwise costs a second memory round trip per level.
-template <int MAXW, int DBG = 0>   // DBG (experiments only): 1 = no factor loads, 2 = no y dependency
-__device__ __forceinline__ void sweep_level(const double4 *__restrict__ A, const unsigned short *__restrict__ ecol,
+template <int MAXW, int DBG = 0, typename FT = double4>   // DBG (experiments only): 1 = no factor loads, 2 = no y dependency
+__device__ __forceinline__ void sweep_level(const FT *__restrict__ A, const unsigned short *__restrict__ ecol,
                                             const unsigned short *__restrict__ jo, double2 *y, int base, int m,
                                             int len0, int len1, int i0, int i1, bool backward, int lane, int zero,
                                             uint64_t pol)
 {
     // jo[t]: level-relative slot offset of diagonal t (jagged layout; shared
     // memory, warp-uniform), so lane q's slot t is base + jo[t] + q
-    double4 a[MAXW];
+    FT a[MAXW];
     int c[MAXW];
-    double4 d0, d1;
+    FT d0, d1;
     if (backward) {
         ldg4_pred(d0, A + base + lane, lane < m, pol);
         ldg4_pred(d1, A + base + lane + 32, lane + 32 < m, pol);
@@ -723,11 +740,11 @@ __device__ __forceinline__ void sweep_level(const double4 *__restrict__ A, const
 #pragma unroll
     for (int t = 0; t < MAXW; ++t) {
         const int e = base + jo[t] + lane;
-        if (DBG == 1) a[t] = make_double4(1e-3 * e, 1e-3, 2e-3, 1e-3 * t);
+        if constexpr (DBG == 1) a[t] = FT{1e-3 * e, 1e-3, 2e-3, 1e-3 * t};
         else ldg4_pred(a[t], A + e, t < len0, pol);
         c[t] = t < len0 ? ecol[e] : 0;
     }
-    const int dep = __double2hiint(a[MAXW - 1].x) & zero;
+    const int dep = anchor_bits(a[MAXW - 1]) & zero;
     double2 acc0 = y[i0 + dep], acc1 = y[i1];
     // (an all-products-first ordering -- bitwise the same result -- measured
     // 17% slower: it gathers y for inactive slots and lengthens the schedule)
@@ -786,12 +803,12 @@ __device__ __forceinline__ void sweep_level(const double4 *__restrict__ A, const
 }
 
 // one subdomain of a class group: gather, forward and backward sweeps, scatter
-template <int VARIANT, int MAXW, int DBG = 0>
+template <int VARIANT, int MAXW, int DBG = 0, typename FT = double4>
 __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev &C, const unsigned char *smem_meta,
                                              double2 *y, int s, const int4 *__restrict__ sub_origin,
                                              const long long *__restrict__ sub_off,
                                              const long long *__restrict__ sub_ext_off,
-                                             const double4 *__restrict__ vals, const double2 *__restrict__ r,
+                                             const FT *__restrict__ vals, const double2 *__restrict__ r,
                                              double2 *__restrict__ z, double2 *__restrict__ ext_out, int zero, int pd)
 {
     const int lane = threadIdx.x & 31;
@@ -812,7 +829,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     const uint64_t pol = evict_first_policy();
     const int4 o = sub_origin[s];
     const long long obase = cell_at(g, o.x, o.y, zplane(g, o.z));   // used when o.w (no wrap)
-    const double4 *__restrict__ A = vals + sub_off[s];
+    const FT *__restrict__ A = vals + sub_off[s];
     const int nall = nlev + nlevb;
     auto prefetch_level = [&](int k) {
         if (k >= nall) return;
@@ -825,7 +842,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
             lo = b_bs[kb];
             hi = kb + 1 < nlevb ? b_bs[kb + 1] : ell_total;
         }
-        prefetch_l2(A + lo, (unsigned)(hi - lo) * 32u);
+        prefetch_l2(A + lo, (unsigned)((hi - lo) * sizeof(FT)));
     };
     if (lane < pd) prefetch_level(lane);
     // gather r into y with many independent loads in flight per lane; the
@@ -874,7 +891,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         const int len1 = lane + 32 < m ? f_len[r0 + lane + 32] : 0;
         const int i0 = lane < m ? f_rows[r0 + lane] : 0;
         const int i1 = lane + 32 < m ? f_rows[r0 + lane + 32] : 0;
-        sweep_level<MAXW, DBG>(A, ecol, f_jo + f_jp[lev], y, f_bs[lev], m, len0, len1, i0, i1, false, lane, zero, pol);
+        sweep_level<MAXW, DBG, FT>(A, ecol, f_jo + f_jp[lev], y, f_bs[lev], m, len0, len1, i0, i1, false, lane, zero, pol);
     }
     for (int lev = 0; lev < nlevb; ++lev) {
         if (lane == 0) prefetch_level(nlev + lev + pd);
@@ -884,7 +901,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         const int len1 = lane + 32 < m ? b_len[r0 + lane + 32] - 1 : 0;
         const int i0 = lane < m ? b_rows[r0 + lane] : 0;
         const int i1 = lane + 32 < m ? b_rows[r0 + lane + 32] : 0;
-        sweep_level<MAXW, DBG>(A, ecol, b_jo + b_jp[lev] + 1, y, b_bs[lev], m, len0, len1, i0, i1, true, lane, zero,
+        sweep_level<MAXW, DBG, FT>(A, ecol, b_jo + b_jp[lev] + 1, y, b_bs[lev], m, len0, len1, i0, i1, true, lane, zero,
                           pol);
     }
     if (VARIANT == 1) {
@@ -900,12 +917,12 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     __syncwarp();   // y is reused by the warp's next subdomain
 }
 
-template <int VARIANT, int NW, int MAXW = 12, int DBG = 0>
+template <int VARIANT, int NW, int MAXW = 12, int DBG = 0, typename FT = double4>
 __global__ void __launch_bounds__(NW * 32, 1)
 apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *__restrict__ groups,
                    const int *__restrict__ grp_sub, const int4 *__restrict__ sub_origin,
                    const long long *__restrict__ sub_off, const long long *__restrict__ sub_ext_off,
-                   const double4 *__restrict__ vals, const double2 *__restrict__ r, double2 *__restrict__ z,
+                   const FT *__restrict__ vals, const double2 *__restrict__ r, double2 *__restrict__ z,
                    double2 *__restrict__ ext_out, int meta_max, int y_stride, int zero, int pd)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -922,7 +939,7 @@ apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *
     // one subdomain per warp (a loop over several per warp measured slower:
     // it pushes the sweep past 255 registers into spills)
     if (warp < G.z)
-        group_solve_one<VARIANT, MAXW, DBG>(g, C, smem_raw, y, grp_sub[G.y + warp], sub_origin, sub_off,
+        group_solve_one<VARIANT, MAXW, DBG, FT>(g, C, smem_raw, y, grp_sub[G.y + warp], sub_origin, sub_off,
                                            sub_ext_off, vals, r, z, ext_out, zero, pd);
 }
 
@@ -2079,6 +2096,8 @@ struct acch_precond {
     int4 *d_sub_origin = nullptr;
     long long *d_sub_off = nullptr, *d_sub_ext_off = nullptr;
     double4 *d_vals = nullptr;
+    float4 *d_vals32 = nullptr;   // opt-in fp32 copy of the factors for the group solver (ACCH_FACTOR_F32=1)
+    int f32 = 0;
     long long total_blocks = 0, total_ext = 0, total_nnzb = 0;
     int *d_bad = nullptr;
     double2 *d_ext_out = nullptr;
@@ -2134,6 +2153,7 @@ static void free_precond(acch_precond *pc)
     cudaFree(pc->d_sub_off);
     cudaFree(pc->d_sub_ext_off);
     cudaFree(pc->d_vals);
+    cudaFree(pc->d_vals32);
     cudaFree(pc->d_bad);
     cudaFree(pc->d_ext_out);
     cudaFree(pc->d_cell_ptr);
@@ -2566,6 +2586,14 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 1>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 2>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 8, 12, 0, float4>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 0, float4>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 8, 12, 0, float4>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4, 12, 0, float4>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4, 12, 0, float4>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4, 12, 0, float4>, attr, b));
+            if (const char *e = getenv("ACCH_FACTOR_F32")) pc->f32 = atoi(e) != 0;
+            if (pc->f32) PC_CUDA(cudaMalloc(&pc->d_vals32, sizeof(float4) * std::max<long long>(1, pc->total_blocks)));
             if (const char *e = getenv("ACCH_APPLY_DBG")) pc->dbg = atoi(e);
         }
         if (getenv("ACCH_DEBUG"))
@@ -2618,6 +2646,17 @@ extern "C" acch_status acch_precond_invalidate(acch_precond *pc)
     }
     pc->have_factors = false;
     return ACCH_OK;
+}
+
+// fp32 storage copy of the fp64 factors (round to nearest), read by the
+// group solver when ACCH_FACTOR_F32=1; the factorisation itself stays fp64
+__global__ void factors_to_f32_kernel(const double4 *__restrict__ src, float4 *__restrict__ dst, long long n)
+{
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const double4 a = src[i];
+        dst[i] = make_float4(__double2float_rn(a.x), __double2float_rn(a.y), __double2float_rn(a.z),
+                             __double2float_rn(a.w));
+    }
 }
 
 extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef, double dt, int32_t reuse,
@@ -2679,6 +2718,10 @@ extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef,
             return ACCH_ERR_ZERO_PIVOT;
         }
     }
+    if (pc->f32) {
+        factors_to_f32_kernel<<<148 * 8, 256, 0, ctx->stream>>>(pc->d_vals, pc->d_vals32, pc->total_blocks);
+        ACCH_LAUNCHED(ctx);
+    }
     pc->have_factors = true;
     if (refactored) *refactored = 1;
     return ACCH_OK;
@@ -2704,9 +2747,13 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
         (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub)
 #define GAPPLY_W(V, NW)                                                                                       \
-    apply_group_kernel<V, NW><<<(unsigned)pc->groups.size(), NW * 32, pc->group_smem, ctx->stream>>>(ctx->g,         \
+    do { if (pc->f32) apply_group_kernel<V, NW, 12, 0, float4><<<(unsigned)pc->groups.size(), NW * 32, pc->group_smem,     \
+        ctx->stream>>>(ctx->g, pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off,          \
+        pc->d_sub_ext_off, pc->d_vals32, (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride,\
+        0, pc->pf_depth);                                                                                         \
+    else apply_group_kernel<V, NW><<<(unsigned)pc->groups.size(), NW * 32, pc->group_smem, ctx->stream>>>(ctx->g,         \
         pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, \
-        (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride, 0, pc->pf_depth)
+        (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride, 0, pc->pf_depth); } while (0)
 #define GAPPLY_DBG(D)                                                                                          \
     apply_group_kernel<1, 8, 12, D><<<(unsigned)pc->groups.size(), 256, pc->group_smem, ctx->stream>>>(ctx->g,      \
         pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, \

@@ -457,3 +457,48 @@ def test_warp_factorisation_bitwise_equal_cta_factorisation(solver, bc, monkeypa
         pre.update(J)
         outs[mode] = host(pre.apply(r))
     assert np.array_equal(outs["1"], outs["0"])
+
+
+# --------------------------------------------------------------------------- fp32 factor storage (opt-in)
+
+@pytest.mark.parametrize("variant", [SchwarzVariant.LEFT_RAS, SchwarzVariant.RIGHT_RAS])
+def test_group_solver_fp32_factor_storage_close_to_fp64(variant, monkeypatch):
+    """ACCH_FACTOR_F32=1 keeps the fp64 factorisation but lets the group
+    solver read an fp32 copy of the factors (half the apply's bytes).  The
+    preconditioner changes by the rounding of the stored blocks only."""
+    rng = np.random.default_rng(5)
+    counts = (24, 24, 24)
+    g = Grid(counts, (1.0, 1.0, 1.0), BoundaryCondition.PERIODIC)
+    uo, vo = 0.5 + rng.uniform(-0.05, 0.05, g.array_shape), rng.uniform(-0.05, 0.05, g.array_shape)
+    un, vn = uo + rng.uniform(-0.01, 0.01, g.array_shape), vo + rng.uniform(-0.01, 0.01, g.array_shape)
+    prob = StepProblem.create(g, PARAMS, st(g, uo, vo), 1e-3)
+    J = assemble_jacobian(prob, st(g, un, vn))
+    r = torch.tensor(rng.standard_normal(2 * g.n_cells), device=DEV)
+    outs = {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("ACCH_FACTOR_F32", mode)
+        pre = SchwarzPreconditioner(partition(g, 27, 1), variant, SubdomainSolverSpec.from_string("ilu0"))
+        pre.update(J)
+        outs[mode] = host(pre.apply(r))
+    rel = np.max(np.abs(outs["1"] - outs["0"])) / np.max(np.abs(outs["0"]))
+    print(f"fp32-storage apply rel diff {rel:.3e}")
+    assert 0.0 < rel <= 1e-4
+
+
+def test_simulate_fp32_factor_storage_matches_reference(monkeypatch):
+    """The adaptive 3D Neumann history with fp32 factor storage: the same
+    accepted dt sequence and Newton counts, fields within 1e-8 of the
+    reference (GMRES counts may differ: the preconditioner is not bitwise)."""
+    monkeypatch.setenv("ACCH_FACTOR_F32", "1")
+    z, g, res = _run_sim("c3small", "dcgs2")
+    ref = z["rows"]
+    assert res.status == str(z["status"])
+    got = np.array([[r.step, r.time, r.dt, r.energy, r.mass_u, r.max_abs_v, r.newton, r.gmres]
+                    for r in res.history])
+    assert got.shape == ref.shape
+    np.testing.assert_allclose(got[:, 2], ref[:, 2], rtol=1e-8)
+    np.testing.assert_array_equal(got[:, 6], ref[:, 6])
+    u, v = res.final_state.to_numpy()
+    err = np.sqrt(np.sum((u - z["u"]) ** 2 + (v - z["v"]) ** 2) / np.sum(z["u"] ** 2 + z["v"] ** 2))
+    print(f"fp32-storage fields rel L2 {err:.3e}; gmres {got[:, 7].tolist()} vs {ref[:, 7].tolist()}")
+    assert err <= 1e-8
