@@ -245,6 +245,22 @@ def measured_traffic(category):
     return sum(v["traffic_bytes"] for v in ent), "ncu --set full: " + ", ".join(v["source"] for v in ent)
 
 
+def measured_issue(category):
+    """Instruction-issue evidence for a compute-heavy kernel from the committed
+    `ncu --set full` capture (profiles/traffic.json): warp instructions per
+    launch, FP64-pipe and issue-slot utilisation.  The residual is bound by
+    FP64 issue, not HBM, so its roofline is stated in both."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(path):
+        return None
+    ent = [v for v in json.load(open(path)).values() if v.get("category") == category and "inst_executed" in v]
+    if not ent:
+        return None
+    e = ent[0]
+    return {"warp_inst_per_launch": e["inst_executed"], "fp64_pipe_pct": e.get("fp64_pipe_pct"),
+            "issue_active_pct": e.get("issue_active_pct"), "source": "ncu --set full: " + e["source"]}
+
+
 def microbench_stencils(args, stepper, peaks, reps=20):
     """Standalone residual and Jacobian-matvec launches at the current state
     (U' = U^n + 1e-4 N(0,1): the chords take the series branch)."""
@@ -281,6 +297,13 @@ def microbench_stencils(args, stepper, peaks, reps=20):
         gbs = nbytes / t / 1e9
         out[name] = {"ms": t * 1e3, "gdof_s": n2 / t / 1e9, "gb_s": gbs, "frac": gbs / peaks["hbm_gbs"],
                      "alg_bytes": nbytes}
+        iss = measured_issue(name)
+        if iss is not None:
+            # issue roofline: 148 SMs x 4 schedulers x 1 warp instruction per clock
+            clk = float(os.environ.get("ACCH_SM_MHZ", "1965")) * 1e6
+            t_issue = iss["warp_inst_per_launch"] / (148 * 4 * clk)
+            iss.update({"issue_bound_ms": t_issue * 1e3, "issue_frac": t_issue / t, "clock_mhz_assumed": clk / 1e6})
+            out[name]["issue"] = iss
     return out
 
 

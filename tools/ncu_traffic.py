@@ -37,4 +37,16 @@ for path in sys.argv[1:]:
         ms = float(r[col["gpu__time_duration.sum"]].replace(",", "")) * {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "s": 1e3}[tu]
         out[name] = {"category": CATEGORY.get(base), "dram_read_bytes": rd, "dram_write_bytes": wr,
                      "traffic_bytes": rd + wr, "duration_ms": ms, "source": path.split("/")[-1]}
+
+        def opt(key):
+            try:
+                return float(r[col[key]].replace(",", ""))
+            except (KeyError, ValueError):
+                return None
+        for k, key in (("inst_executed", "smsp__inst_executed.sum"),
+                       ("fp64_pipe_pct", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                       ("issue_active_pct", "sm__inst_issued.avg.pct_of_peak_sustained_active")):
+            v = opt(key)
+            if v is not None:
+                out[name][k] = v
 print(json.dumps(out, indent=1))
