@@ -802,8 +802,63 @@ __device__ __forceinline__ void sweep_level(const FT *__restrict__ A, const unsi
     __syncwarp();
 }
 
+// A level of at most kWideRows rows whose longest row has more than kWideLen
+// blocks (exact LU / high fill: the factor's levels shrink to single rows of
+// 30-80 blocks): the whole warp works on one row at a time -- lane l takes
+// blocks l, l + 32, ... (all loads in flight at once), then a shuffle tree
+// sums the partial products.  One memory round trip per row instead of one
+// per 4-block batch of a single lane.  (ILU(0) rows never exceed 21 blocks,
+// so the ILU(0) sweeps -- and their bitwise agreement across solvers -- are
+// untouched.)
+constexpr int kWideRows = 4, kWideLen = 32;
+
+template <typename FT>
+__device__ __forceinline__ void sweep_rows_wide(const FT *__restrict__ A, const unsigned short *__restrict__ ecol,
+                                                const unsigned short *__restrict__ jo,
+                                                const unsigned short *__restrict__ rows,
+                                                const unsigned short *__restrict__ lens, double2 *y, int base,
+                                                int m, bool backward, int lane, uint64_t pol)
+{
+    for (int q = 0; q < m; ++q) {
+        const int len = lens[q] - (backward ? 1 : 0);
+        const int i = rows[q];
+        double2 acc = make_double2(0.0, 0.0);
+        for (int t0 = 0; t0 < len; t0 += 4 * 32) {
+            FT a[4];
+            int c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + u * 32 + lane;
+                const int e = base + jo[t < len ? t : 0] + q;
+                ldg4_pred(a[u], A + e, t < len, pol);
+                c[u] = t < len ? ecol[e] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (t0 + u * 32 + lane < len) blk_sub(acc, a[u], y[c[u]]);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+        }
+        if (lane == 0) {
+            double2 v = y[i];
+            v.x += acc.x;
+            v.y += acc.y;
+            if (backward) {
+                FT d;
+                ldg4_pred(d, A + base + q, true, pol);
+                v = make_double2(d.x * v.x + d.y * v.y, d.z * v.x + d.w * v.y);
+            }
+            y[i] = v;
+        }
+        __syncwarp();
+    }
+}
+
 // one subdomain of a class group: gather, forward and backward sweeps, scatter
-template <int VARIANT, int MAXW, int DBG = 0, typename FT = double4>
+template <int VARIANT, int MAXW, int DBG = 0, typename FT = double4, bool WIDE = false>
 __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev &C, const unsigned char *smem_meta,
                                              double2 *y, int s, const int4 *__restrict__ sub_origin,
                                              const long long *__restrict__ sub_off,
@@ -887,6 +942,11 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     for (int lev = 0; lev < nlev; ++lev) {
         if (lane == 0) prefetch_level(lev + pd);
         const int r0 = f_ptr[lev], m = f_ptr[lev + 1] - r0;
+        if (WIDE && m <= kWideRows && f_len[r0] > kWideLen) {
+            sweep_rows_wide<FT>(A, ecol, f_jo + f_jp[lev], f_rows + r0, f_len + r0, y, f_bs[lev], m, false, lane,
+                                pol);
+            continue;
+        }
         const int len0 = lane < m ? f_len[r0 + lane] : 0;
         const int len1 = lane + 32 < m ? f_len[r0 + lane + 32] : 0;
         const int i0 = lane < m ? f_rows[r0 + lane] : 0;
@@ -896,6 +956,11 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     for (int lev = 0; lev < nlevb; ++lev) {
         if (lane == 0) prefetch_level(nlev + lev + pd);
         const int r0 = b_ptr[lev], m = b_ptr[lev + 1] - r0;
+        if (WIDE && m <= kWideRows && b_len[r0] > kWideLen + 1) {
+            sweep_rows_wide<FT>(A, ecol, b_jo + b_jp[lev] + 1, b_rows + r0, b_len + r0, y, b_bs[lev], m, true, lane,
+                                pol);
+            continue;
+        }
         // slot 0 of every backward row is its inverted diagonal block; U slots follow
         const int len0 = lane < m ? b_len[r0 + lane] - 1 : 0;
         const int len1 = lane + 32 < m ? b_len[r0 + lane + 32] - 1 : 0;
@@ -917,7 +982,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     __syncwarp();   // y is reused by the warp's next subdomain
 }
 
-template <int VARIANT, int NW, int MAXW = 12, int DBG = 0, typename FT = double4>
+template <int VARIANT, int NW, int MAXW = 12, int DBG = 0, typename FT = double4, bool WIDE = false>
 __global__ void __launch_bounds__(NW * 32, 1)
 apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *__restrict__ groups,
                    const int *__restrict__ grp_sub, const int4 *__restrict__ sub_origin,
@@ -939,7 +1004,7 @@ apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *
     // one subdomain per warp (a loop over several per warp measured slower:
     // it pushes the sweep past 255 registers into spills)
     if (warp < G.z)
-        group_solve_one<VARIANT, MAXW, DBG, FT>(g, C, smem_raw, y, grp_sub[G.y + warp], sub_origin, sub_off,
+        group_solve_one<VARIANT, MAXW, DBG, FT, WIDE>(g, C, smem_raw, y, grp_sub[G.y + warp], sub_origin, sub_off,
                                            sub_ext_off, vals, r, z, ext_out, zero, pd);
 }
 
@@ -2096,6 +2161,7 @@ struct acch_precond {
     int4 *d_sub_origin = nullptr;
     long long *d_sub_off = nullptr, *d_sub_ext_off = nullptr;
     double4 *d_vals = nullptr;
+    int wide = 0;                 // some factor row exceeds kWideLen blocks (LU / high fill): warp-wide rows
     float4 *d_vals32 = nullptr;   // opt-in fp32 copy of the factors for the group solver (ACCH_FACTOR_F32=1)
     int f32 = 0;
     long long total_blocks = 0, total_ext = 0, total_nnzb = 0;
@@ -2592,6 +2658,17 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4, 12, 0, float4>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4, 12, 0, float4>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4, 12, 0, float4>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 8, 12, 0, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 0, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 8, 12, 0, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4, 12, 0, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4, 12, 0, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4, 12, 0, double4, true>, attr, b));
+            for (const auto &C : pc->classes) {
+                for (int v : C.f_len) pc->wide |= v > kWideLen;
+                for (int v : C.b_len) pc->wide |= v > kWideLen + 1;
+            }
+            if (const char *e = getenv("ACCH_WIDE_ROWS")) pc->wide = pc->wide && atoi(e) != 0;
             if (const char *e = getenv("ACCH_FACTOR_F32")) pc->f32 = atoi(e) != 0;
             if (pc->f32) PC_CUDA(cudaMalloc(&pc->d_vals32, sizeof(float4) * std::max<long long>(1, pc->total_blocks)));
             if (const char *e = getenv("ACCH_APPLY_DBG")) pc->dbg = atoi(e);
@@ -2747,7 +2824,11 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
         (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub)
 #define GAPPLY_W(V, NW)                                                                                       \
-    do { if (pc->f32) apply_group_kernel<V, NW, 12, 0, float4><<<(unsigned)pc->groups.size(), NW * 32, pc->group_smem,     \
+    do { if (pc->wide && !pc->f32) apply_group_kernel<V, NW, 12, 0, double4, true><<<(unsigned)pc->groups.size(),    \
+        NW * 32, pc->group_smem, ctx->stream>>>(ctx->g, pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, \
+        pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max,  \
+        pc->y_stride, 0, pc->pf_depth);                                                                           \
+    else if (pc->f32) apply_group_kernel<V, NW, 12, 0, float4><<<(unsigned)pc->groups.size(), NW * 32, pc->group_smem,     \
         ctx->stream>>>(ctx->g, pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off,          \
         pc->d_sub_ext_off, pc->d_vals32, (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride,\
         0, pc->pf_depth);                                                                                         \

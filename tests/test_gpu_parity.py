@@ -502,3 +502,37 @@ def test_simulate_fp32_factor_storage_matches_reference(monkeypatch):
     err = np.sqrt(np.sum((u - z["u"]) ** 2 + (v - z["v"]) ** 2) / np.sum(z["u"] ** 2 + z["v"] ** 2))
     print(f"fp32-storage fields rel L2 {err:.3e}; gmres {got[:, 7].tolist()} vs {ref[:, 7].tolist()}")
     assert err <= 1e-8
+
+
+# --------------------------------------------------------------------------- warp-wide rows (exact LU)
+
+@pytest.mark.parametrize("bc", [BoundaryCondition.PERIODIC, BoundaryCondition.NEUMANN])
+def test_lu_wide_rows_match_oracle(bc, monkeypatch):
+    """Exact LU on 18x18-cell extended boxes (config 2's box shape): the
+    factor's levels are single rows of up to ~40 blocks, which the group solver sweeps warp-wide (one
+    memory round trip per row).  Against the oracle's LU and against the
+    lane-per-row sweep (ACCH_WIDE_ROWS=0)."""
+    from oracle import acch_oracle as O
+    rng = np.random.default_rng(11)
+    counts = (64, 64)
+    g = Grid(counts, (1.0, 1.0), bc)
+    uo, vo = 0.5 + rng.uniform(-0.05, 0.05, g.array_shape), rng.uniform(-0.05, 0.05, g.array_shape)
+    un, vn = uo + rng.uniform(-0.01, 0.01, g.array_shape), vo + rng.uniform(-0.01, 0.01, g.array_shape)
+    prob = StepProblem.create(g, PARAMS, st(g, uo, vo), 1e-3)
+    J = assemble_jacobian(prob, st(g, un, vn))
+    r = torch.tensor(rng.standard_normal(2 * g.n_cells), device=DEV)
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ACCH_WIDE_ROWS", mode)
+        pre = SchwarzPreconditioner(partition(g, 16, 1), SchwarzVariant.LEFT_RAS,
+                                    SubdomainSolverSpec.from_string("lu"))
+        pre.update(J)
+        outs[mode] = host(pre.apply(r))
+    m = O.Mesh(counts, (1.0, 1.0), bc == BoundaryCondition.PERIODIC)
+    Jo = O.Step(m, O.Coeffs(), uo, vo, 1e-3).jacobian(O.pack(un, vn)).assemble_fast()
+    po = O.SchwarzOracle(O.decompose(m, 16, 1), "ras-left", "lu")
+    po.update(Jo)
+    ref = po.apply(host(r))
+    scale = np.max(np.abs(ref))
+    assert np.max(np.abs(outs["1"] - ref)) <= 1e-10 * scale
+    assert np.max(np.abs(outs["1"] - outs["0"])) <= 1e-12 * scale
