@@ -377,6 +377,10 @@ __device__ __forceinline__ void ldg4_pred(double4 &v, const double4 *p, bool pre
                  : "l"(p), "r"((unsigned)pred), "l"(pol));
 }
 
+// levels of at most kWideRows rows whose longest row exceeds kWideLen blocks
+// are swept warp-wide (sweep_rows_wide*, exact LU / high fill)
+constexpr int kWideRows = 4, kWideLen = 32;
+
 // fp32 copy of the factor blocks (opt-in mixed-precision storage, ACCH_FACTOR_F32=1):
 // one 128-bit load per block, widened exactly to fp64 at the FMA
 __device__ __forceinline__ void ldg4_pred(float4 &v, const float4 *p, bool pred, uint64_t pol)
@@ -522,7 +526,60 @@ struct WarpSmem {
     }
 };
 
-template <int VARIANT, int MAXW = 12, int PREFETCH_DEPTH = 4>
+// Warp-wide sweep of a narrow level (<= 4 rows) with long rows in the
+// ballot-offset layout of apply_warp_kernel: slot (t, q) = base + first +
+// sum_q' min(len_q', t) + q, rows sorted by decreasing length (see
+// sweep_rows_wide for the group solver's table-offset layout).
+__device__ __forceinline__ void sweep_rows_wide_warp(const double4 *__restrict__ A,
+                                                     const int *__restrict__ ecol,
+                                                     const unsigned short *__restrict__ rows,
+                                                     const unsigned short *__restrict__ lens, double2 *y, int base,
+                                                     int m, bool backward, int lane)
+{
+    int L[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) L[q] = q < m ? lens[q] - (backward ? 1 : 0) : 0;
+    const int first = backward ? m : 0;
+    for (int q = 0; q < m; ++q) {
+        const int len = L[q];
+        const int i = rows[q];
+        double2 acc = make_double2(0.0, 0.0);
+        for (int t0 = 0; t0 < len; t0 += 4 * 32) {
+            double4 a[4];
+            int c[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + u * 32 + lane;
+                if (t < len) {
+                    const int e = base + first + min(L[0], t) + min(L[1], t) + min(L[2], t) + min(L[3], t) + q;
+                    a[u] = ldg4(A + e);
+                    c[u] = __ldg(ecol + e);
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (t0 + u * 32 + lane < len) blk_sub(acc, a[u], y[c[u]]);
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+        }
+        if (lane == 0) {
+            double2 v = y[i];
+            v.x += acc.x;
+            v.y += acc.y;
+            if (backward) {
+                const double4 d = ldg4(A + base + q);
+                v = make_double2(d.x * v.x + d.y * v.y, d.z * v.x + d.w * v.y);
+            }
+            y[i] = v;
+        }
+        __syncwarp();
+    }
+}
+
+template <int VARIANT, int MAXW = 12, int PREFETCH_DEPTH = 4, bool WIDE = false>
 __global__ void __launch_bounds__(32, 8)
 apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
                   const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
@@ -595,6 +652,10 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     for (int lev = 0; lev < C.nlev; ++lev) {
         if (lane == 0) prefetch_level(lev + PREFETCH_DEPTH);
         const int r0 = f_ptr[lev], m = f_ptr[lev + 1] - r0, base = f_bs[lev];
+        if (WIDE && m <= kWideRows && f_len[r0] > kWideLen) {
+            sweep_rows_wide_warp(A, C.ecol, f_rows + r0, f_len + r0, y, base, m, false, lane);
+            continue;
+        }
         const int len0 = lane < m ? f_len[r0 + lane] : 0;
         const int len1 = lane + 32 < m ? f_len[r0 + lane + 32] : 0;
         const int i0 = lane < m ? f_rows[r0 + lane] : 0;
@@ -641,6 +702,10 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     for (int lev = 0; lev < C.nlevb; ++lev) {
         if (lane == 0) prefetch_level(C.nlev + lev + PREFETCH_DEPTH);
         const int r0 = b_ptr[lev], m = b_ptr[lev + 1] - r0, base = b_bs[lev];
+        if (WIDE && m <= kWideRows && b_len[r0] > kWideLen + 1) {
+            sweep_rows_wide_warp(A, C.ecol, b_rows + r0, b_len + r0, y, base, m, true, lane);
+            continue;
+        }
         // slot 0 of every row: the inverted diagonal block; U slots follow
         const int len0 = lane < m ? b_len[r0 + lane] - 1 : 0;
         const int len1 = lane + 32 < m ? b_len[r0 + lane + 32] - 1 : 0;
@@ -810,7 +875,6 @@ __device__ __forceinline__ void sweep_level(const FT *__restrict__ A, const unsi
 // per 4-block batch of a single lane.  (ILU(0) rows never exceed 21 blocks,
 // so the ILU(0) sweeps -- and their bitwise agreement across solvers -- are
 // untouched.)
-constexpr int kWideRows = 4, kWideLen = 32;
 
 template <typename FT>
 __device__ __forceinline__ void sweep_rows_wide(const FT *__restrict__ A, const unsigned short *__restrict__ ecol,
@@ -2424,6 +2488,8 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             for (int v : C.f_len) max_len = std::max(max_len, v);
             for (int v : C.b_len) max_len = std::max(max_len, v - 1);
         }
+        pc->wide = max_len > kWideLen;   // exact LU / high fill: warp-wide sweeps of narrow levels
+        if (const char *e = getenv("ACCH_WIDE_ROWS")) pc->wide = pc->wide && atoi(e) != 0;
         pc->warp_mode = (max_width <= 64 && max_nloc <= 65535 && pc->wl.bytes() <= 200 * 1024) ? 1 : 0;
         if (const char *e = getenv("ACCH_PREFETCH_DEPTH")) pc->pf_depth = atoi(e);
         if (const char *e = getenv("ACCH_SCHWARZ_BLOCK_SOLVER"))   // testing: force the CTA-wide solver
@@ -2576,14 +2642,23 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         // the solvers live on shared memory: ask for the full L1/shared carveout
         const auto co = cudaFuncAttributePreferredSharedMemoryCarveout;
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 4>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 4, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 4>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 4, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 8>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 8, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 8>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 8, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 8>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 8, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 16>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 16, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<0>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<1>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<2>, co, 100));
@@ -2598,14 +2673,23 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         const int b = smem_optin();   // per-function state: never lower it under another live preconditioner
         const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4, true>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 4>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 4, true>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 4>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 4, true>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 8>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 8, true>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 8>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 8, true>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 8>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 8, true>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 16>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 16, true>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16, true>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16, true>, attr, b));
     }
     {
         // class-group solver: NW subdomains of one class per CTA sharing the
@@ -2664,11 +2748,6 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4, 12, 0, double4, true>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4, 12, 0, double4, true>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4, 12, 0, double4, true>, attr, b));
-            for (const auto &C : pc->classes) {
-                for (int v : C.f_len) pc->wide |= v > kWideLen;
-                for (int v : C.b_len) pc->wide |= v > kWideLen + 1;
-            }
-            if (const char *e = getenv("ACCH_WIDE_ROWS")) pc->wide = pc->wide && atoi(e) != 0;
             if (const char *e = getenv("ACCH_FACTOR_F32")) pc->f32 = atoi(e) != 0;
             if (pc->f32) PC_CUDA(cudaMalloc(&pc->d_vals32, sizeof(float4) * std::max<long long>(1, pc->total_blocks)));
             if (const char *e = getenv("ACCH_APPLY_DBG")) pc->dbg = atoi(e);
@@ -2820,9 +2899,12 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r, (double2 *)z, pc->d_ext_out,      \
         pc->use_smem, pc->max_nloc, pc->nsub)
 #define WAPPLY_D(V, D)                                                                                        \
-    apply_warp_kernel<V, 12, D><<<(unsigned)pc->nsub, 32, pc->wl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,    \
+    do { if (pc->wide) apply_warp_kernel<V, 12, D, true><<<(unsigned)pc->nsub, 32, pc->wl.bytes(), ctx->stream>>>(ctx->g, \
+        pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals,            \
+        (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub);                                     \
+    else apply_warp_kernel<V, 12, D><<<(unsigned)pc->nsub, 32, pc->wl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,    \
         pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
-        (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub)
+        (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub); } while (0)
 #define GAPPLY_W(V, NW)                                                                                       \
     do { if (pc->wide && !pc->f32) apply_group_kernel<V, NW, 12, 0, double4, true><<<(unsigned)pc->groups.size(),    \
         NW * 32, pc->group_smem, ctx->stream>>>(ctx->g, pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, \

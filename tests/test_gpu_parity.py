@@ -506,8 +506,9 @@ def test_simulate_fp32_factor_storage_matches_reference(monkeypatch):
 
 # --------------------------------------------------------------------------- warp-wide rows (exact LU)
 
+@pytest.mark.parametrize("solver_mode", ["1", "0"])   # ACCH_GROUP: class-group solver / warp solver
 @pytest.mark.parametrize("bc", [BoundaryCondition.PERIODIC, BoundaryCondition.NEUMANN])
-def test_lu_wide_rows_match_oracle(bc, monkeypatch):
+def test_lu_wide_rows_match_oracle(bc, solver_mode, monkeypatch):
     """Exact LU on 18x18-cell extended boxes (config 2's box shape): the
     factor's levels are single rows of up to ~40 blocks, which the group solver sweeps warp-wide (one
     memory round trip per row).  Against the oracle's LU and against the
@@ -521,6 +522,7 @@ def test_lu_wide_rows_match_oracle(bc, monkeypatch):
     prob = StepProblem.create(g, PARAMS, st(g, uo, vo), 1e-3)
     J = assemble_jacobian(prob, st(g, un, vn))
     r = torch.tensor(rng.standard_normal(2 * g.n_cells), device=DEV)
+    monkeypatch.setenv("ACCH_GROUP", solver_mode)
     outs = {}
     for mode in ("1", "0"):
         monkeypatch.setenv("ACCH_WIDE_ROWS", mode)
@@ -531,6 +533,38 @@ def test_lu_wide_rows_match_oracle(bc, monkeypatch):
     m = O.Mesh(counts, (1.0, 1.0), bc == BoundaryCondition.PERIODIC)
     Jo = O.Step(m, O.Coeffs(), uo, vo, 1e-3).jacobian(O.pack(un, vn)).assemble_fast()
     po = O.SchwarzOracle(O.decompose(m, 16, 1), "ras-left", "lu")
+    po.update(Jo)
+    ref = po.apply(host(r))
+    scale = np.max(np.abs(ref))
+    assert np.max(np.abs(outs["1"] - ref)) <= 1e-10 * scale
+    assert np.max(np.abs(outs["1"] - outs["0"])) <= 1e-12 * scale
+
+
+@pytest.mark.parametrize("solver_mode", ["1", "0"])   # ACCH_GROUP: class-group solver / warp solver
+@pytest.mark.parametrize("variant", [SchwarzVariant.LEFT_RAS, SchwarzVariant.RIGHT_RAS])
+def test_ilu2_wide_rows_3d_match_oracle(variant, solver_mode, monkeypatch):
+    """ILU(2) on 8^3-cell boxes of a 16^3 Neumann grid (config 3's solver):
+    factor rows of up to ~90 blocks in levels of <= 4 rows, swept warp-wide
+    by the warp solver (the class image is too large for the group solver)."""
+    from oracle import acch_oracle as O
+    rng = np.random.default_rng(12)
+    counts = (16, 16, 16)
+    g = Grid(counts, (1.0, 1.0, 1.0), BoundaryCondition.NEUMANN)
+    uo, vo = 0.5 + rng.uniform(-0.05, 0.05, g.array_shape), rng.uniform(-0.05, 0.05, g.array_shape)
+    un, vn = uo + rng.uniform(-0.01, 0.01, g.array_shape), vo + rng.uniform(-0.01, 0.01, g.array_shape)
+    prob = StepProblem.create(g, PARAMS, st(g, uo, vo), 1e-3)
+    J = assemble_jacobian(prob, st(g, un, vn))
+    r = torch.tensor(rng.standard_normal(2 * g.n_cells), device=DEV)
+    monkeypatch.setenv("ACCH_GROUP", solver_mode)
+    outs = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("ACCH_WIDE_ROWS", mode)
+        pre = SchwarzPreconditioner(partition(g, 8, 1), variant, SubdomainSolverSpec.from_string("ilu2"))
+        pre.update(J)
+        outs[mode] = host(pre.apply(r))
+    m = O.Mesh(counts, (1.0, 1.0, 1.0), False)
+    Jo = O.Step(m, O.Coeffs(), uo, vo, 1e-3).jacobian(O.pack(un, vn)).assemble_fast()
+    po = O.SchwarzOracle(O.decompose(m, 8, 1), variant.value, "ilu2")
     po.update(Jo)
     ref = po.apply(host(r))
     scale = np.max(np.abs(ref))
