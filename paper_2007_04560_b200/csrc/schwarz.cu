@@ -178,8 +178,62 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
         }
     }
     __syncthreads();
+    // diagonal block of a finished row: scalar pivots as the reference's
+    // factor_inplace sees them, then the inverted block
+    auto finish_diag = [&](int i, int d) {
+        const int pd = C.pos[d];
+        const double4 D = A[pd];
+        const double p0 = D.x;
+        const double p1 = D.w - (D.z / D.x) * D.y;
+        int bad = -1;
+        if (fabs(p0) < 1e-300) bad = 2 * i;
+        else if (fabs(p1) < 1e-300) bad = 2 * i + 1;
+        if (bad >= 0) atomicMin(bad_row + s, bad);
+        const double det = D.x * D.w - D.y * D.z;
+        A[pd] = make_double4(D.w / det, -D.y / det, -D.z / det, D.x / det);
+    };
     // block IKJ elimination, level by level (rows of a level are independent)
     for (int lev = 0; lev < C.nlev; ++lev) {
+        // narrow level of long rows (exact LU / ILU(k>=1) fill: <= 4 rows with
+        // more than 16 pivots): the whole CTA eliminates one row at a time --
+        // the updates of one pivot hit distinct targets, so they are spread
+        // over the threads, with a barrier between pivots.  Every target sees
+        // the same updates in the same pivot order as in the one-thread-per-row
+        // loop below, so the factors are bitwise the same.
+        {
+            const int q0 = C.lev_ptr[lev], m = C.lev_ptr[lev + 1] - q0;
+            const int i0 = C.lev_rows[q0];
+            if (m <= 4 && C.diag[i0] - C.rowptr[i0] > 16) {
+                for (int qq = 0; qq < m; ++qq) {
+                    const int i = C.lev_rows[q0 + qq];
+                    const int d = C.diag[i];
+                    for (int t = C.rowptr[i]; t < d; ++t) {
+                        const int k = C.col[t];
+                        const int pt = C.pos[t];
+                        const double4 ak = A[pt], dk = A[C.pos[C.diag[k]]];
+                        const Blk L = mul({ak.x, ak.y, ak.z, ak.w}, {dk.x, dk.y, dk.z, dk.w});
+                        __syncthreads();   // every thread has read A[pt]
+                        if (tid == 0) A[pt] = make_double4(L.a, L.b, L.c, L.d);
+                        const int u1 = C.upd_ptr[t + 1];
+                        for (int u = C.upd_ptr[t] + tid; u < u1; u += nt) {
+                            const int2 sd = C.upd[u];
+                            const double4 us = A[sd.x];
+                            double4 v = A[sd.y];
+                            const Blk mm = mul(L, {us.x, us.y, us.z, us.w});
+                            v.x -= mm.a;
+                            v.y -= mm.b;
+                            v.z -= mm.c;
+                            v.w -= mm.d;
+                            A[sd.y] = v;
+                        }
+                        __syncthreads();   // the next pivot reads its updated multiplier
+                    }
+                    if (tid == 0) finish_diag(i, d);
+                    __syncthreads();
+                }
+                continue;
+            }
+        }
         for (int q = C.lev_ptr[lev] + tid; q < C.lev_ptr[lev + 1]; q += nt) {
             const int i = C.lev_rows[q];
             const int d = C.diag[i];
@@ -220,17 +274,7 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
                         }
                 }
             }
-            // diagonal block: scalar pivots as the reference's factor_inplace sees them
-            const int pd = C.pos[d];
-            const double4 D = A[pd];
-            const double p0 = D.x;
-            const double p1 = D.w - (D.z / D.x) * D.y;
-            int bad = -1;
-            if (fabs(p0) < 1e-300) bad = 2 * i;
-            else if (fabs(p1) < 1e-300) bad = 2 * i + 1;
-            if (bad >= 0) atomicMin(bad_row + s, bad);
-            const double det = D.x * D.w - D.y * D.z;
-            A[pd] = make_double4(D.w / det, -D.y / det, -D.z / det, D.x / det);
+            finish_diag(i, d);
         }
         __syncthreads();
     }
