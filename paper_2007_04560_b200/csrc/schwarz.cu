@@ -139,8 +139,8 @@ __device__ __forceinline__ Blk mul(const Blk &x, const Blk &y)
 #ifndef ACCH_FACTOR_MINB
 #define ACCH_FACTOR_MINB 8
 #endif
-template <int DIM>
-__global__ void __launch_bounds__(kFactorThreads, ACCH_FACTOR_MINB)
+template <int DIM, int NT = kFactorThreads>
+__global__ void __launch_bounds__(NT, ACCH_FACTOR_MINB * kFactorThreads / NT)
 factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef, const ClassDev *__restrict__ classes,
               const int *__restrict__ sub_class, const int4 *__restrict__ sub_origin,
               const long long *__restrict__ sub_off, double4 *__restrict__ vals, int *__restrict__ bad_row, int ss)
@@ -2883,14 +2883,28 @@ extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef,
             factor_warp_kernel<2, NW><<<nb, NW * 32, sm, ctx->stream>>>(ctx->g, ctx->p, dt, coef, pc->d_classes,
                 pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, pc->d_bad, pc->nsub, pc->factor_rstride,
                 pc->slot_stride);
-    } else if (pc->dim == 3) {
-        factor_kernel<3><<<(unsigned)pc->nsub, kFactorThreads, 0, ctx->stream>>>(
-            ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals,
-            pc->d_bad, pc->slot_stride);
     } else {
-        factor_kernel<2><<<(unsigned)pc->nsub, kFactorThreads, 0, ctx->stream>>>(
-            ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals,
-            pc->d_bad, pc->slot_stride);
+        // threads per subdomain CTA (ACCH_FACTOR_THREADS = 32 / 64 / 128 overrides):
+        // a 3D ILU level is at most 32 rows wide, so one warp per subdomain
+        // keeps every lane busy in the elimination and fits 4x the subdomains
+        // per SM (same per-row update order: bitwise the same factors).
+        // 128^3 ILU(2) 455 -> 262 ms, 256^3 ILU(0) 101.7 -> 86.6 ms
+        // (profiles/r01_factor_threads.txt)
+        int nt = pc->dim == 3 ? 32 : kFactorThreads;
+        if (const char *e = getenv("ACCH_FACTOR_THREADS")) nt = atoi(e);
+#define FK(D, NT) factor_kernel<D, NT><<<(unsigned)pc->nsub, NT, 0, ctx->stream>>>( \
+            ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, \
+            pc->d_bad, pc->slot_stride)
+        if (pc->dim == 3) {
+            if (nt == 32) FK(3, 32);
+            else if (nt == 64) FK(3, 64);
+            else FK(3, kFactorThreads);
+        } else {
+            if (nt == 32) FK(2, 32);
+            else if (nt == 64) FK(2, 64);
+            else FK(2, kFactorThreads);
+        }
+#undef FK
     }
     ACCH_LAUNCHED(ctx);
     std::vector<int> bad(pc->nsub);
