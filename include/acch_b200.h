@@ -72,6 +72,11 @@ acch_status acch_entropy_chord(acch_ctx *ctx, const double *a, const double *b, 
 /* admissibility_gap (physics.py:89-109) of the interleaved state x. */
 acch_status acch_admissibility_gap(acch_ctx *ctx, const double *x, double *gap);
 
+/* admissibility_gap(u, v) (physics.py:89-109) over n interleaved (u, v)
+ * pairs of any origin (not tied to the context's grid; no halo, no
+ * cross-rank reduction).  NaN anywhere gives -inf, as the reference. */
+acch_status acch_gap_pairs(acch_ctx *ctx, const double *x, int64_t n, double *gap);
+
 /* total_energy, integrate(u), max|v| of a history row (physics.py:325-331,
  * grid.py:301-303, cli/drivers.py:62-73).  Any output pointer may be NULL. */
 acch_status acch_diagnostics(acch_ctx *ctx, const double *x, double *energy,
@@ -150,6 +155,16 @@ acch_status acch_gmres(acch_ctx *ctx, const double *coef, double dt, acch_precon
                        const double *b, double *x, double rel_tol, double abs_tol,
                        int32_t restart, int32_t max_iterations, int32_t ortho,
                        int32_t *iterations, int32_t *converged, double *residual_norm);
+
+/* As acch_gmres with the reference's x0 argument (linalg.py:419, 434-439):
+ * x0_given != 0 starts from the x passed in (r = b - J x), else from 0.
+ * With ortho = 2 on one rank the Arnoldi loop is device-resident: Hessenberg
+ * column, Givens rotations, the least-squares solve and the stopping test
+ * run in kernels, and the host synchronises once per restart cycle. */
+acch_status acch_gmres_x0(acch_ctx *ctx, const double *coef, double dt, acch_precond *pc,
+                          const double *b, double *x, int32_t x0_given, double rel_tol,
+                          double abs_tol, int32_t restart, int32_t max_iterations, int32_t ortho,
+                          int32_t *iterations, int32_t *converged, double *residual_norm);
 
 /* ---- z-slab decomposition (multi-GPU; one context per rank) ------------ */
 

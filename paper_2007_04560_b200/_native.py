@@ -66,6 +66,7 @@ SIGNATURES = {
     "acch_set_stream": (_I32, [_P, _P]),
     "acch_entropy_chord": (_I32, [_P, _P, _P, _I64, _I32, _P, _P]),
     "acch_admissibility_gap": (_I32, [_P, _P, _PD]),
+    "acch_gap_pairs": (_I32, [_P, _P, _I64, _PD]),
     "acch_diagnostics": (_I32, [_P, _P, _PD, _PD, _PD]),
     "acch_residual": (_I32, [_P, _P, _D, _P, _P, _PD, _PD]),
     "acch_jacobian_prepare": (_I32, [_P, _P, _D, _P, _P]),
@@ -84,6 +85,7 @@ SIGNATURES = {
     "acch_precond_apply": (_I32, [_P, _P, _P]),
     "acch_precond_info": (_I32, [_P, _PI64, _PI64, _PI64]),
     "acch_gmres": (_I32, [_P, _P, _D, _P, _P, _P, _D, _D, _I32, _I32, _I32, _PI32, _PI32, _PD]),
+    "acch_gmres_x0": (_I32, [_P, _P, _D, _P, _P, _P, _I32, _D, _D, _I32, _I32, _I32, _PI32, _PI32, _PD]),
     "acch_launch_count": (_I64, [_P]),
     "acch_profile_enable": (_I32, [_P, _I32]),
     "acch_ctx_set_slab": (_I32, [_P, ctypes.POINTER(SlabDesc)]),

@@ -31,7 +31,18 @@ struct GridDev {
     int zwall_lo, zwall_hi;
     long long zoff;          // zg * nx * ny: first interior cell in storage
     long long nstore;        // (nz + 2 zg) * nx * ny stored cells
+    // device-resident GMRES: the Arnoldi-step kernels (matvec, Schwarz apply)
+    // return at once while *skip != 0 (the cycle ended on the device and the
+    // host had already queued the next steps); NULL outside GMRES
+    const int *skip;
 };
+
+#ifdef __CUDACC__
+#define ACCH_SKIP_IF(g)                                   \
+    do {                                                  \
+        if ((g).skip != nullptr && __ldcg((g).skip)) return; \
+    } while (0)
+#endif
 
 struct ParamsDev {
     double alpha, beta, gamma, theta, rho;
@@ -116,6 +127,9 @@ struct acch_ctx {
     double *d_zbasis = nullptr;       // lagged CGS2 with a preconditioner: M^-1 u_j per step (restart columns)
     int zbasis_cols = 0;
     double *d_h = nullptr;            // small device array for Hessenberg column
+    void *d_gm = nullptr;             // device-resident GMRES cycle state (krylov.cu GmState)
+    int *h_gm_status = nullptr;       // per-Arnoldi-step status, mapped pinned host memory
+    int *d_gm_status = nullptr;       // its device alias
     double *d_mvtmp = nullptr;        // two-pass matvec intermediate (dG_u, eta), 2 * nstore
     int matvec_mode = 2;              // 2 z-marching one-barrier kernel (3D default), 1 two-pass (2D), 0 older fused kernel
     long long launches = 0;

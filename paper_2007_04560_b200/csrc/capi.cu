@@ -85,11 +85,13 @@ static double gap_value(double g) { return isnan(g) ? -INFINITY : g; }
 acch_status launch_chord(acch_ctx *ctx, const double *a, const double *b, long long n, int force_exact, double *val,
                          double *der);
 acch_status launch_gap(acch_ctx *ctx, const double *x);
+acch_status launch_gap_pairs(acch_ctx *ctx, const double *x, long long n);
 acch_status launch_diagnostics(acch_ctx *ctx, const double *x);
 acch_status launch_trial(acch_ctx *ctx, const double *x, const double *s, double lam, double *y);
 acch_status launch_feasible_cap(acch_ctx *ctx, const double *x, const double *s, double margin);
 acch_status launch_rms_diff(acch_ctx *ctx, const double *a, const double *b, long long n);
 acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precond *pc, const double *b, double *x,
+                       int x0_given,
                        double rel_tol, double abs_tol, int restart, int max_it, int ortho, int *iterations,
                        int *converged, double *residual_norm);
 
@@ -170,6 +172,7 @@ acch_status acch_ctx_create(const acch_grid_desc *grid, const acch_params *param
     g.zwall_lo = g.zwall_hi = g.periodic ? 0 : 1;
     g.zoff = 0;
     g.nstore = g.n;
+    g.skip = nullptr;
     ParamsDev &p = ctx->p;
     p.alpha = params->alpha;
     p.beta = params->beta;
@@ -210,6 +213,8 @@ acch_status acch_ctx_destroy(acch_ctx *ctx)
     cudaFree(ctx->d_work);
     cudaFree(ctx->d_zbasis);
     cudaFree(ctx->d_mvtmp);
+    cudaFree(ctx->d_gm);
+    if (ctx->h_gm_status) cudaFreeHost(ctx->h_gm_status);
     if (ctx->h_result) cudaFreeHost(ctx->h_result);
     delete ctx;
     return ACCH_OK;
@@ -325,6 +330,19 @@ acch_status acch_admissibility_gap(acch_ctx *ctx, const double *x, double *gap)
     double v = gap_value(ctx->h_result[0]);
     TRY(comm_allreduce(ctx, &v, 1, 1));
     if (gap) *gap = v;
+    return ACCH_OK;
+}
+
+acch_status acch_gap_pairs(acch_ctx *ctx, const double *x, int64_t n, double *gap)
+{
+    CHECK_CTX(ctx);
+    if (n < 1 || !x) {
+        acch_set_error("acch_gap_pairs: need at least one (u, v) pair");
+        return ACCH_ERR_INVALID_ARG;
+    }
+    TRY(launch_gap_pairs(ctx, x, n));
+    TRY(acch_fetch_results(ctx, 1));
+    if (gap) *gap = gap_value(ctx->h_result[0]);
     return ACCH_OK;
 }
 
@@ -487,14 +505,23 @@ acch_status acch_gmres(acch_ctx *ctx, const double *coef, double dt, acch_precon
                        double rel_tol, double abs_tol, int32_t restart, int32_t max_iterations, int32_t ortho,
                        int32_t *iterations, int32_t *converged, double *residual_norm)
 {
+    return acch_gmres_x0(ctx, coef, dt, pc, b, x, 0, rel_tol, abs_tol, restart, max_iterations, ortho, iterations,
+                         converged, residual_norm);
+}
+
+acch_status acch_gmres_x0(acch_ctx *ctx, const double *coef, double dt, acch_precond *pc, const double *b, double *x,
+                          int32_t x0_given, double rel_tol, double abs_tol, int32_t restart, int32_t max_iterations,
+                          int32_t ortho, int32_t *iterations, int32_t *converged, double *residual_norm)
+{
     CHECK_CTX(ctx);
-    if (!coef || !b || !x || !(dt > 0.0) || max_iterations < 0) {
+    if (!coef || !b || !x || !(dt > 0.0) || max_iterations < 0 || ortho < 0 || ortho > 2) {
         acch_set_error("acch_gmres: invalid argument");
         return ACCH_ERR_INVALID_ARG;
     }
     int its = 0, conv = 0;
     double rn = 0.0;
-    acch_status st = gmres_impl(ctx, coef, dt, pc, b, x, rel_tol, abs_tol, restart, max_iterations, ortho, &its, &conv, &rn);
+    acch_status st = gmres_impl(ctx, coef, dt, pc, b, x, x0_given != 0, rel_tol, abs_tol, restart, max_iterations,
+                                ortho, &its, &conv, &rn);
     if (iterations) *iterations = its;
     if (converged) *converged = conv;
     if (residual_norm) *residual_norm = rn;

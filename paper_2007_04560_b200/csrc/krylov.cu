@@ -77,8 +77,9 @@ constexpr int MG = 8;
 
 __global__ void __launch_bounds__(kRedThreads)
 mdot_grouped_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ w, long long n,
-                    double *partials, unsigned int *counters, double *result)
+                    double *partials, unsigned int *counters, double *result, const int *skip)
 {
+    if (skip != nullptr && __ldcg(skip)) return;
     const int g = blockIdx.y;
     const int v0 = g * MG;
     double acc[MG + 1];
@@ -462,6 +463,285 @@ lagupd32_kernel(const double *__restrict__ V, long long ld, int J, const double 
     if (threadIdx.x == 0) *counter = 0u;
 }
 
+
+// ---------------------------------------------------------------------------
+// Device-resident Arnoldi state (ortho = 2, one rank).  The host queues the
+// kernels of each Arnoldi step without reading anything back; the Hessenberg
+// column, the pending lagged correction, the Givens rotations, the
+// least-squares right-hand side g and the stopping test (|g_{j+1}| <= tol,
+// breakdown, restart length, iteration cap) are formed by the last CTA of
+// the step's fused update kernel (lagupd_dev_kernel).  When the cycle ends
+// `stop` is set, and the steps the host had already queued return at once
+// (GridDev::skip / the `skip` arguments).  Per step the last CTA also stores
+// 1 (continue) or 2 (stop) into mapped host memory, which the host polls to
+// keep at most kGmLookahead steps in flight.  The arithmetic and operation
+// order are those of the host driver below (linalg.py:457-501 semantics).
+// ---------------------------------------------------------------------------
+constexpr int GM_R = 32;   // maximum restart
+struct GmState {
+    int stop, jfinal, breakdown, lost, total, max_it, restart, keepz;
+    double tol, beta_p;
+    double H[(GM_R + 1) * GM_R];    // rotated Hessenberg matrix (row stride GM_R)
+    double Hr[(GM_R + 1) * GM_R];   // unrotated
+    double cs[GM_R], sn[GM_R], g[GM_R + 1];
+    double h2p[GM_R + 1];           // pending pass-2 coefficients of the newest column
+    double h2n[GM_R + 1];
+    double Tz[GM_R * GM_R];         // M^-1 v_j = sum_i Tz[i, j] z_i (keepz)
+    double y[GM_R], yz[GM_R];
+};
+
+__device__ __forceinline__ void gm_publish(int *status, int j, int code)
+{
+    if (status == nullptr) return;
+    __threadfence_system();
+    *reinterpret_cast<volatile int *>(status + j) = code;
+    __threadfence_system();
+}
+
+// Hessenberg column j is final up to H(j+1, j) = norm_after: append it,
+// rotate, update g and decide whether the cycle goes on.  Whole block.
+__device__ void gm_finish_column(GmState *st, int j, double norm_after, int *status)
+{
+    constexpr int R = GM_R;
+    if (threadIdx.x == 0) {
+        st->Hr[(j + 1) * R + j] = norm_after;
+        for (int k = 0; k <= j + 1; ++k) st->H[k * R + j] = st->Hr[k * R + j];
+        st->total += 1;
+        double *H = st->H;
+        for (int i = 0; i < j; ++i) {
+            const double t = st->cs[i] * H[i * R + j] + st->sn[i] * H[(i + 1) * R + j];
+            H[(i + 1) * R + j] = -st->sn[i] * H[i * R + j] + st->cs[i] * H[(i + 1) * R + j];
+            H[i * R + j] = t;
+        }
+        const double denom = hypot(H[j * R + j], H[(j + 1) * R + j]);
+        if (denom == 0.0) {
+            st->breakdown = 1;   // the column contributes nothing (linalg.py:478-481)
+            st->stop = 1;
+            st->jfinal = j;
+        } else {
+            st->cs[j] = H[j * R + j] / denom;
+            st->sn[j] = H[(j + 1) * R + j] / denom;
+            H[j * R + j] = denom;
+            H[(j + 1) * R + j] = 0.0;
+            st->g[j + 1] = -st->sn[j] * st->g[j];
+            st->g[j] = st->cs[j] * st->g[j];
+            const int jn = j + 1;
+            st->jfinal = jn;
+            if (norm_after == 0.0) {
+                st->breakdown = 1;
+                st->stop = 1;
+            } else if (fabs(st->g[jn]) <= st->tol || jn >= st->restart || st->total >= st->max_it) {
+                st->stop = 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (st->keepz && !st->stop) {
+        // Tz[:, j+1] = (e_{j+1} - sum_i h2p_i Tz[:, i]) / beta_p
+        const int k = threadIdx.x, c = j + 1;
+        if (k <= c) {
+            double t = k == c ? 1.0 : 0.0;
+            for (int i2 = k; i2 < c; ++i2) t -= st->h2p[i2] * st->Tz[k * R + i2];
+            st->Tz[k * R + c] = t / st->beta_p;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) gm_publish(status, j, st->stop ? 2 : 1);
+}
+
+// Step j after the fused lagged pass: d = multi-dot (gslot layout), e =
+// [||u_{j+1}||^2, <V_s, u_{j+1}> (s < j), ...], e[vslot] = <v_j, u_{j+1}>.
+// Whole block.
+__device__ void gm_hess_step(GmState *st, int j, const double *d, const double *e, int vslot, int *status)
+{
+    constexpr int R = GM_R;
+    __shared__ double s_pj, s_na;
+    __shared__ int s_lost;
+    if (threadIdx.x == 0) {
+        double pj = d[gslot(j)];
+        for (int s2 = 0; s2 < j; ++s2) pj -= st->h2p[s2] * d[gslot(s2)];
+        s_pj = pj / st->beta_p;
+    }
+    __syncthreads();
+    const int k = threadIdx.x;
+    if (k <= j) {
+        double c = 0.0;
+        for (int i2 = k > 0 ? k - 1 : 0; i2 < j; ++i2) c += st->h2p[i2] * st->Hr[k * R + i2];
+        const double pk = k < j ? d[gslot(k)] : s_pj;
+        const double h2 = k < j ? e[1 + k] : e[vslot];
+        st->h2n[k] = h2;
+        st->Hr[k * R + j] = (pk - c) / st->beta_p + h2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double hh = 0.0;
+        for (int q = 0; q <= j; ++q) hh += st->h2n[q] * st->h2n[q];
+        const double xx = e[0];
+        if (xx - hh > 0.0 && hh <= 1e-6 * xx) {
+            s_na = sqrt(xx - hh);
+            for (int q = 0; q <= j; ++q) st->h2p[q] = st->h2n[q];
+            st->beta_p = s_na;
+            s_lost = 0;
+        } else {
+            s_lost = 1;   // orthogonality lost beyond rounding: gm_lost_kernel finishes the column
+        }
+        st->lost = s_lost;
+    }
+    __syncthreads();
+    if (!s_lost) gm_finish_column(st, j, s_na, status);
+}
+
+// The fused lagged pass (lagupd_kernel) with beta and h2 taken from the
+// device state; the last CTA forms Hessenberg column j.
+template <int NS>
+__global__ void __launch_bounds__(kRedThreads)
+lagupd_dev_kernel(const double *__restrict__ V, long long ld, int J, GmState *st, const double *__restrict__ d,
+                  double *__restrict__ U, double *__restrict__ W, long long n, double *partials,
+                  unsigned int *counter, double *result, int *status, int zero)
+{
+    if (__ldcg(&st->stop)) return;
+    __shared__ double sh[NS], sp[NS];
+    const double beta = st->beta_p;
+    lag_coeffs(J, st->h2p, d, beta, sh, sp, NS);
+    __syncthreads();
+    double acc[NS + 1];
+#pragma unroll
+    for (int s = 0; s <= NS; ++s) acc[s] = 0.0;
+    const long long n2 = n >> 1;
+    double2 *__restrict__ u2 = reinterpret_cast<double2 *>(U);
+    double2 *__restrict__ w2 = reinterpret_cast<double2 *>(W);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        double2 v[NS - 1];
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s) v[s] = ldg2_pred(reinterpret_cast<const double2 *>(V + s * ld) + i, s < J);
+        double2 u = u2[i], x = w2[i];
+        const int a0 = NS > 1 ? anchor(v[NS > 1 ? NS - 2 : 0], zero) : 0;
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s)
+            if (s < J) {
+                const double hs = sh[s + (s == 0 ? a0 : 0)];
+                u.x -= hs * v[s].x;
+                u.y -= hs * v[s].y;
+            }
+        u.x /= beta;
+        u.y /= beta;
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s)
+            if (s < J) {
+                x.x -= sp[s] * v[s].x;
+                x.y -= sp[s] * v[s].y;
+            }
+        const double pj = sp[J];
+        x.x -= pj * u.x;
+        x.y -= pj * u.y;
+        x.x /= beta;
+        x.y /= beta;
+        u2[i] = u;
+        w2[i] = x;
+        acc[0] += x.x * x.x + x.y * x.y;
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s)
+            if (s < J) acc[1 + s] += v[s].x * x.x + v[s].y * x.y;
+        acc[NS] += u.x * x.x + u.y * x.y;   // <v_j, x>
+    }
+    int ops[NS + 1];
+#pragma unroll
+    for (int s = 0; s <= NS; ++s) ops[s] = RED_SUM;
+    if (!reduce_finish<NS + 1>(acc, ops, partials, counter, result)) return;
+    __syncthreads();   // result[] (thread 0) visible to the block
+    gm_hess_step(st, J, d, result, NS, status);
+}
+
+// Explicit second pass when the lagged identity is unusable (st->lost):
+// w -= V h2n, ||w||^2, then the column is finished with the measured norm.
+// v_{j+1} = u_{j+1} / ||u_{j+1}|| is left to the next step's lagged pass
+// (h2p = 0, beta_p = ||u_{j+1}||), which divides exactly as a scaling would.
+template <int NS>
+__global__ void __launch_bounds__(kRedThreads)
+gm_lost_kernel(const double *__restrict__ V, long long ld, int m, GmState *st, double *__restrict__ w, long long n,
+               double *partials, unsigned int *counter, double *result, int *status)
+{
+    if (__ldcg(&st->stop) || !__ldcg(&st->lost)) return;
+    __shared__ double sh[NS];
+    if (threadIdx.x < NS) sh[threadIdx.x] = threadIdx.x < m ? st->h2n[threadIdx.x] : 0.0;
+    __syncthreads();
+    double acc = 0.0;
+    const long long n2 = n >> 1;
+    double2 *__restrict__ w2 = reinterpret_cast<double2 *>(w);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n2; i += (long long)gridDim.x * blockDim.x) {
+        double2 wi = w2[i];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+            if (s < m) {
+                const double2 v = reinterpret_cast<const double2 *>(V + s * ld)[i];
+                wi.x -= sh[s] * v.x;
+                wi.y -= sh[s] * v.y;
+            }
+        w2[i] = wi;
+        acc += wi.x * wi.x + wi.y * wi.y;
+    }
+    double v1[1] = {acc};
+    const int ops[1] = {RED_SUM};
+    if (!reduce_finish<1>(v1, ops, partials, counter, result)) return;
+    __syncthreads();
+    __shared__ double s_na;
+    if (threadIdx.x == 0) {
+        s_na = sqrt(result[0]);
+        for (int q = 0; q <= GM_R; ++q) st->h2p[q] = 0.0;
+        st->beta_p = s_na > 0.0 ? s_na : 1.0;
+        st->lost = 0;
+    }
+    __syncthreads();
+    gm_finish_column(st, m - 1, s_na, status);
+}
+
+__global__ void gm_init_kernel(GmState *st, double res_norm, double tol, int total, int max_it, int restart, int keepz)
+{
+    constexpr int R = GM_R;
+    for (int i = threadIdx.x; i < (R + 1) * R; i += blockDim.x) {
+        st->H[i] = 0.0;
+        st->Hr[i] = 0.0;
+    }
+    for (int i = threadIdx.x; i < R * R; i += blockDim.x) st->Tz[i] = 0.0;
+    for (int i = threadIdx.x; i <= R; i += blockDim.x) {
+        st->g[i] = 0.0;
+        st->h2p[i] = 0.0;
+        st->h2n[i] = 0.0;
+        if (i < R) st->cs[i] = st->sn[i] = st->y[i] = st->yz[i] = 0.0;
+    }
+    if (threadIdx.x == 0) {
+        st->g[0] = res_norm;
+        st->Tz[0] = 1.0;   // M^-1 v_0 = z_0
+        st->stop = st->jfinal = st->breakdown = st->lost = 0;
+        st->total = total;
+        st->max_it = max_it;
+        st->restart = restart;
+        st->keepz = keepz;
+        st->tol = tol;
+        st->beta_p = 1.0;   // v_0 is final
+    }
+}
+
+// upper-triangular solve H[:j,:j] y = g[:j] (solve_triangular, linalg.py:500)
+// and, with keepz, yz = Tz y
+__global__ void gm_tri_kernel(GmState *st)
+{
+    constexpr int R = GM_R;
+    if (threadIdx.x != 0) return;
+    const int j = st->jfinal;
+    for (int i = j - 1; i >= 0; --i) {
+        double s = st->g[i];
+        for (int k = i + 1; k < j; ++k) s -= st->H[i * R + k] * st->y[k];
+        st->y[i] = s / st->H[i * R + i];
+    }
+    if (st->keepz)
+        for (int k = 0; k < j; ++k) {
+            double t = 0.0;
+            for (int i2 = k; i2 < j; ++i2) t += st->Tz[k * R + i2] * st->y[i2];
+            st->yz[k] = t;
+        }
+}
+
 template <int NS>
 __global__ void combine_kernel(const double *__restrict__ V, long long ld, int m, const double *__restrict__ y,
                                double *__restrict__ t, long long n)
@@ -507,8 +787,15 @@ __global__ void axpy_dev_kernel(const double *__restrict__ hdev, const double *_
         w[i] -= h * v[i];
 }
 
+// y = a x + b y; b == 0 never reads y (the BLAS beta = 0 convention: y may
+// hold uninitialised memory, NaN patterns included)
 __global__ void axpby_kernel(double a, const double *__restrict__ x, double b, double *__restrict__ y, long long n)
 {
+    if (b == 0.0) {
+        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+            y[i] = a * x[i];
+        return;
+    }
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         y[i] = a * x[i] + b * y[i];
 }
@@ -539,7 +826,8 @@ static acch_status mdot_to(acch_ctx *ctx, const double *V, long long ld, int m, 
     }
     const int groups = (m + MG - 1) / MG;
     const dim3 grid(rgrid(n), groups);
-    mdot_grouped_kernel<<<grid, kRedThreads, 0, ctx->stream>>>(V, ld, m, w, n, ctx->d_partials, ctx->d_counter, out);
+    mdot_grouped_kernel<<<grid, kRedThreads, 0, ctx->stream>>>(V, ld, m, w, n, ctx->d_partials, ctx->d_counter, out,
+                                                                ctx->g.skip);
     *ns = MG + 1;
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
@@ -688,9 +976,46 @@ static acch_status fetch(acch_ctx *ctx, double *host, const double *dev, int cou
         if (_s != ACCH_OK) return _s;            \
     } while (0)
 
+static acch_status ensure_gm(acch_ctx *ctx)
+{
+    if (ctx->d_gm) return ACCH_OK;
+    ACCH_CUDA(cudaMalloc(&ctx->d_gm, sizeof(GmState)));
+    ACCH_CUDA(cudaHostAlloc(reinterpret_cast<void **>(&ctx->h_gm_status), sizeof(int) * 64, cudaHostAllocMapped));
+    ACCH_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&ctx->d_gm_status), ctx->h_gm_status, 0));
+    return ACCH_OK;
+}
+
+// steps queued ahead of the newest step whose outcome the host has seen
+constexpr int kGmLookahead = 2;
+
+// Wait until step j of the device-resident cycle has published its status
+// (mapped memory, no stream synchronisation).  Returns 1 (continue), 2
+// (stop) or 0 when the stream drained without a status (the step was
+// skipped: an earlier step ended the cycle).
+static acch_status gm_wait(acch_ctx *ctx, int j, int *code)
+{
+    volatile int *st = ctx->h_gm_status;
+    for (long long spin = 0;; ++spin) {
+        const int c = st[j];
+        if (c != 0) {
+            *code = c;
+            return ACCH_OK;
+        }
+        if ((spin & 1023) == 1023) {
+            const cudaError_t e = cudaStreamQuery(ctx->stream);
+            if (e == cudaSuccess) {
+                const int c2 = st[j];
+                *code = c2 != 0 ? c2 : 0;
+                return ACCH_OK;
+            }
+            if (e != cudaErrorNotReady) return acch_cuda_fail(e, "gmres step");
+        }
+    }
+}
+
 acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precond *pc, const double *b, double *x,
-                       double rel_tol, double abs_tol, int restart, int max_it, int ortho, int *iterations,
-                       int *converged, double *residual_norm)
+                       int x0_given, double rel_tol, double abs_tol, int restart, int max_it, int ortho,
+                       int *iterations, int *converged, double *residual_norm)
 {
     if (restart < 1 || restart > 32) {
         acch_set_error("gmres: restart must be in [1, 32]");
@@ -731,9 +1056,18 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
     const double bnorm = sqrt(tmp[0]);
     const double tol = std::max(rel_tol * bnorm, abs_tol);
 
-    ACCH_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nv, ctx->stream));
-    ACCH_CUDA(cudaMemcpyAsync(R, b, sizeof(double) * nv, cudaMemcpyDeviceToDevice, ctx->stream));
     double res_norm = bnorm;
+    if (x0_given) {
+        // r = b - J x0 (linalg.py:437-439)
+        TRY(matvec(x, R));
+        TRY(launch_axpby(ctx, 1.0, b, -1.0, R, nv));
+        TRY(dot_to(ctx, R + off, R + off, ni, dh));
+        TRY(reduce_dots(tmp, dh, 1, false));
+        res_norm = sqrt(tmp[0]);
+    } else {
+        ACCH_CUDA(cudaMemsetAsync(x, 0, sizeof(double) * nv, ctx->stream));
+        ACCH_CUDA(cudaMemcpyAsync(R, b, sizeof(double) * nv, cudaMemcpyDeviceToDevice, ctx->stream));
+    }
     int total = 0;
     std::vector<double> H((restart + 1) * restart), cs(restart), sn(restart), gv(restart + 1), y(restart);
     auto h = [&](int i, int j) -> double & { return H[i * restart + j]; };
@@ -746,17 +1080,134 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
     // ortho = 2 with a preconditioner: z_j = M^-1 u_j is kept per step, and
     // M^-1 v_j = sum_i Tz[i, j] z_i (v_j = (u_j - V h2p) / beta_p), so the
     // cycle's update x += M^-1 V y = Z (Tz y) needs no extra apply
-    const bool keepz = ortho == 2 && pc;
-    std::vector<double> Tz(keepz ? restart * restart : 0), yz(restart);
-    auto tz = [&](int i, int j) -> double & { return Tz[i * restart + j]; };
+    // keepz costs restart extra vectors (restart x 2N doubles: 8 GB at 256^3
+    // with restart 30); when they cannot be allocated the cycle update falls
+    // back to one extra preconditioner apply (x += M^-1 V y)
+    bool keepz = ortho == 2 && pc;
     if (keepz && ctx->zbasis_cols < restart) {
         if (ctx->d_zbasis) cudaFree(ctx->d_zbasis);
         ctx->d_zbasis = nullptr;
-        ACCH_CUDA(cudaMalloc(&ctx->d_zbasis, sizeof(double) * nv * restart));
-        ACCH_CUDA(cudaMemsetAsync(ctx->d_zbasis, 0, sizeof(double) * nv * restart, ctx->stream));
-        ctx->zbasis_cols = restart;
+        ctx->zbasis_cols = 0;
+        if (cudaMalloc(&ctx->d_zbasis, sizeof(double) * nv * restart) != cudaSuccess) {
+            cudaGetLastError();   // clear the allocation error
+            ctx->d_zbasis = nullptr;
+            keepz = false;
+        } else {
+            ACCH_CUDA(cudaMemsetAsync(ctx->d_zbasis, 0, sizeof(double) * nv * restart, ctx->stream));
+            ctx->zbasis_cols = restart;
+        }
     }
+    std::vector<double> Tz(keepz ? restart * restart : 0), yz(restart);
+    auto tz = [&](int i, int j) -> double & { return Tz[i * restart + j]; };
     auto zcol = [&](int j) { return ctx->d_zbasis + (long long)j * nv; };
+
+    if (ortho == 2 && !multi) {
+        // ---- device-resident cycles (see GmState) ----
+        TRY(ensure_gm(ctx));
+        GmState *st = reinterpret_cast<GmState *>(ctx->d_gm);
+        GmState hst;   // header read back once per cycle
+        const size_t hdr = offsetof(GmState, tol);
+        for (;;) {
+            if (res_norm <= tol) {
+                *iterations = total; *converged = 1; *residual_norm = res_norm;
+                return ACCH_OK;
+            }
+            if (total >= max_it) {
+                *iterations = total; *converged = 0; *residual_norm = res_norm;
+                return ACCH_OK;
+            }
+            gm_init_kernel<<<1, 256, 0, ctx->stream>>>(st, res_norm, tol, total, max_it, restart, keepz ? 1 : 0);
+            ACCH_LAUNCHED(ctx);
+            TRY(scale_by(ctx, res_norm, R, col(0), nv));
+            const int jmax = std::min(restart, max_it - total);
+            for (int q = 0; q < jmax; ++q) ctx->h_gm_status[q] = 0;
+            const GridDev gsave = ctx->g;
+            ctx->g.skip = &st->stop;
+            acch_status err = ACCH_OK;
+            auto step = [&](int j) -> acch_status {
+                const double *zj;
+                if (keepz) {
+                    TRY(precond(col(j), zcol(j)));
+                    zj = zcol(j);
+                } else if (pc) {
+                    TRY(precond(col(j), Z));
+                    zj = Z;
+                } else {
+                    zj = col(j);
+                }
+                double *w = col(j + 1);
+                TRY(matvec(zj, w));
+                int ns = 0;
+                TRY(mdot_to(ctx, V + off, nv, j + 1, w + off, ni, dh, &ns));
+                {
+                    ProfScope ps(ctx, PC_KUPDATE, 8.0 * (j + 4) * ni);
+                    const int G = rgrid(ni);
+#define LAGD(NS) lagupd_dev_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V + off, nv, j, st, dh, col(j) + off, \
+                     w + off, ni, ctx->d_partials, ctx->d_counter, dh + 64, ctx->d_gm_status, 0)
+                    if (j + 1 <= 4) LAGD(4);
+                    else if (j + 1 <= 8) LAGD(8);
+                    else if (j + 1 <= 16) LAGD(16);
+                    else if (j + 1 <= 24) LAGD(24);
+                    else LAGD(32);
+#undef LAGD
+                    ACCH_LAUNCHED(ctx);
+                }
+                {
+                    ProfScope ps(ctx, PC_KUPDATE, 0.0);
+                    const int G = rgrid(ni);
+#define LOSTK(NS) gm_lost_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V + off, nv, j + 1, st, w + off, ni, \
+                      ctx->d_partials, ctx->d_counter, dh + 40, ctx->d_gm_status)
+                    if (j + 1 <= 4) LOSTK(4);
+                    else if (j + 1 <= 8) LOSTK(8);
+                    else if (j + 1 <= 16) LOSTK(16);
+                    else LOSTK(32);
+#undef LOSTK
+                    ACCH_LAUNCHED(ctx);
+                }
+                return ACCH_OK;
+            };
+            for (int j = 0; j < jmax; ++j) {
+                if (j >= kGmLookahead) {
+                    int code = 0;
+                    err = gm_wait(ctx, j - kGmLookahead, &code);
+                    if (err != ACCH_OK || code != 1) break;
+                }
+                err = step(j);
+                if (err != ACCH_OK) break;
+            }
+            ctx->g = gsave;
+            if (err != ACCH_OK) return err;
+            ACCH_CUDA(cudaMemcpyAsync(&hst, st, hdr, cudaMemcpyDeviceToHost, ctx->stream));
+            ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
+            const int j = hst.jfinal;
+            total = hst.total;
+            if (j > 0) {
+                gm_tri_kernel<<<1, 32, 0, ctx->stream>>>(st);
+                ACCH_LAUNCHED(ctx);
+                if (keepz) {
+                    TRY(combine(ctx, ctx->d_zbasis, nv, j, st->yz, T, nv));
+                    TRY(launch_axpby(ctx, 1.0, T, 1.0, x, nv));
+                } else {
+                    TRY(combine(ctx, V, nv, j, st->y, T, nv));
+                    if (pc) {
+                        TRY(precond(T, Z));
+                        TRY(launch_axpby(ctx, 1.0, Z, 1.0, x, nv));
+                    } else {
+                        TRY(launch_axpby(ctx, 1.0, T, 1.0, x, nv));
+                    }
+                }
+            }
+            TRY(matvec(x, R));
+            TRY(launch_axpby(ctx, 1.0, b, -1.0, R, nv));
+            TRY(dot_to(ctx, R + off, R + off, ni, dh));
+            TRY(reduce_dots(tmp, dh, 1, false));
+            res_norm = sqrt(tmp[0]);
+            if (hst.breakdown && res_norm > tol) {
+                *iterations = total; *converged = 0; *residual_norm = res_norm;
+                return ACCH_OK;
+            }
+        }
+    }
 
     for (;;) {
         if (res_norm <= tol) {

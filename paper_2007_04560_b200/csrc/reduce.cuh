@@ -59,8 +59,9 @@ __device__ __forceinline__ void block_reduce(double (&v)[NS], const int (&ops)[N
 }
 
 // Grid-wide deterministic finish.  partials: [NS][nblocks]; result: [NS].
+// Returns true in the one block that folded the partials (the last to arrive).
 template <int NS>
-__device__ __forceinline__ void reduce_finish(double (&v)[NS], const int (&ops)[NS], double *partials,
+__device__ __forceinline__ bool reduce_finish(double (&v)[NS], const int (&ops)[NS], double *partials,
                                               unsigned int *counter, double *result)
 {
     __shared__ double smem[32 * NS];
@@ -78,7 +79,7 @@ __device__ __forceinline__ void reduce_finish(double (&v)[NS], const int (&ops)[
         is_last = (t == (unsigned int)(nb - 1));
     }
     __syncthreads();
-    if (!is_last) return;
+    if (!is_last) return false;
     __threadfence();
     double w[NS];
 #pragma unroll
@@ -93,13 +94,14 @@ __device__ __forceinline__ void reduce_finish(double (&v)[NS], const int (&ops)[
         for (int s = 0; s < NS; ++s) result[s] = w[s];
         *counter = 0u;
     }
+    return true;   // the last block (result[] is written by its thread 0)
 }
 
 // Finish over blockIdx.x only: blocks with the same (blockIdx.y, blockIdx.z)
 // form one independent reduction; the caller offsets partials / counter /
 // result per group.
 template <int NS>
-__device__ __forceinline__ void reduce_finish_x(double (&v)[NS], const int (&ops)[NS], double *partials,
+__device__ __forceinline__ bool reduce_finish_x(double (&v)[NS], const int (&ops)[NS], double *partials,
                                                 unsigned int *counter, double *result)
 {
     __shared__ double smem[32 * NS];
@@ -117,7 +119,7 @@ __device__ __forceinline__ void reduce_finish_x(double (&v)[NS], const int (&ops
         is_last = (t == (unsigned int)(nb - 1));
     }
     __syncthreads();
-    if (!is_last) return;
+    if (!is_last) return false;
     __threadfence();
     double w[NS];
 #pragma unroll
@@ -132,4 +134,5 @@ __device__ __forceinline__ void reduce_finish_x(double (&v)[NS], const int (&ops
         for (int s = 0; s < NS; ++s) result[s] = w[s];
         *counter = 0u;
     }
+    return true;   // the last block (result[] is written by its thread 0)
 }

@@ -459,6 +459,7 @@ apply_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restr
              const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out, int use_smem,
              int max_nloc, long long nsub)
 {
+    ACCH_SKIP_IF(g);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int group = threadIdx.x / TPS;               // subdomain slot within the CTA
     const int lane = threadIdx.x % TPS;
@@ -631,6 +632,7 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
                   const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
                   WarpSmem L, long long nsub)
 {
+    ACCH_SKIP_IF(g);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = threadIdx.x;
     const long long s = blockIdx.x;
@@ -1098,6 +1100,7 @@ apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *
                    const FT *__restrict__ vals, const double2 *__restrict__ r, double2 *__restrict__ z,
                    double2 *__restrict__ ext_out, int meta_max, int y_stride, int zero, int pd)
 {
+    ACCH_SKIP_IF(g);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int4 G = groups[blockIdx.x];   // (class, first entry of grp_sub, count, -)
     const ClassDev &C = classes[G.x];
@@ -1168,6 +1171,7 @@ apply_rs_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *__r
                 const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
                 double2 *__restrict__ scratch, int meta_pad, int ring_stride, int max_nloc, int pf_rows)
 {
+    ACCH_SKIP_IF(g);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int4 it = items[blockIdx.x];   // (class, first batch, batches, -)
     const ClassDev &C = classes[it.x];
@@ -1452,6 +1456,7 @@ apply_tma_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__r
                  const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
                  TmaSmem L, long long nsub)
 {
+    ACCH_SKIP_IF(g);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x;
     const long long s = blockIdx.x;
@@ -1654,8 +1659,9 @@ apply_tma_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__r
 
 // z[c] = sum over subdomains containing c, in subdomain order, of their local solution
 __global__ void gather_kernel(long long n, const long long *__restrict__ cell_ptr, const long long *__restrict__ cell_src,
-                              const double2 *__restrict__ ext_out, double2 *__restrict__ z)
+                              const double2 *__restrict__ ext_out, double2 *__restrict__ z, const int *skip)
 {
+    if (skip != nullptr && __ldcg(skip)) return;
     const long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (c >= n) return;
     double2 acc = make_double2(0.0, 0.0);
@@ -3051,7 +3057,7 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     if (pc->variant != 1) {
         const long long n = ctx->g.n;
         gather_kernel<<<(unsigned)((n + 255) / 256), 256, 0, ctx->stream>>>(n, pc->d_cell_ptr, pc->d_cell_src,
-                                                                          pc->d_ext_out, (double2 *)z);
+                                                                          pc->d_ext_out, (double2 *)z, ctx->g.skip);
         ACCH_LAUNCHED(ctx);
     }
     return ACCH_OK;

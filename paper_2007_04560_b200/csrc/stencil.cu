@@ -562,6 +562,7 @@ __global__ void __launch_bounds__(TX *(TY / RPT))
 matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
               const double2 *__restrict__ w_g, double2 *__restrict__ yout)
 {
+    ACCH_SKIP_IF(g);
     using L = MatvecSmem<DIM, TX, TY>;
     constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, TB = TY / RPT, NT = TX * TB;
     constexpr int NJ = (GX * GY + NT - 1) / NT;   // tile+1-halo cells per thread
@@ -799,6 +800,7 @@ __global__ void __launch_bounds__(TX *TY + (RW ? 32 * ((2 * TX + 2 * TY + 31) / 
 mv_zm_kernel(const GridDev g, const MvConst mc, const double2 *__restrict__ w_g, double2 *__restrict__ yout,
              int nchunk)
 {
+    ACCH_SKIP_IF(g);
     using L = ZmSmem<TX, TY>;
     constexpr int HX = L::HX, GX = L::GX, NW = L::NW, NB = L::NB, NRING = L::NRING, NT = TX * TY;
     // RW: the ring columns get their own warps (every thread owns one column,
@@ -1059,6 +1061,7 @@ __global__ void __launch_bounds__(PTX * PTY)
 mv_pass1_kernel(GridDev g, ParamsDev P, const double *__restrict__ coef, const double2 *__restrict__ w,
                 double2 *__restrict__ T, int zlo)
 {
+    ACCH_SKIP_IF(g);
     // planes zlo .. : in slab mode also the first ghost plane past an
     // interior slab boundary, which pass 2 reads as a z-neighbour
     const int x = blockIdx.x * PTX + threadIdx.x, y = blockIdx.y * PTY + threadIdx.y;
@@ -1087,6 +1090,7 @@ __global__ void __launch_bounds__(PTX * PTY)
 mv_pass2_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef, const double2 *__restrict__ w,
                 const double2 *__restrict__ T, double2 *__restrict__ yout)
 {
+    ACCH_SKIP_IF(g);
     const int x = blockIdx.x * PTX + threadIdx.x, y = blockIdx.y * PTY + threadIdx.y;
     if (x >= g.nx || y >= g.ny) return;
     const int z = (int)blockIdx.z;
@@ -1551,6 +1555,17 @@ acch_status launch_gap(acch_ctx *ctx, const double *x)
     ProfScope prof_scope(ctx, PC_REDUCE, 16.0 * ctx->g.n);
     const long long n = ctx->g.n;
     gap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x + ctx->g.zoff, ctx->d_partials, ctx->d_counter,
+                                                            ctx->d_result);
+    ACCH_LAUNCHED(ctx);
+    return ACCH_OK;
+}
+
+// gap over n arbitrary interleaved (u, v) pairs (the reference's
+// admissibility_gap(u, v) on plain arrays, physics.py:89-109)
+acch_status launch_gap_pairs(acch_ctx *ctx, const double *x, long long n)
+{
+    ProfScope prof_scope(ctx, PC_REDUCE, 16.0 * n);
+    gap_kernel<<<red_grid(n), kRedThreads, 0, ctx->stream>>>(n, (const double2 *)x, ctx->d_partials, ctx->d_counter,
                                                             ctx->d_result);
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;

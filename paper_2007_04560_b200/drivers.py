@@ -2,12 +2,14 @@
 the reference's acch/cli/config.py:23-120 dataclasses and
 acch/cli/drivers.py:26-184 ``build_initial_state`` / ``simulate``).
 
-INI parsing, file output and the experiment drivers are out of scope; the
-dataclasses keep the reference's field names and defaults so a RunConfig
-built for the reference maps over field by field."""
+INI parsing and the experiment drivers are out of scope; the dataclasses
+keep the reference's field names and defaults so a RunConfig built for the
+reference maps over field by field.  ``simulate(out_dir=...)`` writes the
+reference's history CSV and VTK snapshots (io.py)."""
 
 from __future__ import annotations
 
+import os
 import time
 from dataclasses import dataclass, field, replace
 
@@ -70,12 +72,20 @@ class SolverSpec:
 
 
 @dataclass(frozen=True)
+class OutputSpec:
+    history: str = "history.csv"
+    snapshot_times: tuple = ()
+    snapshot_every: int = 0
+
+
+@dataclass(frozen=True)
 class RunConfig:
     grid: Grid
     params: Params
     initial: InitialSpec
     time: TimeSpec
     solver: SolverSpec = SolverSpec()
+    output: OutputSpec = OutputSpec()
 
     @property
     def eta(self) -> float:
@@ -244,39 +254,67 @@ class Stepper:
         return dt, newton_count, gmres_count
 
 
-def simulate(config: RunConfig, threads: int = 1, max_steps: int | None = None, state: State | None = None,
-             device=None, diagnostics_every: int = 1) -> SimulationResult:
+def simulate(config: RunConfig, threads: int = 1, out_dir: str | None = None, snapshot_every: int = 0,
+             max_steps: int | None = None, state: State | None = None, device=None,
+             diagnostics_every: int = 1) -> SimulationResult:
     """Advance from t = 0 to the horizon (drivers.py:76-184) and record
     energy / mass / max|v| per accepted step.  ``events`` lists
-    (step, dt, reason) for every divergence."""
+    (step, dt, reason) for every divergence.  With ``out_dir`` the history
+    CSV is written incrementally (flushed per step) and VTK snapshots at the
+    configured times / every ``snapshot_every`` steps plus ``final.vtk``,
+    as the reference does; partial outputs survive a stall."""
+    from .io import HistoryWriter, write_vtk
     if state is None:
         state = build_initial_state(config, device)
     stepper = Stepper(config, state, threads)
     history = []
+    snapshot_every = snapshot_every or config.output.snapshot_every
+    pending = sorted(config.output.snapshot_times)
+    writer = None
+    if out_dir is not None:
+        os.makedirs(out_dir, exist_ok=True)
+        writer = HistoryWriter(os.path.join(out_dir, config.output.history))
 
     def row(step, t, dt, st, newton, gm, wall):
         if diagnostics_every and (step % diagnostics_every == 0):
             e, m, v = diagnostics(st, config.params)
         else:
             e = m = v = float("nan")
-        history.append(HistoryRow(step, t, dt, e, m, v, newton, gm, wall))
+        r = HistoryRow(step, t, dt, e, m, v, newton, gm, wall)
+        history.append(r)
+        if writer is not None:
+            writer.write(r)
 
     row(0, 0.0, 0.0, state, 0, 0, 0.0)
     status = COMPLETED
     horizon = config.time.horizon
-    while stepper.t < horizon * (1.0 - 1e-12):
-        if max_steps is not None and stepper.step >= max_steps:
-            break
-        wall0 = time.perf_counter()
-        try:
-            dt, nn, ng = stepper.advance()
-        except SolverStallError:
-            status = STALLED
-            break
-        row(stepper.step, stepper.t, dt, stepper.state, nn, ng, time.perf_counter() - wall0)
+    try:
+        while stepper.t < horizon * (1.0 - 1e-12):
+            if max_steps is not None and stepper.step >= max_steps:
+                break
+            wall0 = time.perf_counter()
+            try:
+                dt, nn, ng = stepper.advance()
+            except SolverStallError:
+                status = STALLED
+                break
+            row(stepper.step, stepper.t, dt, stepper.state, nn, ng, time.perf_counter() - wall0)
+            if out_dir is not None:
+                t = stepper.t
+                while pending and t >= pending[0] * (1.0 - 1e-12):
+                    target = pending.pop(0)
+                    write_vtk(stepper.state, os.path.join(out_dir, f"snapshot_t{target:g}.vtk"),
+                              title=f"state at t={t:.10g} (requested {target:g})")
+                if snapshot_every and stepper.step % snapshot_every == 0:
+                    write_vtk(stepper.state, os.path.join(out_dir, f"step_{stepper.step:06d}.vtk"))
+    finally:
+        if writer is not None:
+            writer.close()
+    if out_dir is not None:
+        write_vtk(stepper.state, os.path.join(out_dir, "final.vtk"), title="final state")
     return SimulationResult(status, history, stepper.state, stepper.controller, stepper.factorizations,
                             stepper.events)
 
 
-__all__ = ["InitialSpec", "TimeSpec", "SolverSpec", "RunConfig", "initial_fields", "build_initial_state",
+__all__ = ["InitialSpec", "TimeSpec", "SolverSpec", "OutputSpec", "RunConfig", "initial_fields", "build_initial_state",
            "HistoryRow", "SimulationResult", "Stepper", "simulate", "COMPLETED", "STALLED"]

@@ -297,39 +297,165 @@ class GmresResult:
 ORTHO = {"mgs": 0, "cgs2": 1, "dcgs2": 2}
 
 
+def _generic_ctx(device):
+    """A context for the grid-independent vector kernels (dot / axpby)."""
+    from .physics import DEFAULT_PARAMS
+    return nat.context_for(Grid((4, 4), (1.0, 1.0), BoundaryCondition.PERIODIC), DEFAULT_PARAMS, device)
+
+
+def _gmres_generic(matvec, b, precond, rel_tol, abs_tol, restart, max_iterations, x0) -> GmresResult:
+    """The reference's GMRES (linalg.py:411-506) for an arbitrary device
+    matvec / preconditioner callable: the reference's operation order (MGS,
+    second pass when ||w|| < ||w_0|| / 2, Givens, true-residual restarts),
+    vectors on the device through the library's deterministic dot / axpby
+    kernels, the (restart+1) x restart Hessenberg matrix on the host."""
+    as_numpy = isinstance(b, np.ndarray) or np.isscalar(b)
+    dev = b.device if isinstance(b, torch.Tensor) and b.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    bt = torch.as_tensor(np.asarray(b, dtype=float) if as_numpy else b, dtype=torch.float64, device=dev).reshape(-1)
+    bt = bt.contiguous()
+    n = bt.numel()
+    ctx = _generic_ctx(dev)
+    L = nat.lib()
+
+    def to_dev(y):
+        t = torch.as_tensor(np.asarray(y, dtype=float) if isinstance(y, np.ndarray) else y, dtype=torch.float64,
+                            device=dev).reshape(-1)
+        return t.contiguous()
+
+    def dot(a, c):
+        out = ctypes.c_double()
+        nat.check(L.acch_dot(ctx.bind(), nat.ptr(a), nat.ptr(c), n, ctypes.byref(out)), "dot")
+        return out.value
+
+    def axpby(a, xv, bb, yv):      # yv <- a xv + bb yv
+        nat.check(L.acch_axpby(ctx.bind(), float(a), nat.ptr(xv), float(bb), nat.ptr(yv), n), "axpby")
+
+    if precond is None:
+        apply_m = lambda v: v   # noqa: E731
+    elif hasattr(precond, "apply"):
+        apply_m = precond.apply
+    else:
+        apply_m = precond
+    tol = max(rel_tol * math.sqrt(dot(bt, bt)), abs_tol)
+    if x0 is None:
+        x = torch.zeros_like(bt)
+        r = bt.clone()
+    else:
+        x = to_dev(x0).clone()
+        r = bt.clone()
+        axpby(-1.0, to_dev(matvec(x)).clone(), 1.0, r)
+    total = 0
+    res_norm = math.sqrt(dot(r, r))
+    while True:
+        if res_norm <= tol:
+            break
+        if total >= max_iterations:
+            break
+        V = torch.zeros((restart + 1, n), dtype=torch.float64, device=dev)
+        H = np.zeros((restart + 1, restart))
+        cs = np.zeros(restart)
+        sn = np.zeros(restart)
+        g = np.zeros(restart + 1)
+        axpby(1.0 / res_norm, r, 0.0, V[0])
+        g[0] = res_norm
+        j = 0
+        breakdown = False
+        while j < restart and total < max_iterations:
+            # copy: matvec / preconditioner may hand back their input
+            w = to_dev(matvec(to_dev(apply_m(V[j])))).clone()
+            norm_before = math.sqrt(dot(w, w))
+            for i in range(j + 1):
+                H[i, j] = dot(V[i], w)
+                axpby(-H[i, j], V[i], 1.0, w)
+            norm_after = math.sqrt(dot(w, w))
+            if norm_after < 0.5 * norm_before:
+                for i in range(j + 1):
+                    corr = dot(V[i], w)
+                    H[i, j] += corr
+                    axpby(-corr, V[i], 1.0, w)
+                norm_after = math.sqrt(dot(w, w))
+            H[j + 1, j] = norm_after
+            total += 1
+            for i in range(j):
+                t = cs[i] * H[i, j] + sn[i] * H[i + 1, j]
+                H[i + 1, j] = -sn[i] * H[i, j] + cs[i] * H[i + 1, j]
+                H[i, j] = t
+            denom = math.hypot(H[j, j], H[j + 1, j])
+            if denom == 0.0:
+                breakdown = True
+                break
+            cs[j] = H[j, j] / denom
+            sn[j] = H[j + 1, j] / denom
+            H[j, j] = denom
+            H[j + 1, j] = 0.0
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            j += 1
+            if norm_after == 0.0:
+                breakdown = True
+                break
+            axpby(1.0 / norm_after, w, 0.0, V[j])
+            if abs(g[j]) <= tol:
+                break
+        if j > 0:
+            y = np.zeros(j)
+            for i in range(j - 1, -1, -1):
+                y[i] = (g[i] - H[i, i + 1:j] @ y[i + 1:j]) / H[i, i]
+            comb = torch.zeros_like(bt)
+            for i in range(j):
+                axpby(y[i], V[i], 1.0, comb)
+            axpby(1.0, to_dev(apply_m(comb)).clone(), 1.0, x)
+        r = bt.clone()
+        axpby(-1.0, to_dev(matvec(x)).clone(), 1.0, r)
+        res_norm = math.sqrt(dot(r, r))
+        if breakdown and res_norm > tol:
+            xo = x.cpu().numpy() if as_numpy else x
+            return GmresResult(xo, total, False, res_norm)
+    xo = x.cpu().numpy() if as_numpy else x
+    return GmresResult(xo, total, res_norm <= tol, res_norm)
+
+
 def gmres(matvec, b, precond=None, rel_tol: float = 1e-8, abs_tol: float = 1e-14, restart: int = 30,
           max_iterations: int = 500, x0=None, ortho: str = "dcgs2") -> GmresResult:
     """Restarted right-preconditioned GMRES (linalg.py:411-506).
 
-    ``matvec`` must be a JacobianOperator (or its bound ``matvec``) and
-    ``precond`` None or a SchwarzPreconditioner; the whole solve then runs in
-    libacch_b200.  ``ortho='mgs'`` reproduces the reference's modified
-    Gram-Schmidt operation order; ``'cgs2'`` is classical
-    Gram-Schmidt with the reference's conditional second pass, fused into two
-    sweeps over the basis; ``'dcgs2'`` lags the second pass by one Arnoldi
-    step (always taken) so that one multi-dot and one fused update sweep the
-    basis per step (default).  Stopping and restarts follow the reference: the
-    recomputed true residual decides convergence."""
+    With a JacobianOperator (or its bound ``matvec``) and ``precond`` None or
+    a SchwarzPreconditioner, the whole solve runs in libacch_b200 (device
+    basis, device Hessenberg / Givens, no host round trip per Arnoldi step).
+    ``ortho='mgs'`` reproduces the reference's modified Gram-Schmidt operation
+    order; ``'cgs2'`` is classical Gram-Schmidt with the reference's
+    conditional second pass, fused into two sweeps over the basis;
+    ``'dcgs2'`` lags the second pass by one Arnoldi step (always taken) so
+    that one multi-dot and one fused update sweep the basis per step
+    (default).  Any other matvec (a callable on device vectors, e.g. a dense
+    torch matrix) or preconditioner callable runs the reference's MGS
+    algorithm through the library's vector kernels.  Stopping and restarts
+    follow the reference: the recomputed true residual decides convergence;
+    ``x0`` (default 0) is the initial guess."""
     from .scheme import JacobianOperator
     op = matvec
     if not isinstance(op, JacobianOperator):
         op = getattr(matvec, "__self__", None)
-    if not isinstance(op, JacobianOperator):
-        raise TypeError("gmres on this backend takes a JacobianOperator (assemble_jacobian) as matvec")
-    if x0 is not None:
-        raise NotImplementedError("gmres starts from x0 = 0 (the only form newton_solve uses, newton.py:144-152)")
-    if precond is not None and not isinstance(precond, SchwarzPreconditioner):
-        raise TypeError("precond must be a SchwarzPreconditioner or None")
-    if precond is not None and precond.handle is None:
-        raise RuntimeError("preconditioner has no factorization; call update() first")
-    b = nat.dev_f64(b, 2 * op.n_store, "b")
-    x = torch.empty_like(b)
-    its, conv, rn = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
-    nat.check(nat.lib().acch_gmres(op.ctx.bind(), nat.ptr(op.coef), op.dt,
-                                   precond.handle if precond is not None else None, nat.ptr(b), nat.ptr(x),
-                                   float(rel_tol), float(abs_tol), int(restart), int(max_iterations), ORTHO[ortho],
-                                   ctypes.byref(its), ctypes.byref(conv), ctypes.byref(rn)), "gmres")
-    return GmresResult(x, int(its.value), bool(conv.value), float(rn.value))
+    native = isinstance(op, JacobianOperator) and (precond is None or isinstance(precond, SchwarzPreconditioner))
+    if native and isinstance(b, torch.Tensor) and restart <= 32:
+        if precond is not None and precond.handle is None:
+            raise RuntimeError("preconditioner has no factorization; call update() first")
+        b = nat.dev_f64(b, 2 * op.n_store, "b")
+        if x0 is None:
+            x = torch.empty_like(b)
+        else:
+            x = nat.dev_f64(torch.as_tensor(x0, dtype=torch.float64, device=b.device).reshape(-1).clone(),
+                            2 * op.n_store, "x0")
+        its, conv, rn = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_double()
+        nat.check(nat.lib().acch_gmres_x0(op.ctx.bind(), nat.ptr(op.coef), op.dt,
+                                          precond.handle if precond is not None else None, nat.ptr(b), nat.ptr(x),
+                                          int(x0 is not None), float(rel_tol), float(abs_tol), int(restart),
+                                          int(max_iterations), ORTHO[ortho], ctypes.byref(its), ctypes.byref(conv),
+                                          ctypes.byref(rn)), "gmres")
+        return GmresResult(x, int(its.value), bool(conv.value), float(rn.value))
+    if restart < 1:
+        raise ValueError("restart must be >= 1")
+    return _gmres_generic(matvec, b, precond, rel_tol, abs_tol, restart, max_iterations, x0)
 
 
 __all__ = ["Decomposition", "partition", "SchwarzVariant", "SubdomainSolverSpec", "SchwarzPreconditioner",

@@ -147,12 +147,25 @@ def state_gap(state: State) -> float:
     return out.value
 
 
-def admissibility_gap(u, v) -> float:
+def admissibility_gap(u, v=None) -> float:
     """Smallest distance from the admissible-set boundary (physics.py:89-109).
     Accepts a State or a (u, v) pair of arrays/tensors."""
     if isinstance(u, State):
         return state_gap(u)
-    raise TypeError("admissibility_gap takes a State on this backend")
+    if v is None:
+        raise TypeError("admissibility_gap takes a State or a (u, v) pair")
+    nat.require_cuda()
+    dev = u.device if isinstance(u, torch.Tensor) and u.is_cuda else (
+        v.device if isinstance(v, torch.Tensor) and v.is_cuda else _default_device())
+    ut, vt = torch.broadcast_tensors(_as_device(u, dev), _as_device(v, dev))
+    if ut.numel() == 0:
+        raise ValueError("admissibility_gap of an empty field")
+    x = torch.stack((ut.reshape(-1), vt.reshape(-1)), dim=1).contiguous()
+    from .grid import BoundaryCondition
+    ctx = _ctx(Grid((4, 4), (1.0, 1.0), BoundaryCondition.PERIODIC), None, dev)
+    out = ctypes.c_double()
+    nat.check(nat.lib().acch_gap_pairs(ctx.bind(), nat.ptr(x), ut.numel(), ctypes.byref(out)), "gap_pairs")
+    return out.value
 
 
 def is_admissible(state: State, margin: float = ADMISSIBILITY_MARGIN) -> bool:

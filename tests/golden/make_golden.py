@@ -202,8 +202,8 @@ def newton_cases():
 
 
 def sim_case(tag, counts, bc, center, amp, mode, dt, horizon, nsub, solver="ilu0", eta=None,
-             max_steps=None, variant="ras-left"):
-    grid = Grid(counts, tuple(1.0 for _ in counts), BC[bc])
+             max_steps=None, variant="ras-left", length=1.0):
+    grid = Grid(counts, tuple(length for _ in counts), BC[bc])
     cfg = RunConfig(
         grid, PARAMS, InitialSpec("random_uniform", center, amp, 1234),
         TimeSpec(horizon=horizon, mode=mode, dt=dt, dt_min=1e-4, dt_max=10.0, eta=eta),
@@ -221,7 +221,8 @@ def sim_case(tag, counts, bc, center, amp, mode, dt, horizon, nsub, solver="ilu0
          meta=np.array([center, amp, dt, horizon, nsub, -1 if eta is None else eta,
                         -1 if max_steps is None else max_steps]),
          counts=np.array(counts), periodic=np.array(bc == "periodic"), mode=np.array(mode),
-         solver=np.array(solver), variant=np.array(variant), wall=np.array(wall))
+         solver=np.array(solver), variant=np.array(variant), wall=np.array(wall), length=np.array(length),
+         eta=np.array(cfg.eta))
     print(f"  {tag}: {res.status}, {len(h) - 1} steps, {wall:.1f} s, divergences {res.controller.divergence_count}")
 
 
@@ -259,6 +260,19 @@ def main():
         sim_case("c2small", (32, 32), "periodic", 0.4, 0.02, "adaptive", 1e-4, 10.0, 4, max_steps=40)
         # config-3 analogue: 3D Neumann, adaptive eta=1e2, 8 boxes
         sim_case("c3small", (16, 16, 16), "neumann", 0.5, 0.01, "adaptive", 1e-4, 10.0, 8, max_steps=4)
+    # the BASELINE solver regimes (VERDICT r1 "next" #1)
+    if want("sim3p"):
+        # config-3 stiffness proxy: 32^3 Neumann on a box of side 0.25 (dx = 1/128, the
+        # 128^3 grid's spacing), 8^3-cell boxes, ILU(2) (ILU(0)/ILU(1) fail here), eta = 1e2
+        sim_case("c3proxy", (32, 32, 32), "neumann", 0.5, 0.01, "adaptive", 1e-4, 10.0, 64, solver="ilu2",
+                 max_steps=3, length=0.25)
+    if want("sim2a"):
+        # config-2 analogue: 128^2 periodic, 16x16-cell boxes, exact LU, adaptive eta = 1e4
+        sim_case("c2analog", (128, 128), "periodic", 0.4, 0.02, "adaptive", 1e-4, 10.0, 64, solver="lu",
+                 max_steps=20)
+    if want("sim4a"):
+        # config-4 analogue (the bench's regime): 32^3 periodic, 8^3-cell boxes, ILU(0), eta = 1e2
+        sim_case("c4analog", (32, 32, 32), "periodic", 0.5, 0.01, "adaptive", 1e-4, 10.0, 64, max_steps=5)
 
 
 if __name__ == "__main__":

@@ -49,12 +49,15 @@ def configs():
     }
 
 
-def run(tag, desc, cfg, steps, wall_cap):
+def run(tag, desc, cfg, steps, wall_cap, profile=False):
     dev = torch.device("cuda", 0)
     state = build_initial_state(cfg, dev)
     e0, m0, v0 = diagnostics(state, cfg.params)
     rows = [dict(step=0, t=0.0, dt=0.0, energy=e0, mass=m0, max_abs_v=v0, newton=0, gmres=0, wall_s=0.0)]
     st = Stepper(cfg, state)
+    if profile:
+        st.ctx.profile(True)
+        st.ctx.profile_read()
     torch.cuda.synchronize()
     t_start = time.perf_counter()
     status = "completed"
@@ -73,6 +76,10 @@ def run(tag, desc, cfg, steps, wall_cap):
             break
     torch.cuda.synchronize()
     wall = time.perf_counter() - t_start
+    prof = None
+    if profile:
+        prof = {k: {"ms": round(v[0], 3), "launches": int(v[1])} for k, v in st.ctx.profile_read().items() if v[1]}
+        st.ctx.profile(False)
     energies = [r["energy"] for r in rows]
     masses = [r["mass"] for r in rows]
     rises = [energies[i + 1] - energies[i] for i in range(len(energies) - 1)]
@@ -85,7 +92,7 @@ def run(tag, desc, cfg, steps, wall_cap):
                max_energy_rise=max(rises) if rises else 0.0,
                mass_drift=max(abs(m - masses[0]) for m in masses),
                energy_first=energies[0], energy_last=energies[-1], rows=rows,
-               events=[list(map(str, e)) for e in st.events])
+               events=[list(map(str, e)) for e in st.events], kernel_ms=prof)
     return out
 
 
@@ -94,12 +101,14 @@ def main():
     ap.add_argument("--configs", default="1,2,3")
     ap.add_argument("--wall", type=float, default=900.0, help="wall-clock cap per config (s)")
     ap.add_argument("--out", default="gpurun_out")
+    ap.add_argument("--steps", type=int, default=0, help="override the step count")
+    ap.add_argument("--profile", action="store_true", help="CUDA-event time per kernel category")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
     table = configs()
     for c in [int(x) for x in a.configs.split(",")]:
         desc, cfg, steps = table[c]
-        res = run(c, desc, cfg, steps, a.wall)
+        res = run(c, desc, cfg, a.steps or steps, a.wall, a.profile)
         with open(os.path.join(a.out, f"config{c}_trace.json"), "w") as f:
             json.dump(res, f, indent=1)
         print(json.dumps({k: v for k, v in res.items() if k not in ("rows",)}), flush=True)
