@@ -11,8 +11,9 @@ repeats K steps through the public API with the state staged from pinned host
 memory and read back every step; `roofline` is for the kernel category with
 the largest share of the timed region (algorithmic bytes / measured time,
 from CUDA events recorded around every launch on the launching stream);
-`cpu_baseline` times the CPU oracle (a port of the reference algorithm) on a
-bounded sample on this host.  Every vector is 268 MB (> 126 MB L2), so no L2
+`cpu_baseline` times the unmodified reference package (baseline/_ref) by parts
+on a bounded 32^3 sample on this host and composes a 256^3 step from the
+window's work counts (see "CPU baseline / reference arm" below).  Every vector is 268 MB (> 126 MB L2), so no L2
 flush is needed between iterations.
 """
 
@@ -64,6 +65,9 @@ def parse_args():
                          "not the headline configuration)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-micro", action="store_true", help="reference arm: skip the full-size microbenchmarks")
+    ap.add_argument("--record-counts", action="store_true",
+                    help="write this window's per-step work counts into bench_counts.json")
     ap.add_argument("--verbose", action="store_true")
     return ap.parse_args()
 
@@ -160,49 +164,205 @@ def workload_name(args):
 
 
 # ---------------------------------------------------------------------------
-# CPU baseline: the oracle (a port of the reference algorithm) on this host
+# CPU baseline / reference arm: the UNMODIFIED reference package `acch`
 # ---------------------------------------------------------------------------
+#
+# The reference (pure Python + numpy / scipy / numba) is installed, unmodified,
+# into baseline/_ref (git-ignored; it travels to the GPU box with the repo):
+#   python -m pip install --no-index --no-build-isolation --no-deps \
+#       --target baseline/_ref <copy of /root/reference/pkg>
+# It cannot run a 256^3 step on a host in useful time (its Jacobian assembly
+# alone needs 47.7 GB and 242 s; one GMRES iteration ~17 s), so a step is
+# timed by parts on a bounded sample: the same solver (left-RAS, 8^3-cell
+# boxes, overlap 1, ILU(0), GMRES(30)) on a 32^3 periodic grid with the same
+# seeded fields, each part timed with the reference's own functions --
+# residual_vector, assemble_jacobian, SchwarzPreconditioner.update (numba
+# ILU), one 30-iteration gmres cycle -- and composed into a 256^3 step with
+# the cell ratio (every part is linear in the cell count) and the work counts
+# of the timed window (GMRES iterations, Newton iterations, factorisations,
+# residual evaluations), which bench_counts.json records per (warmup, steps)
+# window from the GPU arm's own run of the identical workload; the GPU arm
+# checks its counts against that table on every run.
 
-# Per-step work of the timed region of the 256^3 GPU run (steps 4-7 after the
-# 3 warm-up steps; profiles/r01_bench_*.json): used by the reference arm,
-# which runs without a GPU and cannot measure them itself.
-REF_STEP_COUNTS = {"gmres_per_step": 922.0, "factorizations_per_step": 1.25, "newton_per_step": 2.25}
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+COUNTS_FILE = os.path.join(ROOT, "bench_counts.json")
 
 
-def cpu_sample(args, threads=1, counts=None):
-    """CPU oracle (numpy + C ILU port of the reference, tests only) timed on
-    this host on a bounded sample of the same workload: the per-cell cost of
-    one GMRES iteration (matvec + left-RAS ILU(0) apply + MGS) and of one
-    Jacobian assembly + subdomain factorisation, measured on a 32^3 periodic
-    grid with the same 8^3 boxes, scaled to the full grid and to the GMRES
-    iterations and factorisations per step of the GPU run."""
+def import_reference():
+    """The reference package from baseline/_ref, or None."""
+    if not os.path.isdir(os.path.join(REF_DIR, "acch")):
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", os.path.join(tempfile.gettempdir(), "acch_ref_numba"))
+    if REF_DIR not in sys.path:
+        sys.path.insert(0, REF_DIR)
+    try:
+        import acch  # noqa: F401
+        import acch.linalg  # noqa: F401
+        return acch
+    except Exception:
+        return None
+
+
+def window_key(args):
+    return f"{args.n}^{args.dim}:box{args.box}:{args.solver}:{args.variant}:r{args.restart}:W{args.warmup}:K{args.steps}"
+
+
+def load_counts(args):
+    """Per-step work of the timed window, recorded from the GPU arm."""
+    try:
+        table = json.load(open(COUNTS_FILE))
+    except Exception:
+        return None, None
+    key = window_key(args)
+    if key in table:
+        return table[key], key
+    # same workload, another window: nearest recorded window (stated in `sample`)
+    pre = key.rsplit(":W", 1)[0] + ":W"
+    cands = [k for k in table if k.startswith(pre)]
+    if not cands:
+        return None, None
+    return table[cands[0]], cands[0]
+
+
+def reference_parts(args, threads, ns=32, reps=1):
+    """Seconds per call of each part of the reference's NKS step on an ns^dim
+    sample (after a warm-up that compiles the numba ILU kernels)."""
+    import numpy as np
+    acch = import_reference()
+    if acch is None:
+        return None
+    from acch.grid import BoundaryCondition as RBC, Field as RField, Grid as RGrid
+    from acch.linalg import (SchwarzPreconditioner as RSP, SchwarzVariant as RSV, SubdomainSolverSpec as RSS,
+                             gmres as rgmres, partition as rpartition)
+    from acch.parallel import WorkerPool
+    from acch.physics import Params as RParams, State as RState
+    from acch.scheme import (StepProblem as RStep, assemble_jacobian as rjac, residual_vector as rres,
+                             state_from_vector, vector_from_state)
+    g = RGrid((ns,) * args.dim, (1.0,) * args.dim, RBC.PERIODIC)
+    rng = np.random.default_rng(1234)
+    u = 0.5 + rng.uniform(-0.01, 0.01, g.array_shape)
+    v = rng.uniform(-0.01, 0.01, g.array_shape)
+    old = RState(RField.from_interior(g, u), RField.from_interior(g, v))
+    prob = RStep.create(g, RParams(4.0, 2.0, 0.005, 0.1, 0.001), old, 0.0111)
+    x = vector_from_state(old) + 1e-4 * np.random.default_rng(1234).standard_normal(2 * g.n_cells)
+    new = state_from_vector(g, x)
+    nsub = (ns // args.box) ** args.dim
+    out = {}
+    with WorkerPool(threads) as pool:
+        pre = RSP(rpartition(g, nsub, 1), RSV(args.variant), RSS.from_string(args.solver), pool)
+        F = rres(prob, new)
+        J = rjac(prob, new)
+        pre.update(J)                                        # numba compile (factor)
+        rgmres(J.matvec, -F, pre, 1e-30, 1e-300, 2, 2)       # numba compile (solve)
+        ts = {"residual": [], "jacobian": [], "factor": [], "gmres_iter": []}
+        for _ in range(reps):
+            t0 = time.perf_counter(); F = rres(prob, new); ts["residual"].append(time.perf_counter() - t0)
+            t0 = time.perf_counter(); J = rjac(prob, new); ts["jacobian"].append(time.perf_counter() - t0)
+            pre.invalidate()
+            t0 = time.perf_counter(); pre.update(J); ts["factor"].append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            res = rgmres(J.matvec, -F, pre, 1e-30, 1e-300, args.restart, args.restart)   # exactly one cycle
+            ts["gmres_iter"].append((time.perf_counter() - t0) / max(res.iterations, 1))
+        for k, vals in ts.items():
+            out[k] = min(vals)
+    out["cells"] = g.n_cells
+    out["ns"] = ns
+    return out
+
+
+def reference_step_estimate(args, parts, counts):
+    scale = float(args.n ** args.dim) / parts["cells"]
+    t = scale * (counts["gmres"] * parts["gmres_iter"] + counts["factorizations"] * parts["factor"] +
+                 counts["jacobians"] * parts["jacobian"] + counts["residuals"] * parts["residual"])
+    return t, scale
+
+
+def reference_microbench(args, threads):
+    """the unmodified residual_vector at the bench grid
+    and StencilMatrix.matvec at 128^3 (assembly at 256^3 needs 47.7 GB), on
+    the microbenchmark state pair U' = U^n + 1e-4 N(0,1)."""
+    import numpy as np
+    if import_reference() is None:
+        return None
+    from acch.grid import BoundaryCondition as RBC, Field as RField, Grid as RGrid
+    from acch.physics import Params as RParams, State as RState
+    from acch.scheme import (StepProblem as RStep, assemble_jacobian as rjac, residual_vector as rres,
+                             state_from_vector, vector_from_state)
+    out = {}
+    for name, n in (("residual", args.n), ("matvec", min(args.n, 128))):
+        g = RGrid((n,) * args.dim, (1.0,) * args.dim, RBC.PERIODIC)
+        rng = np.random.default_rng(1234)
+        u = 0.5 + rng.uniform(-0.01, 0.01, g.array_shape)
+        v = rng.uniform(-0.01, 0.01, g.array_shape)
+        old = RState(RField.from_interior(g, u), RField.from_interior(g, v))
+        prob = RStep.create(g, RParams(4.0, 2.0, 0.005, 0.1, 0.001), old, 1e-4)
+        x = vector_from_state(old) + 1e-4 * np.random.default_rng(1234).standard_normal(2 * g.n_cells)
+        new = state_from_vector(g, x)
+        if name == "residual":
+            t0 = time.perf_counter()
+            rres(prob, new)
+            t = time.perf_counter() - t0
+        else:
+            t0 = time.perf_counter()
+            J = rjac(prob, new)
+            t_asm = time.perf_counter() - t0
+            w = np.random.default_rng(7).standard_normal(2 * g.n_cells)
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                J.matvec(w)
+                ts.append(time.perf_counter() - t0)
+            t = min(ts)
+            out["matvec_assembly_s"] = t_asm
+        out[name] = {"grid": [n] * args.dim, "s": t, "gdof_s": 2 * g.n_cells / t / 1e9}
+        del prob, new, old
+    out["threads"] = threads
+    out["kind"] = "reference"
+    return out
+
+
+def cpu_sample(args, threads=1, counts=None, ns=None):
+    """The reference's step cost on this host (see above); falls back to the
+    oracle port (numpy + C ILU, tests only) when the reference package is not
+    importable."""
+    counts = counts or load_counts(args)[0]
+    parts = reference_parts(args, threads, ns or 32) if import_reference() is not None else None
+    if parts is not None and counts is not None:
+        t_step, scale = reference_step_estimate(args, parts, counts)
+        return {"value": 1.0 / t_step, "unit": "time steps/s", "cores": threads, "kind": "reference",
+                "parts_s": {k: parts[k] for k in ("residual", "jacobian", "factor", "gmres_iter")},
+                "sample": (f"unmodified reference acch (baseline/_ref) on {parts['ns']}^{args.dim} periodic, "
+                           f"{args.box}^{args.dim}-cell boxes, {args.solver}, {threads} thread(s): "
+                           f"{parts['gmres_iter'] * 1e3:.1f} ms per GMRES iteration, {parts['factor']:.3f} s per "
+                           f"factorisation, {parts['jacobian']:.3f} s per assembly, {parts['residual'] * 1e3:.1f} ms "
+                           f"per residual; x{scale:.0f} cells, per-step counts {counts['gmres']:.1f} GMRES + "
+                           f"{counts['factorizations']:.2f} factorisations + {counts['jacobians']:.2f} Jacobians + "
+                           f"{counts['residuals']:.2f} residuals (bench_counts.json); step estimate {t_step:.0f} s")}
+    # fallback: the oracle port
     import numpy as np
     from oracle import acch_oracle as O
-    counts = counts or REF_STEP_COUNTS
-    ns = 32 if args.dim == 3 else 256
+    if counts is None:
+        return {"error": "no recorded per-step counts for this workload (bench_counts.json)"}
+    ns = ns or 32
     m = O.Mesh((ns,) * args.dim, (1.0,) * args.dim, True)
     u, v = O.initial_fields(m, 0.5, 0.01, 1234)
     st = O.Step(m, O.Coeffs(), u, v, 2e-3)
-    rng = np.random.default_rng(1234)
-    x = O.pack(u, v) + 1e-4 * rng.standard_normal(2 * m.n_cells)
+    x = O.pack(u, v) + 1e-4 * np.random.default_rng(1234).standard_normal(2 * m.n_cells)
     pre = O.SchwarzOracle(O.decompose(m, (ns // args.box) ** args.dim, 1), args.variant, args.solver, threads)
     t0 = time.perf_counter()
     J = st.jacobian(x)
     pre.update(J.assemble_fast())
     t_fact = time.perf_counter() - t0
     b = -st.residual(x)
-    its = 30
     t0 = time.perf_counter()
-    res = O.gmres(J.matvec, b, pre.apply, 1e-30, 1e-300, its, its)   # exactly `its` Arnoldi steps
+    res = O.gmres(J.matvec, b, pre.apply, 1e-30, 1e-300, args.restart, args.restart)
     t_gm = (time.perf_counter() - t0) / max(res.iterations, 1)
     scale = float(args.n ** args.dim) / m.n_cells
-    t_step = scale * (counts["gmres_per_step"] * t_gm + counts["factorizations_per_step"] * t_fact)
+    t_step = scale * (counts["gmres"] * t_gm + counts["factorizations"] * t_fact)
     return {"value": 1.0 / t_step, "unit": "time steps/s", "cores": threads, "kind": "port",
-            "sample": (f"oracle (numpy + C ILU port of acch) on {ns}^{args.dim} periodic, {args.box}^{args.dim} boxes: "
-                       f"{t_gm * 1e3:.1f} ms per GMRES iteration, {t_fact:.2f} s per assembly+factorisation; "
-                       f"scaled by the cell ratio {scale:.0f} and per-step counts {counts['gmres_per_step']:.0f} "
-                       f"GMRES + {counts['factorizations_per_step']:.2f} factorisations "
-                       f"(CPU step estimate {t_step:.0f} s)")}
+            "sample": (f"oracle port (reference not importable) on {ns}^{args.dim}: {t_gm * 1e3:.1f} ms per GMRES "
+                       f"iteration, {t_fact:.2f} s per assembly+factorisation, x{scale:.0f} cells, "
+                       f"{counts['gmres']:.1f} GMRES + {counts['factorizations']:.2f} factorisations per step")}
 
 
 def run_reference(args):
@@ -210,21 +370,33 @@ def run_reference(args):
     if rank != 0:
         return
     threads = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    vals = []
+    counts, key = load_counts(args)
+    vals, sample = [], None
+    micro = None
+    t_start = time.perf_counter()
     for i in range(min(args.warmup, 1) + args.steps):
-        r = cpu_sample(args, threads=threads)
+        r = cpu_sample(args, threads=threads, counts=counts)
+        if "value" not in r:
+            print(json.dumps({"impl": "reference", "unavailable": r.get("error", "no sample")}), flush=True)
+            return
         if i >= min(args.warmup, 1):
             vals.append(r["value"])
+            sample = r
+        if i == 0 and r["kind"] == "reference" and not args.no_micro:
+            micro = reference_microbench(args, threads)
     value = sum(vals) / len(vals)
     line = {"metric": METRIC, "value": value, "unit": "time steps/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "dtype": "f64", "data": "synthetic",
             "config": {"workload": workload_name(args), "grid": [args.n] * args.dim, "bc": "periodic",
                        "ic": "u0=0.5+0.01U(-1,1), v0=0.01U(-1,1), seed 1234",
-                       "parallelism": f"host CPU, {threads} threads"},
-            "cpu_baseline": {"value": value, "unit": "time steps/s", "cores": threads, "kind": "port",
-                             "sample": r["sample"]},
-            "e2e": {"value": value, "unit": "time steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+                       "parallelism": f"host CPU, {threads} threads (the reference's WorkerPool)",
+                       "counts_window": key},
+            "cpu_baseline": {"value": value, "unit": "time steps/s", "cores": threads, "kind": sample["kind"],
+                             "sample": sample["sample"], "parts_s": sample.get("parts_s")},
+            "reference_microbench": micro,
+            "e2e": {"value": value, "unit": "time steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t_start}
     print(json.dumps(line), flush=True)
 
 
@@ -433,14 +605,40 @@ def run_ours(args):
                 "avg_launch_ms": (d["ms"] / d["launches"]) if d else None,
                 "alg_bytes_per_launch": d.get("alg_bytes_per_launch"), "peak_source": peaks["source"]}
 
+    # per-step work of the timed window (the reference arm composes its step
+    # from these; bench_counts.json pins them per window)
+    steps_done = max(args.steps, 1)
+    counts = {"gmres": gmres_total / steps_done, "newton": newton_total / steps_done,
+              "factorizations": prof.get("precond_factor", (0, 0, 0))[1] / steps_done,
+              "jacobians": prof.get("jacobian_prepare", (0, 0, 0))[1] / steps_done,
+              "residuals": prof.get("residual", (0, 0, 0))[1] / steps_done, "retries": retries / steps_done}
+    counts_check = None
+    if world == 1:
+        rec, key = load_counts(args)
+        if args.record_counts and rank == 0:
+            try:
+                table = json.load(open(COUNTS_FILE))
+            except Exception:
+                table = {}
+            table[window_key(args)] = counts
+            with open(COUNTS_FILE, "w") as f:
+                json.dump(table, f, indent=1, sort_keys=True)
+            counts_check = "recorded"
+        elif rec is not None and key == window_key(args):
+            bad = {k: (counts[k], rec.get(k)) for k in ("gmres", "newton", "factorizations", "jacobians", "residuals")
+                   if rec.get(k) is None or abs(counts[k] - rec[k]) > 1e-9 * max(1.0, abs(rec[k]))}
+            counts_check = "match" if not bad else {"MISMATCH": bad}
+            if bad and rank == 0:
+                print(f"bench.py: WARNING: the timed window's work counts differ from bench_counts.json[{key}]: "
+                      f"{bad} -- the reference arm's step estimate is keyed to the recorded counts", file=sys.stderr,
+                      flush=True)
+        else:
+            counts_check = "no recorded counts for this window"
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            steps_done = max(args.steps, 1)
-            cpu = cpu_sample(args, threads=1, counts={
-                "gmres_per_step": gmres_total / steps_done,
-                "factorizations_per_step": max(prof.get("precond_factor", (0, 0, 0))[1], 1) / steps_done,
-                "newton_per_step": newton_total / steps_done})
+            cpu = cpu_sample(args, threads=1, counts=counts)
         except Exception as e:  # the baseline must not break the GPU line
             cpu = {"error": repr(e)}
 
@@ -458,7 +656,8 @@ def run_ours(args):
                        "l2": "every vector 268 MB > 126 MB L2 (no flush needed)",
                        "steps_timed": f"accepted steps {first_timed}..{first_timed + args.steps - 1} (after {args.warmup} warm-up steps)"},
             "solver_stats": {"newton": newton_total, "gmres": gmres_total, "retries": retries,
-                             "dt": [round(x, 6) for x in dts]},
+                             "dt": [round(x, 6) for x in dts], "per_step": counts, "counts_check": counts_check,
+                             "ms_per_gmres_iteration": elapsed * 1e3 / max(gmres_total, 1)},
             "roofline": roofline,
             "matvec": micro["matvec"], "residual": micro["residual"],
             "kernels": cats,
