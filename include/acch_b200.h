@@ -197,6 +197,20 @@ typedef int32_t (*acch_halo_fn)(void *user, double *vec, int64_t plane_doubles, 
 
 acch_status acch_ctx_set_slab(acch_ctx *ctx, const acch_slab_desc *slab);
 acch_status acch_set_comm(acch_ctx *ctx, acch_allreduce_fn allreduce, acch_halo_fn halo, void *user);
+
+/* ---- in-library NCCL data plane (replaces the host hooks) ---------------
+ * Rank 0 calls acch_nccl_unique_id and shares the acch_nccl_id_bytes()
+ * bytes with every rank (torch.distributed broadcast); every rank then calls
+ * acch_set_nccl on its slab context (collective, blocks until all ranks
+ * joined).  From then on ghost-plane exchanges are grouped ncclSend /
+ * ncclRecv and every cross-rank reduction an ncclAllReduce, all enqueued on
+ * the context's stream; the GMRES Arnoldi loop stays device-resident at
+ * N > 1.  nccl_path: the libnccl to dlopen (NULL: "libnccl.so.2"). */
+acch_status acch_nccl_unique_id(const char *nccl_path, void *id_out);
+int32_t acch_nccl_id_bytes(void);
+acch_status acch_set_nccl(acch_ctx *ctx, const char *nccl_path, const void *id, int32_t nranks, int32_t rank);
+/* halo bytes sent and NCCL calls made by this context so far */
+acch_status acch_comm_stats(acch_ctx *ctx, double *bytes, int64_t *calls);
 int64_t acch_storage_cells(acch_ctx *ctx);
 
 /* Count of kernels this library has launched on ctx since creation (for the

@@ -92,6 +92,10 @@ SIGNATURES = {
     "acch_set_comm": (_I32, [_P, ALLREDUCE_FN, HALO_FN, _P]),
     "acch_storage_cells": (_I64, [_P]),
     "acch_profile_read": (_I32, [_P, _PD, _PI64, _PD, _I32]),
+    "acch_nccl_unique_id": (_I32, [ctypes.c_char_p, ctypes.c_void_p]),
+    "acch_nccl_id_bytes": (_I32, []),
+    "acch_set_nccl": (_I32, [_P, ctypes.c_char_p, ctypes.c_char_p, _I32, _I32]),
+    "acch_comm_stats": (_I32, [_P, _PD, _PI64]),
 }
 
 PROFILE_CATEGORIES = ("residual", "jacobian_prepare", "matvec", "precond_factor", "precond_apply",
@@ -200,8 +204,11 @@ class Context:
             comm = comm_for(grid)
             if comm is None:
                 raise RuntimeError("no communicator bound to this slab grid (slab.bind_comm)")
-            ar, ha = comm.c_hooks(self.device)
-            check(self._lib.acch_set_comm(h, ar, ha, None), "acch_set_comm")
+            if getattr(comm, "native", False):
+                comm.bind(h)            # in-library NCCL (collective across ranks)
+            else:
+                ar, ha = comm.c_hooks(self.device)
+                check(self._lib.acch_set_comm(h, ar, ha, None), "acch_set_comm")
             self.comm = comm
 
     def bind(self):
@@ -213,6 +220,12 @@ class Context:
     @property
     def launches(self) -> int:
         return int(self._lib.acch_launch_count(self.handle))
+
+    def comm_stats(self) -> dict:
+        """Halo bytes sent and NCCL calls made by this context."""
+        b, c = ctypes.c_double(), ctypes.c_int64()
+        check(self._lib.acch_comm_stats(self.handle, ctypes.byref(b), ctypes.byref(c)), "comm_stats")
+        return {"halo_bytes": b.value, "nccl_calls": c.value}
 
     def profile(self, on: bool = True):
         check(self._lib.acch_profile_enable(self.handle, int(bool(on))), "profile_enable")

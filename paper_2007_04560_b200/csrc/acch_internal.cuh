@@ -141,11 +141,22 @@ struct acch_ctx {
     acch_allreduce_cb allreduce = nullptr;
     acch_halo_cb halo = nullptr;
     void *comm_user = nullptr;
+    // in-library NCCL data plane (comm.cu, acch_set_nccl): replaces the hooks
+    void *nccl_comm = nullptr;
+    double *d_comm = nullptr;         // 64-double staging buffer for host-value allreduces
+    double comm_bytes = 0.0;          // halo bytes sent (statistics)
+    long long comm_calls = 0;
 };
 
 // multi-rank helpers (capi.cu): no-ops for a single domain
 acch_status comm_allreduce(acch_ctx *ctx, double *vals, int n, int op);
 acch_status comm_halo(acch_ctx *ctx, const double *vec, int doubles_per_cell, int depth);
+// NCCL data plane (comm.cu)
+bool comm_has_nccl(const acch_ctx *ctx);
+acch_status nccl_halo(acch_ctx *ctx, double *vec, long long plane, int depth);
+acch_status comm_allreduce_dev(acch_ctx *ctx, double *dev, int n, int op);   // in place on ctx->stream
+acch_status nccl_allreduce_host(acch_ctx *ctx, double *vals, int n, int op);
+void comm_release(acch_ctx *ctx);
 
 // Records a CUDA event pair around the launches in its scope when profiling is on.
 struct ProfScope {

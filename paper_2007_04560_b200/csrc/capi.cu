@@ -58,7 +58,9 @@ acch_status acch_fetch_results(acch_ctx *ctx, int count)
 
 acch_status comm_allreduce(acch_ctx *ctx, double *vals, int n, int op)
 {
-    if (ctx->nranks <= 1 || !ctx->allreduce || n <= 0) return ACCH_OK;
+    if (ctx->nranks <= 1 || n <= 0) return ACCH_OK;
+    if (ctx->nccl_comm) return nccl_allreduce_host(ctx, vals, n, op);
+    if (!ctx->allreduce) return ACCH_OK;
     if (ctx->allreduce(ctx->comm_user, vals, n, op) != 0) {
         g_last_error = "allreduce hook failed";
         return ACCH_ERR_CUDA;
@@ -68,9 +70,11 @@ acch_status comm_allreduce(acch_ctx *ctx, double *vals, int n, int op)
 
 acch_status comm_halo(acch_ctx *ctx, const double *vec, int doubles_per_cell, int depth)
 {
-    if (ctx->g.zg == 0 || !ctx->halo) return ACCH_OK;
-    ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->g.zg == 0) return ACCH_OK;
     const long long plane = (long long)doubles_per_cell * ctx->g.nx * ctx->g.ny;
+    if (ctx->nccl_comm) return nccl_halo(ctx, const_cast<double *>(vec), plane, depth);   // stream-ordered
+    if (!ctx->halo) return ACCH_OK;
+    ACCH_CUDA(cudaStreamSynchronize(ctx->stream));
     if (ctx->halo(ctx->comm_user, const_cast<double *>(vec), plane, ctx->g.nz, ctx->g.zg, depth) != 0) {
         g_last_error = "halo hook failed";
         return ACCH_ERR_CUDA;
@@ -205,6 +209,7 @@ acch_status acch_ctx_destroy(acch_ctx *ctx)
 {
     if (!ctx) return ACCH_OK;
     cudaSetDevice(ctx->device);
+    comm_release(ctx);
     cudaFree(ctx->d_partials);
     cudaFree(ctx->d_counter);
     cudaFree(ctx->d_result);

@@ -597,7 +597,7 @@ template <int NS>
 __global__ void __launch_bounds__(kRedThreads)
 lagupd_dev_kernel(const double *__restrict__ V, long long ld, int J, GmState *st, const double *__restrict__ d,
                   double *__restrict__ U, double *__restrict__ W, long long n, double *partials,
-                  unsigned int *counter, double *result, int *status, int zero)
+                  unsigned int *counter, double *result, int *status, int do_hess, int zero)
 {
     if (__ldcg(&st->stop)) return;
     __shared__ double sh[NS], sp[NS];
@@ -647,10 +647,20 @@ lagupd_dev_kernel(const double *__restrict__ V, long long ld, int J, GmState *st
     int ops[NS + 1];
 #pragma unroll
     for (int s = 0; s <= NS; ++s) ops[s] = RED_SUM;
-    if (!reduce_finish<NS + 1>(acc, ops, partials, counter, result)) return;
+    if (!reduce_finish<NS + 1>(acc, ops, partials, counter, result) || !do_hess) return;
     __syncthreads();   // result[] (thread 0) visible to the block
     gm_hess_step(st, J, d, result, NS, status);
 }
+
+// the same column step as a kernel of its own (N > 1: after the allreduce of
+// the multi-dot and of the lagged-pass projections)
+__global__ void gm_hess_kernel(GmState *st, int j, const double *d, const double *e, int vslot, int *status)
+{
+    if (__ldcg(&st->stop)) return;
+    gm_hess_step(st, j, d, e, vslot, status);
+}
+
+__device__ void gm_lost_finish(GmState *st, int m, const double *norm2, int *status);
 
 // Explicit second pass when the lagged identity is unusable (st->lost):
 // w -= V h2n, ||w||^2, then the column is finished with the measured norm.
@@ -659,7 +669,7 @@ lagupd_dev_kernel(const double *__restrict__ V, long long ld, int J, GmState *st
 template <int NS>
 __global__ void __launch_bounds__(kRedThreads)
 gm_lost_kernel(const double *__restrict__ V, long long ld, int m, GmState *st, double *__restrict__ w, long long n,
-               double *partials, unsigned int *counter, double *result, int *status)
+               double *partials, unsigned int *counter, double *result, int *status, int do_finish)
 {
     if (__ldcg(&st->stop) || !__ldcg(&st->lost)) return;
     __shared__ double sh[NS];
@@ -682,17 +692,29 @@ gm_lost_kernel(const double *__restrict__ V, long long ld, int m, GmState *st, d
     }
     double v1[1] = {acc};
     const int ops[1] = {RED_SUM};
-    if (!reduce_finish<1>(v1, ops, partials, counter, result)) return;
+    if (!reduce_finish<1>(v1, ops, partials, counter, result) || !do_finish) return;
     __syncthreads();
+    gm_lost_finish(st, m, result, status);
+}
+
+// finish of the explicit second pass from ||w||^2 in norm2[0] (whole block)
+__device__ void gm_lost_finish(GmState *st, int m, const double *norm2, int *status)
+{
     __shared__ double s_na;
     if (threadIdx.x == 0) {
-        s_na = sqrt(result[0]);
+        s_na = sqrt(norm2[0]);
         for (int q = 0; q <= GM_R; ++q) st->h2p[q] = 0.0;
         st->beta_p = s_na > 0.0 ? s_na : 1.0;
         st->lost = 0;
     }
     __syncthreads();
     gm_finish_column(st, m - 1, s_na, status);
+}
+
+__global__ void gm_lost_finish_kernel(GmState *st, int m, const double *norm2, int *status)
+{
+    if (__ldcg(&st->stop) || !__ldcg(&st->lost)) return;
+    gm_lost_finish(st, m, norm2, status);
 }
 
 __global__ void gm_init_kernel(GmState *st, double res_norm, double tol, int total, int max_it, int restart, int keepz)
@@ -1025,7 +1047,9 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
     // nv: stored vector length (column stride); [off, off + ni): this rank's
     // interior, the only part that enters dots and norms
     const long long nv = 2 * ctx->g.nstore, off = 2 * ctx->g.zoff, ni = 2 * ctx->g.n;
-    const bool multi = ctx->nranks > 1;
+    // with an NCCL communicator every reduction goes through it (also at one
+    // rank, where the allreduce is a copy: the N > 1 code path stays tested)
+    const bool multi = ctx->nranks > 1 || comm_has_nccl(ctx);
     double *V = ctx->d_krylov;
     double *Z = ctx->d_work, *R = ctx->d_work + nv, *T = ctx->d_work + 2 * nv;
     double *dh = ctx->d_h;      // [0..63] scratch for dots
@@ -1101,7 +1125,7 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
     auto tz = [&](int i, int j) -> double & { return Tz[i * restart + j]; };
     auto zcol = [&](int j) { return ctx->d_zbasis + (long long)j * nv; };
 
-    if (ortho == 2 && !multi) {
+    if (ortho == 2 && (!multi || comm_has_nccl(ctx))) {
         // ---- device-resident cycles (see GmState) ----
         TRY(ensure_gm(ctx));
         GmState *st = reinterpret_cast<GmState *>(ctx->d_gm);
@@ -1139,11 +1163,14 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                 TRY(matvec(zj, w));
                 int ns = 0;
                 TRY(mdot_to(ctx, V + off, nv, j + 1, w + off, ni, dh, &ns));
+                if (multi) TRY(comm_allreduce_dev(ctx, dh, 4 * (MG + 1), 0));
+                int vslot = 0;
                 {
                     ProfScope ps(ctx, PC_KUPDATE, 8.0 * (j + 4) * ni);
                     const int G = rgrid(ni);
-#define LAGD(NS) lagupd_dev_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V + off, nv, j, st, dh, col(j) + off, \
-                     w + off, ni, ctx->d_partials, ctx->d_counter, dh + 64, ctx->d_gm_status, 0)
+#define LAGD(NS) do { lagupd_dev_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V + off, nv, j, st, dh, col(j) + off, \
+                     w + off, ni, ctx->d_partials, ctx->d_counter, dh + 64, ctx->d_gm_status, multi ? 0 : 1, 0); \
+                     vslot = NS; } while (0)
                     if (j + 1 <= 4) LAGD(4);
                     else if (j + 1 <= 8) LAGD(8);
                     else if (j + 1 <= 16) LAGD(16);
@@ -1152,16 +1179,29 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
 #undef LAGD
                     ACCH_LAUNCHED(ctx);
                 }
+                if (multi) {
+                    // Hessenberg column from the rank-combined projections
+                    TRY(comm_allreduce_dev(ctx, dh + 64, 33, 0));
+                    gm_hess_kernel<<<1, kRedThreads, 0, ctx->stream>>>(st, j, dh, dh + 64, vslot, ctx->d_gm_status);
+                    ACCH_LAUNCHED(ctx);
+                }
                 {
                     ProfScope ps(ctx, PC_KUPDATE, 0.0);
                     const int G = rgrid(ni);
 #define LOSTK(NS) gm_lost_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V + off, nv, j + 1, st, w + off, ni, \
-                      ctx->d_partials, ctx->d_counter, dh + 40, ctx->d_gm_status)
+                      ctx->d_partials, ctx->d_counter, dh + 40, ctx->d_gm_status, multi ? 0 : 1)
                     if (j + 1 <= 4) LOSTK(4);
                     else if (j + 1 <= 8) LOSTK(8);
                     else if (j + 1 <= 16) LOSTK(16);
                     else LOSTK(32);
 #undef LOSTK
+                    ACCH_LAUNCHED(ctx);
+                }
+                if (multi) {
+                    // (issued every step on every rank: collectives must match; the
+                    // finish kernel returns unless the explicit pass ran)
+                    TRY(comm_allreduce_dev(ctx, dh + 40, 1, 0));
+                    gm_lost_finish_kernel<<<1, kRedThreads, 0, ctx->stream>>>(st, j + 1, dh + 40, ctx->d_gm_status);
                     ACCH_LAUNCHED(ctx);
                 }
                 return ACCH_OK;

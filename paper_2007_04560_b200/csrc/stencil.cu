@@ -107,6 +107,92 @@ __device__ __forceinline__ double chord_fast(double a, double b, const ParamsDev
     return (entropy(a) - entropy(b)) / (a - b);
 }
 
+// ---------------------------------------------------------------------------
+// Residual chord, warp-cooperative (res_zm_kernel).  Same branch predicates
+// as entropy_chord (physics.py:193-200, 240-261).  Cost cuts:
+//  * ln z - ln(1 - z) = 2 atanh(s) with s = 2 z - 1 (exact for z >= 1/4):
+//    for |s| <= 0.2 an odd series in s with coefficients 1/(2k+1) from the
+//    constant bank (no log call, no 64-bit immediates); libdevice log only
+//    for |s| > 0.2;
+//  * the chord's series P(t), t = (sigma/z)^2, is cut after 4 terms when no
+//    lane of the warp has t > 6.3e-5 (the dropped tail is below 2^-60 of the
+//    leading term, far under one rounding of the sum: the value is that of
+//    the full series up to the last-bit rounding of its partial sums) --
+//    always the case for Newton iterates near U^n -- else all S terms;
+//  * one reciprocal 1/(z (1 - z)) for both ratios.
+// All lanes of a warp must call it together.
+// ---------------------------------------------------------------------------
+__constant__ double c_atanh[12] = {1.0,        1.0 / 3.0,  1.0 / 5.0,  1.0 / 7.0,  1.0 / 9.0,  1.0 / 11.0,
+                                   1.0 / 13.0, 1.0 / 15.0, 1.0 / 17.0, 1.0 / 19.0, 1.0 / 21.0, 1.0 / 23.0};
+
+// q = sum_{k=1}^{K-1} x^{k-1} / (2k+1), Horner from the top (K compile-time)
+template <int K>
+__device__ __forceinline__ double atanh_tail(double x)
+{
+    double q = c_atanh[K - 1];
+#pragma unroll
+    for (int k = K - 2; k >= 1; --k) q = fma(q, x, c_atanh[k]);
+    return q;
+}
+
+// P(t)/t = sum_{s=1}^{K} t^{s-1} c1[s-1], Horner from the top
+template <int K>
+__device__ __forceinline__ void chord_poly2(double tz, double tw, const ParamsDev &P, double &pz, double &pw)
+{
+    pz = P.c1[K - 1];
+    pw = P.c1[K - 1];
+#pragma unroll
+    for (int s = K - 2; s >= 0; --s) {
+        pz = fma(pz, tz, P.c1[s]);
+        pw = fma(pw, tw, P.c1[s]);
+    }
+}
+
+
+// cell_gap with plain compare-selects (NaN in u or v -> NaN, then -inf in
+// the caller's reduction, as physics.py:107-108)
+__device__ __forceinline__ double cell_gap_fast(double u, double v)
+{
+    const double p = u + v, q = u - v;
+    double g = u;
+    const double c[7] = {1.0 - u, p, 1.0 - p, q, 1.0 - q, 0.5 - v, 0.5 + v};
+#pragma unroll
+    for (int k = 0; k < 7; ++k) g = c[k] < g ? c[k] : g;
+    return (v != v) ? v : g;
+}
+
+template <int ORDER>
+__device__ __forceinline__ double chord_res(double a, double b, const ParamsDev &P)
+{
+    static_assert(ORDER == 10, "short series: the reference's default order");
+    const double zeta = 0.5 * (a + b);
+    const double sigma = 0.5 * (a - b);
+    const double w = 1.0 - zeta;
+    const double s = 2.0 * zeta - 1.0;
+    const double s2 = s * s;
+    // ln(zeta) - ln(1 - zeta) = 2 atanh(s): 12 terms for |s| <= 0.2025
+    double lg;
+    if (s2 <= 0.0410) lg = fma(2.0 * s * s2, atanh_tail<12>(s2), 2.0 * s);
+    else lg = log(zeta) - log1p(-zeta);                 // far from 1/2: libdevice
+    const bool exact = sigma == 0.0;                    // exact branch (physics.py:245-247): lg
+    const double as = fabs(sigma);
+    const bool near = !exact && as <= 0.4 * zeta && as <= 0.4 * w;   // 0.4 min(zeta, 1 - zeta)
+    double val = lg;
+    if (__any_sync(0xffffffffu, near)) {
+        const double r = 1.0 / (zeta * w);              // 1/zeta = w r, 1/w = zeta r
+        const double rz = sigma * (w * r), rw = sigma * (zeta * r);
+        const double tz = rz * rz, tw = rw * rw;
+        double pz, pw;
+        // Newton iterates sit close to U^n: t = (sigma/z)^2 is tiny and 4
+        // terms leave a tail below 2^-60 of the sum (t <= 6.3e-5)
+        if (!__any_sync(0xffffffffu, near && (tz > 6.3e-5 || tw > 6.3e-5))) chord_poly2<4>(tz, tw, P, pz, pw);
+        else chord_poly2<ORDER>(tz, tw, P, pz, pw);
+        if (near) val = lg - pz * tz + pw * tw;
+    }
+    if (!exact && !near) val = (entropy(a) - entropy(b)) / (a - b);   // direct quotient (physics.py:259-261)
+    return val;
+}
+
 template <int DIM, int TX, int TY>
 __global__ void __launch_bounds__(TX *TY)
 residual_kernel(GridDev g, ParamsDev P, double dt, const double2 *__restrict__ xo_g,
@@ -311,6 +397,9 @@ res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__re
     const int zb = (int)(((long long)blockIdx.z * g.nz) / nchunk);
     const int ze = (int)(((long long)(blockIdx.z + 1) * g.nz) / nchunk);
     const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
+    const double c2lap = 2.0 * (ihx + ihy + ihz);
+    const double ha = -0.5 * P.alpha, hb = -0.5 * P.beta, hg = 0.5 * P.gamma;
+    const double idt = 1.0 / dt, irho = 1.0 / P.rho;
 
     int woff[NWR];
 #pragma unroll
@@ -373,28 +462,27 @@ res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__re
                 const double2 nxm = N1[h - 1], nxp = N1[h + 1], nym = N1[h - HX], nyp = N1[h + HX];
                 const double2 oxm = O1[h - 1], oxp = O1[h + 1], oym = O1[h - HX], oyp = O1[h + HX];
                 const double2 nzp = N2[h], ozp = O2[h];
-                // Laplacians, axes summed x, y, z (grid.py:263-271)
-                double lun = (nxp.x - 2.0 * n0.x + nxm.x) * ihx;
-                double lvn = (nxp.y - 2.0 * n0.y + nxm.y) * ihx;
-                double luo = (oxp.x - 2.0 * o0.x + oxm.x) * ihx;
-                double lvo = (oxp.y - 2.0 * o0.y + oxm.y) * ihx;
-                lun += (nyp.x - 2.0 * n0.x + nym.x) * ihy;
-                lvn += (nyp.y - 2.0 * n0.y + nym.y) * ihy;
-                luo += (oyp.x - 2.0 * o0.x + oym.x) * ihy;
-                lvo += (oyp.y - 2.0 * o0.y + oym.y) * ihy;
-                lun += (nzp.x - 2.0 * n0.x + nz[j].x) * ihz;
-                lvn += (nzp.y - 2.0 * n0.y + nz[j].y) * ihz;
-                luo += (ozp.x - 2.0 * o0.x + oz[j].x) * ihz;
-                lvo += (ozp.y - 2.0 * o0.y + oz[j].y) * ihz;
-                const double phi = chord_fast<ORDER>(n0.x + n0.y, o0.x + o0.y, P);
-                const double psi = chord_fast<ORDER>(n0.x - n0.y, o0.x - o0.y, P);
-                const double Gu = -0.5 * P.alpha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) - 0.5 * P.gamma * (lun + luo);
+                // Laplacians of U' + U^n (the DVD needs only their sum,
+                // scheme.py:277-286): neighbour pairs per axis, one centre term
+                const double lu = (nxp.x + nxm.x + (oxp.x + oxm.x)) * ihx + (nyp.x + nym.x + (oyp.x + oym.x)) * ihy +
+                                  (nzp.x + nz[j].x + (ozp.x + oz[j].x)) * ihz - c2lap * (n0.x + o0.x);
+                const double lv = (nxp.y + nxm.y + (oxp.y + oxm.y)) * ihx + (nyp.y + nym.y + (oyp.y + oym.y)) * ihy +
+                                  (nzp.y + nz[j].y + (ozp.y + oz[j].y)) * ihz - c2lap * (n0.y + o0.y);
+                double phi, psi;
+                if constexpr (ORDER == 10) {
+                    phi = chord_res<ORDER>(n0.x + n0.y, o0.x + o0.y, P);
+                    psi = chord_res<ORDER>(n0.x - n0.y, o0.x - o0.y, P);
+                } else {
+                    phi = chord_fast<0>(n0.x + n0.y, o0.x + o0.y, P);
+                    psi = chord_fast<0>(n0.x - n0.y, o0.x - o0.y, P);
+                }
+                const double Gu = ha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) - hg * lu;
                 const double cb = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
                 sB[sb * NB + gc[j]] = make_double2(Gu, cb);
                 nz[j] = n0;
                 oz[j] = o0;
                 if (j == 0) {
-                    gvk1 = -0.5 * P.beta * (n0.y + o0.y) + P.theta * (phi - psi) - 0.5 * P.gamma * (lvn + lvo);
+                    gvk1 = hb * (n0.y + o0.y) + P.theta * (phi - psi) - hg * lv;
                     nk1 = n0;
                     ok1 = o0;
                 }
@@ -467,11 +555,11 @@ res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__re
                 div += (fp - fm) * ihz;
             }
             double2 f;
-            f.x = (nk.x - ok_.x) / dt - div;
-            f.y = (nk.y - ok_.y) / dt + (C0 / P.rho) * gvk;
+            f.x = (nk.x - ok_.x) * idt - div;
+            f.y = (nk.y - ok_.y) * idt + (C0 * irho) * gvk;
             F[poff(z0) + coff[0]] = f;
             acc_norm += f.x * f.x + f.y * f.y;
-            acc_gap = red_combine(acc_gap, cell_gap(nk.x, nk.y), RED_MIN);
+            acc_gap = red_combine(acc_gap, cell_gap_fast(nk.x, nk.y), RED_MIN);
         }
         nk = nk1;
         ok_ = ok1;

@@ -7,9 +7,12 @@ radius-2 stencils by composition), and combines every reduction across ranks.
 The library calls two host hooks (include/acch_b200.h, acch_set_comm): a halo
 exchange of ghost planes and an allreduce of partial sums / minima.
 
-Two communicators implement the hooks:
-* ``TorchDistComm`` -- torch.distributed point-to-point + all_reduce (NCCL
-  over NVLink on GPUs, gloo on CPU tensors), one process per GPU;
+Communicators:
+* ``NcclComm`` -- the production data plane: the library itself runs NCCL
+  send / recv of ghost planes and all-reduces on its stream (csrc/comm.cu),
+  one process per GPU; the GMRES Arnoldi loop stays device-resident;
+* ``TorchDistComm`` -- host hooks through torch.distributed point-to-point +
+  all_reduce (NCCL over NVLink on GPUs, gloo on CPU tensors);
 * ``ThreadComm`` -- ranks emulated as threads of one process (each with its
   own context and stream on one GPU), for validating the decomposition
   without several GPUs.  Ranks only meet in host-side barriers; no kernel
@@ -218,6 +221,71 @@ class TorchDistComm(Comm):
             torch.cuda.current_stream(vec.device).synchronize()
 
 
+def nccl_library_path() -> str | None:
+    """The libnccl torch.distributed uses (its pip wheel), or None (then the
+    library dlopens "libnccl.so.2", which resolves to the copy already loaded
+    into the process)."""
+    try:
+        import nvidia.nccl
+        import os
+        base = list(nvidia.nccl.__path__)[0]
+        path = os.path.join(base, "lib", "libnccl.so.2")
+        return path if os.path.exists(path) else None
+    except Exception:
+        return None
+
+
+class NcclComm(Comm):
+    """The in-library NCCL data plane (csrc/comm.cu): every context on a slab
+    grid bound to this communicator gets its own NCCL communicator, created
+    collectively -- rank 0 draws an ncclUniqueId, torch.distributed
+    broadcasts it (any backend: gloo on CPU works), every rank calls
+    acch_set_nccl.  Halos and reductions then run as NCCL operations on the
+    library's stream; nothing comes back to Python per exchange."""
+
+    native = True
+
+    def __init__(self, periodic: bool, group=None, nccl_path: str | None = None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.nccl_path = nccl_path if nccl_path is not None else nccl_library_path()
+        super().__init__(dist.get_world_size(group), dist.get_rank(group), periodic)
+
+    def unique_id(self) -> bytes:
+        """A fresh ncclUniqueId, identical on every rank (collective)."""
+        import ctypes
+        from . import _native as nat
+        L = nat.lib()
+        nbytes = int(L.acch_nccl_id_bytes())
+        buf = torch.zeros(nbytes, dtype=torch.uint8)
+        if self.rank == 0:
+            raw = (ctypes.c_char * nbytes)()
+            path = self.nccl_path.encode() if self.nccl_path else None
+            nat.check(L.acch_nccl_unique_id(path, raw), "acch_nccl_unique_id")
+            buf.copy_(torch.frombuffer(bytearray(raw.raw), dtype=torch.uint8))
+        dev_bcast = self.dist.get_backend(self.group) == "nccl"
+        t = buf.cuda() if dev_bcast else buf
+        src = self.dist.get_global_rank(self.group, 0) if self.group is not None else 0
+        self.dist.broadcast(t, src=src, group=self.group)
+        return bytes(t.cpu().numpy().tobytes())
+
+    def bind(self, ctx_handle) -> None:
+        """Collective: give the context its NCCL communicator."""
+        import ctypes
+        from . import _native as nat
+        uid = self.unique_id()
+        path = self.nccl_path.encode() if self.nccl_path else None
+        nat.check(nat.lib().acch_set_nccl(ctx_handle, path, ctypes.c_char_p(uid), self.nranks, self.rank),
+                  "acch_set_nccl")
+
+    def allreduce(self, values: np.ndarray, op: str) -> None:   # pragma: no cover - the library reduces itself
+        raise RuntimeError("NcclComm reduces inside the library")
+
+    def halo(self, vec, plane, nz, zg, depth) -> None:           # pragma: no cover
+        raise RuntimeError("NcclComm exchanges inside the library")
+
+
 class ThreadGroup:
     """Shared state of ranks emulated as threads of one process."""
 
@@ -284,5 +352,5 @@ def comm_for(slab: SlabGrid) -> Comm | None:
     return _comms.get(slab)
 
 
-__all__ = ["SlabGrid", "split_grid", "local_fields", "Comm", "TorchDistComm", "ThreadGroup", "ThreadComm",
-           "bind_comm", "comm_for"]
+__all__ = ["SlabGrid", "split_grid", "local_fields", "Comm", "TorchDistComm", "NcclComm", "ThreadGroup",
+           "ThreadComm", "bind_comm", "comm_for", "nccl_library_path"]

@@ -226,6 +226,33 @@ def sim_case(tag, counts, bc, center, amp, mode, dt, horizon, nsub, solver="ilu0
     print(f"  {tag}: {res.status}, {len(h) - 1} steps, {wall:.1f} s, divergences {res.controller.divergence_count}")
 
 
+def io_case():
+    """History CSV and VTK bytes written by the reference's cli/io.py."""
+    import tempfile
+    from acch.cli.io import HistoryRow, write_history, write_vtk
+    from acch.grid import Field
+    rng = np.random.default_rng(77)
+    rows = [HistoryRow(k, 0.1 * k + 1e-17 * k, 1e-4 * (k + 1), 0.36 + rng.standard_normal() * 1e-3,
+                       0.5 + 1e-13 * k, abs(rng.standard_normal()), 2 + k % 2, 10 * k, 1e-3 * k) for k in range(5)]
+    out = {"rows": np.array([[r.step, r.time, r.dt, r.energy, r.mass_u, r.max_abs_v, r.newton, r.gmres, r.wall_s]
+                             for r in rows])}
+    with tempfile.TemporaryDirectory() as d:
+        write_history(rows, os.path.join(d, "h.csv"))
+        out["csv"] = np.array(open(os.path.join(d, "h.csv")).read())
+        for tag, counts in (("2d", (7, 5)), ("3d", (5, 4, 6))):
+            grid = Grid(counts, tuple(0.5 + 0.25 * a for a in range(len(counts))), BoundaryCondition.PERIODIC)
+            u = 0.5 + rng.uniform(-0.2, 0.2, grid.array_shape)
+            v = rng.uniform(-0.2, 0.2, grid.array_shape)
+            st = State(Field.from_interior(grid, u), Field.from_interior(grid, v))
+            write_vtk(st, os.path.join(d, f"{tag}.vtk"), title=f"snapshot {tag}")
+            out[f"vtk_{tag}"] = np.array(open(os.path.join(d, f"{tag}.vtk")).read())
+            out[f"u_{tag}"] = u
+            out[f"v_{tag}"] = v
+            out[f"counts_{tag}"] = np.array(counts)
+            out[f"lengths_{tag}"] = np.array(grid.lengths)
+    save("io.npz", **out)
+
+
 def main():
     which = set(sys.argv[1:])
 
@@ -234,6 +261,8 @@ def main():
 
     if want("chord"):
         chord_battery()
+    if want("io"):
+        io_case()
     if want("stencil"):
         stencil_case("2d_neu", (8, 6), "neumann", 1, 1e-3)
         stencil_case("2d_per", (8, 6), "periodic", 2, 1e-3)

@@ -169,3 +169,41 @@ def test_thread_comm_halo_and_allreduce(nranks, periodic):
         if "top" in exp:
             np.testing.assert_array_equal(got[r][(zg + nz) * plane:], exp["top"])
         assert sums[r][0] == sum(range(nranks))
+
+
+def _nccl_id_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2007_04560_b200.slab import NcclComm
+        comm = NcclComm(periodic=True)
+        ids = [comm.unique_id(), comm.unique_id()]
+        q.put((rank, ids, comm.lower(), comm.upper(), comm.nccl_path))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_nccl_unique_id_is_shared_over_gloo():
+    """The in-library NCCL data plane's bootstrap on 2 CPU processes: rank 0
+    draws an ncclUniqueId (dlopen of libnccl, no GPU needed), the gloo group
+    broadcasts it, both ranks hold identical bytes; a second communicator gets
+    a fresh id; the neighbour ranks are the periodic wrap."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_nccl_id_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    out = {}
+    for _ in range(2):
+        rank, ids, lo, hi, path = q.get(timeout=120)
+        out[rank] = (ids, lo, hi)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    ids0, ids1 = out[0][0], out[1][0]
+    assert len(ids0[0]) == 128 and ids0 == ids1 and ids0[0] != ids0[1]
+    assert out[0][1:] == (1, 1) and out[1][1:] == (0, 0)
