@@ -60,9 +60,6 @@ def parse_args():
     ap.add_argument("--variant", default="ras-left")
     ap.add_argument("--restart", type=int, default=30)
     ap.add_argument("--ortho", default="dcgs2", choices=["cgs2", "dcgs2", "mgs"])
-    ap.add_argument("--factor-storage", default="f64", choices=["f64", "f32"],
-                    help="f32: opt-in fp32 copy of the fp64 ILU factors read by the Schwarz apply (experiment; "
-                         "not the headline configuration)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-micro", action="store_true", help="reference arm: skip the full-size microbenchmarks")
@@ -159,8 +156,7 @@ def make_config(args, world=1, rank=0):
 
 def workload_name(args):
     return (f"AC/CH {args.dim}D {args.n}^{args.dim} periodic fp64, adaptive dt (eta=1e2), NKS: Newton + "
-            f"GMRES({args.restart}) + {args.variant} {args.box}^{args.dim}-cell boxes overlap 1 {args.solver}"
-            + (" (factors stored fp32, opt-in)" if getattr(args, "factor_storage", "f64") == "f32" else ""))
+            f"GMRES({args.restart}) + {args.variant} {args.box}^{args.dim}-cell boxes overlap 1 {args.solver}")
 
 
 # ---------------------------------------------------------------------------
@@ -680,8 +676,6 @@ def run_ours(args):
 
 def main():
     args = parse_args()
-    if args.factor_storage == "f32":
-        os.environ["ACCH_FACTOR_F32"] = "1"
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -364,106 +364,6 @@ lagupd_kernel(const double *__restrict__ V, long long ld, int J, const double *_
     reduce_finish<NS + 1>(acc, ops, partials, counter, result);
 }
 
-// The lagged pass for 16 < J + 1 <= 32 with an element per lane pair (as
-// mupdate_mdot32_kernel): the even lane holds V_0..V_15, the odd V_16..;
-// the halves of V h2 and V p are exchanged by shuffles.  <v_j, x> is
-// returned in result[32].
-#ifndef ACCH_LAG32_MINB
-#define ACCH_LAG32_MINB 2
-#endif
-__global__ void __launch_bounds__(kRedThreads, ACCH_LAG32_MINB)
-lagupd32_kernel(const double *__restrict__ V, long long ld, int J, const double *__restrict__ h2,
-                const double *__restrict__ d, double beta, double *__restrict__ U, double *__restrict__ W, long long n,
-                double *partials, unsigned int *counter, double *result, int zero)
-{
-    constexpr int H = 16, NV = 2 * H + 1;   // norm + 32 dots
-    __shared__ double sh[2 * H + 1], sp[2 * H + 1];
-    __shared__ double red[kRedThreads / 32][2][H + 1];
-    __shared__ bool is_last;
-    lag_coeffs(J, h2, d, beta, sh, sp, 2 * H + 1);
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, half = threadIdx.x & 1;
-    const int s0 = half * H;
-    double acc[H + 1];
-#pragma unroll
-    for (int k = 0; k <= H; ++k) acc[k] = 0.0;
-    const long long n2 = n >> 1;
-    double2 *__restrict__ u2 = reinterpret_cast<double2 *>(U);
-    double2 *__restrict__ w2 = reinterpret_cast<double2 *>(W);
-    const long long pairs = (long long)gridDim.x * (blockDim.x >> 1);
-    for (long long base = blockIdx.x * (long long)(blockDim.x >> 1) + warp * 16; base < n2; base += pairs) {
-        const long long i = base + (lane >> 1);
-        const bool ok = i < n2;
-        double2 v[H];
-#pragma unroll
-        for (int k = 0; k < H; ++k)
-            v[k] = ldg2_pred(reinterpret_cast<const double2 *>(V + (s0 + k) * ld) + i, ok && s0 + k < J);
-        double2 u = ok ? u2[i] : make_double2(0.0, 0.0), x = ok ? w2[i] : make_double2(0.0, 0.0);
-        const int a0 = anchor(v[H - 1], zero);
-        double2 ph = make_double2(0.0, 0.0), pp = make_double2(0.0, 0.0);   // halves of V h2, V p
-#pragma unroll
-        for (int k = 0; k < H; ++k)
-            if (s0 + k < J) {
-                const double hs = sh[s0 + k + (k == 0 ? a0 : 0)], ps = sp[s0 + k];
-                ph.x += hs * v[k].x;
-                ph.y += hs * v[k].y;
-                pp.x += ps * v[k].x;
-                pp.y += ps * v[k].y;
-            }
-        double2 oh, op;
-        oh.x = __shfl_xor_sync(0xffffffffu, ph.x, 1);
-        oh.y = __shfl_xor_sync(0xffffffffu, ph.y, 1);
-        op.x = __shfl_xor_sync(0xffffffffu, pp.x, 1);
-        op.y = __shfl_xor_sync(0xffffffffu, pp.y, 1);
-        const double2 hlo = half == 0 ? ph : oh, hhi = half == 0 ? oh : ph;
-        const double2 plo = half == 0 ? pp : op, phi = half == 0 ? op : pp;
-        u.x = ((u.x - hlo.x) - hhi.x) / beta;
-        u.y = ((u.y - hlo.y) - hhi.y) / beta;
-        const double pj = sp[J];
-        x.x = (((x.x - plo.x) - phi.x) - pj * u.x) / beta;
-        x.y = (((x.y - plo.y) - phi.y) - pj * u.y) / beta;
-        if (half == 1 && ok) {
-            u2[i] = u;
-            w2[i] = x;
-        }
-        if (half == 1) acc[0] += x.x * x.x + x.y * x.y;   // 0 when !ok
-#pragma unroll
-        for (int k = 0; k < H; ++k)
-            if (s0 + k < J) acc[1 + k] += v[k].x * x.x + v[k].y * x.y;
-        if (half == 1) acc[H] += u.x * x.x + u.y * x.y;   // <v_j, x> -> result[2H] (V_31's slot, unused: J <= 31)
-    }
-#pragma unroll
-    for (int off = 16; off >= 2; off >>= 1)
-#pragma unroll
-        for (int k = 0; k <= H; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], off);
-    if (lane < 2)
-#pragma unroll
-        for (int k = 0; k <= H; ++k) red[warp][lane][k] = acc[k];
-    __syncthreads();
-    const long long nb = gridDim.x;
-    if (threadIdx.x < NV) {
-        const int j = threadIdx.x;
-        const int hh = j == 0 ? 1 : (j - 1) / H, kk = j == 0 ? 0 : 1 + (j - 1) % H;
-        double t = 0.0;
-        for (int q = 0; q < kRedThreads / 32; ++q) t += red[q][hh][kk];
-        partials[j * nb + blockIdx.x] = t;
-    }
-    if (threadIdx.x == 0) {
-        __threadfence();
-        is_last = atomicAdd(counter, 1u) == (unsigned int)(nb - 1);
-    }
-    __syncthreads();
-    if (!is_last) return;
-    __threadfence();
-    if (threadIdx.x < NV) {
-        double t = 0.0;
-        for (long long b = 0; b < nb; ++b) t += __ldcg(partials + threadIdx.x * nb + b);
-        result[threadIdx.x] = t;
-    }
-    if (threadIdx.x == 0) *counter = 0u;
-}
-
-
 // ---------------------------------------------------------------------------
 // Device-resident Arnoldi state (ortho = 2, one rank).  The host queues the
 // kernels of each Arnoldi step without reading anything back; the Hessenberg
@@ -904,19 +804,14 @@ static acch_status lagupd_to(acch_ctx *ctx, const double *V, long long ld, int J
 #define LAG_CASE(NS) \
     lagupd_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V, ld, J, h2, d, beta, U, W, n, ctx->d_partials, \
                                                           ctx->d_counter, out, 0);
-    // one lane per element up to 32 vectors (measured 14% faster than the
-    // lane-pair form at J + 1 = 17..32; ACCH_LAG32=0 selects the pair form)
-    static const int single32 = getenv("ACCH_LAG32") ? atoi(getenv("ACCH_LAG32")) : 1;
+    // one lane per element up to 32 vectors (measured 14% faster than a
+    // lane-pair form at J + 1 = 17..32)
     if (J + 1 <= 4) { LAG_CASE(4) *vslot = 4; }
     else if (J + 1 <= 8) { LAG_CASE(8) *vslot = 8; }
     else if (J + 1 <= 16) { LAG_CASE(16) *vslot = 16; }
-    else if (J + 1 <= 24 && single32) { LAG_CASE(24) *vslot = 24; }
-    else if (J + 1 <= 32 && single32) { LAG_CASE(32) *vslot = 32; }
-    else if (J + 1 <= 32) {
-        *vslot = 32;
-        lagupd32_kernel<<<G, kRedThreads, 0, ctx->stream>>>(V, ld, J, h2, d, beta, U, W, n, ctx->d_partials,
-                                                             ctx->d_counter, out, 0);
-    } else { acch_set_error("lagged update: too many vectors"); return ACCH_ERR_INVALID_ARG; }
+    else if (J + 1 <= 24) { LAG_CASE(24) *vslot = 24; }
+    else if (J + 1 <= 32) { LAG_CASE(32) *vslot = 32; }
+    else { acch_set_error("lagged update: too many vectors"); return ACCH_ERR_INVALID_ARG; }
 #undef LAG_CASE
     ACCH_LAUNCHED(ctx);
     return ACCH_OK;
@@ -1186,8 +1081,10 @@ acch_status gmres_impl(acch_ctx *ctx, const double *coef, double dt, acch_precon
                     ACCH_LAUNCHED(ctx);
                 }
                 {
+                    // almost always a no-op (returns at once): one CTA per SM
+                    // keeps the empty launch cheap; grid-stride when it runs
                     ProfScope ps(ctx, PC_KUPDATE, 0.0);
-                    const int G = rgrid(ni);
+                    const int G = std::min(rgrid(ni), 148);
 #define LOSTK(NS) gm_lost_kernel<NS><<<G, kRedThreads, 0, ctx->stream>>>(V + off, nv, j + 1, st, w + off, ni, \
                       ctx->d_partials, ctx->d_counter, dh + 40, ctx->d_gm_status, multi ? 0 : 1)
                     if (j + 1 <= 4) LOSTK(4);

@@ -67,14 +67,6 @@ struct ClassDev {
     const int *lin;   // local cell -> storage offset from the box origin (boxes that do not wrap)
     const int *own_list;   // local ids of the owned cells, ascending
     int n_owned;
-    // row-local forms for factor_warp_kernel: J stencil entry -> index within
-    // the row's CSR pattern, update target -> index within row i's pattern
-    const int *jmap_local, *upd_dl;
-    int rmax;   // longest pattern row
-    // row-sequential batched solver (apply_rs_kernel): shared-memory image
-    // lenL[nloc] | lenU[nloc] | own[nloc] (uint8) | colL[nL] | colU[nU] (uint16) | rel x,y,z (int)
-    const unsigned char *rs_meta;
-    int rs_meta_bytes, rs_m_lenU, rs_m_own, rs_m_colL, rs_m_colU, rs_m_rel, rs_nL, rs_ring, rs_far;
     int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
     int m_lin, m_ixyz, m_own, m_rel;   // gather / scatter tables in the group image
     int jdup;   // some row has two stencil entries on one pattern position (tiny periodic axes)
@@ -90,17 +82,8 @@ struct ClassHost {
     std::vector<int2> upd;
     std::vector<unsigned char> owned;
     std::vector<unsigned char> meta;   // ClassDev::meta image
-    std::vector<int> lin, own_list, jmap_local, upd_dl;
-    // CSR-entry forms of jmap / upd (before the slot layout is applied) and
-    // the row-sequential layout: forward rows ascending (L entries), then
-    // backward rows descending ([inv D_i] + U entries)
-    std::vector<int> jmap_csr;
-    std::vector<int2> upd_csr;
-    std::vector<int> rs_pos;
-    std::vector<unsigned char> rs_meta;
-    int rs_ok = 0, rs_ring = 0, rs_nL = 0, rs_far = 0, rs_m[5] = {0};
+    std::vector<int> lin, own_list;
     int jdup = 0;
-    int rmax = 0;
     int m_off[17] = {0};
     int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
     void *dev_mem = nullptr;
@@ -280,101 +263,6 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
     }
 }
 
-// Warp-per-subdomain factorisation (default when a row fits the row buffer).
-// Lane q owns row q of the current level: its pattern row is assembled from
-// the 7 coefficient planes straight into a shared-memory row buffer (no
-// zero-fill pass over the factor array), eliminated there -- the IKJ updates
-// read the finished U rows of earlier levels from global memory (L2-resident:
-// a row reaches at most ~2 box planes back) in batches of 8 loads -- and
-// written to its factor slots once.  The factor array therefore sees one
-// write per block instead of a read-modify-write per update.
-template <int DIM, int NW>
-__global__ void __launch_bounds__(NW * 32)
-factor_warp_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
-                   const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
-                   const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
-                   double4 *__restrict__ vals, int *__restrict__ bad_row, long long nsub, int rstride, int ss)
-{
-    constexpr int NOFF = DIM == 3 ? 25 : 13;
-    constexpr int UB = 8;
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const long long s = (long long)blockIdx.x * NW + warp;
-    if (s >= nsub) return;
-    const ClassDev &C = classes[sub_class[s]];
-    const int4 o = sub_origin[s];
-    StridedBlocks A{vals + sub_off[s], ss};
-    // row buffer: entry j of the lane's row at rb[j * 32] (conflict-free across lanes)
-    double4 *rb = reinterpret_cast<double4 *>(smem_raw) + (size_t)warp * 32 * rstride + lane;
-    for (int lev = 0; lev < C.nlev; ++lev) {
-        const int q1 = C.lev_ptr[lev + 1];
-        for (int q0 = C.lev_ptr[lev]; q0 < q1; q0 += 32) {
-            const int q = q0 + lane;
-            if (q < q1) {
-                const int i = C.lev_rows[q];
-                const int r0 = C.rowptr[i], len = C.rowptr[i + 1] - r0, d = C.diag[i] - r0;
-                for (int j = 0; j < len; ++j) rb[j * 32] = make_double4(0.0, 0.0, 0.0, 0.0);
-                {
-                    // J's row straight into the row buffer (no local-memory block array)
-                    int gx, gy, gz;
-                    local_to_global(g, C, o, i, gx, gy, gz);
-                    const int *jm = C.jmap_local + i * NOFF;
-                    jac_row_emit<DIM>(g, P, dt, coef, gx, gy, gz, [&](int e, int comp, double v) {
-                        const int p = jm[e];
-                        if (p >= 0) reinterpret_cast<double *>(rb + p * 32)[comp] += v;
-                    });
-                }
-                for (int t = 0; t < d; ++t) {
-                    const int k = C.col[r0 + t];
-                    const double4 dk = A[C.pos[C.diag[k]]];   // row k: finished, inverted diagonal
-                    const double4 ak = rb[t * 32];
-                    const Blk L = mul({ak.x, ak.y, ak.z, ak.w}, {dk.x, dk.y, dk.z, dk.w});
-                    rb[t * 32] = make_double4(L.a, L.b, L.c, L.d);
-                    const int u1 = C.upd_ptr[r0 + t + 1];
-                    for (int u0 = C.upd_ptr[r0 + t]; u0 < u1; u0 += UB) {
-                        double4 us[UB];
-                        int dl[UB];
-#pragma unroll
-                        for (int b = 0; b < UB; ++b) {
-                            const bool ok = u0 + b < u1;
-                            dl[b] = ok ? C.upd_dl[u0 + b] : 0;
-                            us[b] = ok ? A[C.upd[u0 + b].x] : make_double4(0.0, 0.0, 0.0, 0.0);
-                        }
-#pragma unroll
-                        for (int b = 0; b < UB; ++b)
-                            if (u0 + b < u1) {
-                                const Blk m = mul(L, {us[b].x, us[b].y, us[b].z, us[b].w});
-                                double4 v = rb[dl[b] * 32];
-                                v.x -= m.a;
-                                v.y -= m.b;
-                                v.z -= m.c;
-                                v.w -= m.d;
-                                rb[dl[b] * 32] = v;
-                            }
-                    }
-                }
-                // diagonal block: scalar pivots as the reference's factor_inplace sees them
-                const double4 D = rb[d * 32];
-                const double p0 = D.x;
-                const double p1 = D.w - (D.z / D.x) * D.y;
-                int bad = -1;
-                if (fabs(p0) < 1e-300) bad = 2 * i;
-                else if (fabs(p1) < 1e-300) bad = 2 * i + 1;
-                if (bad >= 0) atomicMin(bad_row + s, bad);
-                const double det = D.x * D.w - D.y * D.z;
-                rb[d * 32] = make_double4(D.w / det, -D.y / det, -D.z / det, D.x / det);
-                for (int j = 0; j < len; ++j) A[C.pos[r0 + j]] = rb[j * 32];
-            }
-            __syncwarp();   // this level's rows are visible to the next level's lanes
-        }
-    }
-}
-
-// Level-scheduled forward (unit-L) and backward (U with inverted diagonal)
-// sweeps of one subdomain.  TPS threads cooperate on a subdomain: 32 (one
-// warp, __syncwarp between levels) for boxes whose levels are narrow, or the
-// whole CTA.  Factor slots are level-major, so the q-th row of a level reads
-// slot base + t*m + q: consecutive lanes touch consecutive 32-byte blocks.
 template <int TPS>
 __device__ __forceinline__ void level_sync()
 {
@@ -425,18 +313,7 @@ __device__ __forceinline__ void ldg4_pred(double4 &v, const double4 *p, bool pre
 // are swept warp-wide (sweep_rows_wide*, exact LU / high fill)
 constexpr int kWideRows = 4, kWideLen = 32;
 
-// fp32 copy of the factor blocks (opt-in mixed-precision storage, ACCH_FACTOR_F32=1):
-// one 128-bit load per block, widened exactly to fp64 at the FMA
-__device__ __forceinline__ void ldg4_pred(float4 &v, const float4 *p, bool pred, uint64_t pol)
-{
-    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %5, 0;\n\t"
-                 "@q ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %6;\n\t}"
-                 : "+f"(v.x), "+f"(v.y), "+f"(v.z), "+f"(v.w)
-                 : "l"(p), "r"((unsigned)pred), "l"(pol));
-}
-__device__ __forceinline__ float4 ldg4(const float4 *p) { return __ldg(p); }
 __device__ __forceinline__ int anchor_bits(const double4 &a) { return __double2hiint(a.x); }
-__device__ __forceinline__ int anchor_bits(const float4 &a) { return __float_as_int(a.x); }
 
 // acc -= a y for a 2x2 block, with the rounding pinned by intrinsics
 // (product, fused second product, subtraction): every solver and code path
@@ -445,10 +322,6 @@ __device__ __forceinline__ void blk_sub(double2 &acc, const double4 &a, const do
 {
     acc.x = __dsub_rn(acc.x, __fma_rn(a.y, y.y, __dmul_rn(a.x, y.x)));
     acc.y = __dsub_rn(acc.y, __fma_rn(a.w, y.y, __dmul_rn(a.z, y.x)));
-}
-__device__ __forceinline__ void blk_sub(double2 &acc, const float4 &a, const double2 &y)
-{
-    blk_sub(acc, make_double4(a.x, a.y, a.z, a.w), y);
 }
 
 template <int VARIANT, int TPS, int MAXW = 12>   // VARIANT: 0 asm, 1 ras-left, 2 ras-right
@@ -833,7 +706,7 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
 // load's result (masked by `zero`, a runtime 0 the compiler cannot fold), so
 // ptxas cannot start consuming loads 0..5 before it has issued loads 6..11 --
 // the interleaving that otherwise costs a second memory round trip per level.
-template <int MAXW, int DBG = 0, typename FT = double4>   // DBG (experiments only): 1 = no factor loads, 2 = no y dependency
+template <int MAXW, typename FT = double4>
 __device__ __forceinline__ void sweep_level(const FT *__restrict__ A, const unsigned short *__restrict__ ecol,
                                             const unsigned short *__restrict__ jo, double2 *y, int base, int m,
                                             int len0, int len1, int i0, int i1, bool backward, int lane, int zero,
@@ -851,8 +724,7 @@ __device__ __forceinline__ void sweep_level(const FT *__restrict__ A, const unsi
 #pragma unroll
     for (int t = 0; t < MAXW; ++t) {
         const int e = base + jo[t] + lane;
-        if constexpr (DBG == 1) a[t] = FT{1e-3 * e, 1e-3, 2e-3, 1e-3 * t};
-        else ldg4_pred(a[t], A + e, t < len0, pol);
+        ldg4_pred(a[t], A + e, t < len0, pol);
         c[t] = t < len0 ? ecol[e] : 0;
     }
     const int dep = anchor_bits(a[MAXW - 1]) & zero;
@@ -862,15 +734,6 @@ __device__ __forceinline__ void sweep_level(const FT *__restrict__ A, const unsi
 #pragma unroll
     for (int t = 0; t < MAXW; ++t)
         if (t < len0) blk_sub(acc0, a[t], y[c[t]]);
-    if (DBG == 2) {   // loads only: fold them into one value, no FMA chain on y
-        double sink = 0.0;
-#pragma unroll
-        for (int t = 0; t < MAXW; ++t)
-            if (t < len0) sink += a[t].x + a[t].w;
-        if (lane < m && sink == 12345.678) y[i0] = make_double2(sink, sink);
-        __syncwarp();
-        return;
-    }
     if (len1 > 0) {
 #pragma unroll
         for (int t = 0; t < MAXW; ++t)
@@ -968,7 +831,7 @@ __device__ __forceinline__ void sweep_rows_wide(const FT *__restrict__ A, const 
 }
 
 // one subdomain of a class group: gather, forward and backward sweeps, scatter
-template <int VARIANT, int MAXW, int DBG = 0, typename FT = double4, bool WIDE = false>
+template <int VARIANT, int MAXW, typename FT = double4, bool WIDE = false>
 __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev &C, const unsigned char *smem_meta,
                                              double2 *y, int s, const int4 *__restrict__ sub_origin,
                                              const long long *__restrict__ sub_off,
@@ -1061,7 +924,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         const int len1 = lane + 32 < m ? f_len[r0 + lane + 32] : 0;
         const int i0 = lane < m ? f_rows[r0 + lane] : 0;
         const int i1 = lane + 32 < m ? f_rows[r0 + lane + 32] : 0;
-        sweep_level<MAXW, DBG, FT>(A, ecol, f_jo + f_jp[lev], y, f_bs[lev], m, len0, len1, i0, i1, false, lane, zero, pol);
+        sweep_level<MAXW, FT>(A, ecol, f_jo + f_jp[lev], y, f_bs[lev], m, len0, len1, i0, i1, false, lane, zero, pol);
     }
     for (int lev = 0; lev < nlevb; ++lev) {
         if (lane == 0) prefetch_level(nlev + lev + pd);
@@ -1076,7 +939,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         const int len1 = lane + 32 < m ? b_len[r0 + lane + 32] - 1 : 0;
         const int i0 = lane < m ? b_rows[r0 + lane] : 0;
         const int i1 = lane + 32 < m ? b_rows[r0 + lane + 32] : 0;
-        sweep_level<MAXW, DBG, FT>(A, ecol, b_jo + b_jp[lev] + 1, y, b_bs[lev], m, len0, len1, i0, i1, true, lane, zero,
+        sweep_level<MAXW, FT>(A, ecol, b_jo + b_jp[lev] + 1, y, b_bs[lev], m, len0, len1, i0, i1, true, lane, zero,
                           pol);
     }
     if (VARIANT == 1) {
@@ -1092,7 +955,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     __syncwarp();   // y is reused by the warp's next subdomain
 }
 
-template <int VARIANT, int NW, int MAXW = 12, int DBG = 0, typename FT = double4, bool WIDE = false>
+template <int VARIANT, int NW, int MAXW = 12, typename FT = double4, bool WIDE = false>
 __global__ void __launch_bounds__(NW * 32, 1)
 apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *__restrict__ groups,
                    const int *__restrict__ grp_sub, const int4 *__restrict__ sub_origin,
@@ -1115,549 +978,10 @@ apply_group_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *
     // one subdomain per warp (a loop over several per warp measured slower:
     // it pushes the sweep past 255 registers into spills)
     if (warp < G.z)
-        group_solve_one<VARIANT, MAXW, DBG, FT, WIDE>(g, C, smem_raw, y, grp_sub[G.y + warp], sub_origin, sub_off,
+        group_solve_one<VARIANT, MAXW, FT, WIDE>(g, C, smem_raw, y, grp_sub[G.y + warp], sub_origin, sub_off,
                                            sub_ext_off, vals, r, z, ext_out, zero, pd);
 }
 
-// ---------------------------------------------------------------------------
-// Row-sequential batched solver (opt-in: ACCH_RS=1; measured slower than the
-// class-group solver at the bench size, kept as a tested alternative).
-//
-// A warp solves 8 subdomains of ONE class at once, row after row, with no
-// level schedule: lane = 8 q + b works on subdomain b and on the blocks
-// t = q, q + 4, q + 8 of the current row (rows have <= 12 blocks), and the
-// four partial sums of a row are combined by two shuffles.  Because the 8
-// subdomains share the class's pattern, every lane runs the same row at the
-// same time, and the factor blocks of a batch are stored slot-major and
-// subdomain-minor (slot p of subdomain b at batch_base + 8 p + b), so one
-// row's blocks are one contiguous, fully coalesced 1 KB stream per warp step.
-// Blocks are loaded RS_D rows ahead into registers; the solution values a
-// row reads (<= max|i - j| rows back / ahead) live in a per-warp shared
-// memory ring; the forward result y is kept in an L2-resident scratch
-// (one slot per resident warp, indexed by %smid) for the backward sweep.
-// ---------------------------------------------------------------------------
-
-constexpr int RS_B = 8;       // subdomains per warp
-#ifndef ACCH_RS_D
-#define ACCH_RS_D 3
-#endif
-constexpr int RS_D = ACCH_RS_D;   // rows of factor blocks in flight per warp
-constexpr int RS_PITCH = 9;   // ring row pitch in double2 (8 subdomains + 1: conflict-free gathers)
-
-// volatile: issued where written (RS_D rows ahead of its use), never sunk
-// toward the consuming FMA by the scheduler
-__device__ __forceinline__ double4 ldg_stream(const double4 *p, uint64_t pol)
-{
-    double4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
-        : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
-        : "l"(p), "l"(pol));
-    return v;
-}
-
-__device__ __forceinline__ unsigned smid()
-{
-    unsigned r;
-    asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
-    return r;
-}
-
-template <int VARIANT, int NW>
-__global__ void __launch_bounds__(NW * 32, 1)
-apply_rs_kernel(GridDev g, const ClassDev *__restrict__ classes, const int4 *__restrict__ items,
-                const int4 *__restrict__ batches, const long long *__restrict__ batch_base,
-                const int *__restrict__ members, const int4 *__restrict__ sub_origin,
-                const long long *__restrict__ sub_ext_off, const double4 *__restrict__ vals,
-                const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
-                double2 *__restrict__ scratch, int meta_pad, int ring_stride, int max_nloc, int pf_rows)
-{
-    ACCH_SKIP_IF(g);
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int4 it = items[blockIdx.x];   // (class, first batch, batches, -)
-    const ClassDev &C = classes[it.x];
-    {
-        const uint4 *__restrict__ src = reinterpret_cast<const uint4 *>(C.rs_meta);
-        uint4 *dst = reinterpret_cast<uint4 *>(smem_raw);
-        for (int i = threadIdx.x; i < C.rs_meta_bytes / 16; i += NW * 32) dst[i] = __ldg(src + i);
-    }
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (warp >= it.z) return;
-    const unsigned char *lenL = smem_raw, *lenU = smem_raw + C.rs_m_lenU, *own = smem_raw + C.rs_m_own;
-    const unsigned short *colL = reinterpret_cast<const unsigned short *>(smem_raw + C.rs_m_colL);
-    const unsigned short *colU = reinterpret_cast<const unsigned short *>(smem_raw + C.rs_m_colU);
-    const int *relx = reinterpret_cast<const int *>(smem_raw + C.rs_m_rel);
-    const int lx = C.len[0], ly = C.len[1], lz = C.len[2];
-    const int *rely = relx + lx, *relz = rely + ly;
-    const int nloc = C.nloc, R = C.rs_ring, nL = C.rs_nL;
-    const bool any_far = C.rs_far != 0;
-
-    const int4 bt = batches[it.y + warp];   // (first member, count, -, -)
-    const int b = lane & 7, q = lane >> 3;
-    const bool bval = b < bt.y;
-    const int s = members[bt.x + (bval ? b : 0)];
-    const int4 o = sub_origin[s];
-    const double4 *__restrict__ A = vals + batch_base[it.y + warp] + b;     // slot p at A[8 p]
-    double2 *ring = reinterpret_cast<double2 *>(smem_raw + meta_pad) + (size_t)warp * ring_stride + b;
-    double2 *scr = scratch + ((size_t)smid() * NW + warp) * (size_t)max_nloc * RS_B + b;   // row i at scr[8 i]
-    const uint64_t pol = evict_first_policy();
-
-    // column code -> operand index: ring element (>= 0) or, for a far
-    // column, ~(scratch element) (< 0)
-    auto operand = [&](unsigned code) -> int {
-        return (code & 0x8000u) ? ~(int)((code & 0x7fffu) * RS_B) : (int)code * RS_PITCH;
-    };
-    // sum over this lane's blocks of a row: acc -= blk * x[col]; blocks
-    // 12.. of a long row (block t at slot off + t, column code col[t]) are
-    // loaded here
-    auto row_sum = [&](double2 &acc, const double4 (&f)[3], const int (&c)[3], int len, bool far, int off,
-                       const unsigned short *col) {
-        if (!far) {
-#pragma unroll
-            for (int u = 0; u < 3; ++u)
-                if (4 * u + q < len) blk_sub(acc, f[u], ring[c[u]]);
-        } else {
-#pragma unroll
-            for (int u = 0; u < 3; ++u)
-                if (4 * u + q < len) blk_sub(acc, f[u], c[u] >= 0 ? ring[c[u]] : scr[~c[u]]);
-        }
-        for (int t = 12 + q; t < len; t += 4) {
-            const int cu = operand(col[t]);
-            blk_sub(acc, ldg_stream(A + (size_t)(off + t) * RS_B, pol), cu >= 0 ? ring[cu] : scr[~cu]);
-        }
-    };
-
-    // storage index of local cell (ix, iy, iz) of this lane's subdomain
-    auto cell = [&](int ix, int iy, int iz) -> long long {
-        int gx = o.x + relx[ix];
-        if (gx >= g.nx) gx -= g.nx;
-        int gy = o.y + rely[iy];
-        if (gy >= g.ny) gy -= g.ny;
-        int gz = 0;
-        if (g.dim == 3) {
-            gz = o.z + relz[iz];
-            if (g.zg == 0) gz = gz >= g.nz ? gz - g.nz : gz;
-            else gz += g.zg;
-        }
-        return ((long long)gz * g.ny + gy) * g.nx + gx;
-    };
-
-    // ---------------- forward sweep: y_i = r_i - sum_j L_ij y_j ----------------
-    double4 F[RS_D][3];
-    int Cc[RS_D][3];
-    double2 Rv[RS_D];
-    int ld_i = 0, ld_off = 0, lx_ = 0, ly_ = 0, lz_ = 0;
-    // every lane issues the same number of loads per row (a block past the
-    // row's end re-reads its last block), so the compiler can wait for a
-    // row's loads by count while the later rows' loads stay in flight
-    auto issue_fwd = [&](double4 (&f)[3], int (&c)[3], double2 &rv) {
-        if (ld_i < nloc) {
-            const int len = lenL[ld_i] & 0x7f;
-#pragma unroll
-            for (int u = 0; u < 3; ++u) {
-                const int t = 4 * u + q;
-                if (t < len) {   // (blocks 12.. of a long row: row_sum)
-                    f[u] = ldg_stream(A + (size_t)(ld_off + t) * RS_B, pol);
-                    c[u] = operand(colL[ld_off + t]);
-                }
-            }
-            const bool keep = VARIANT != 2 || own[ld_i];
-            rv = (bval && keep) ? r[cell(lx_, ly_, lz_)] : make_double2(0.0, 0.0);
-            ld_off += len;
-            ++ld_i;
-            if (++lx_ == lx) {
-                lx_ = 0;
-                if (++ly_ == ly) {
-                    ly_ = 0;
-                    ++lz_;
-                }
-            }
-        }
-    };
-    // the TMA engine pulls the batch's blocks pf_rows rows ahead into L2, so
-    // the register loads RS_D rows ahead hit L2
-    const char *Abatch = reinterpret_cast<const char *>(A - b);
-    int pf_i = 0, pf_off = 0;
-    auto prefetch_fwd = [&]() {
-        if (pf_i < nloc) {
-            const int len = lenL[pf_i] & 0x7f;
-            if (lane == 0 && len) prefetch_l2(Abatch + (size_t)pf_off * RS_B * 32, (unsigned)len * RS_B * 32);
-            pf_off += len;
-            ++pf_i;
-        }
-    };
-    for (int k = 0; k < pf_rows; ++k) prefetch_fwd();
-#pragma unroll
-    for (int st = 0; st < RS_D; ++st) issue_fwd(F[st], Cc[st], Rv[st]);
-    int ri = 0, off_c = 0;
-    for (int i0 = 0; i0 < nloc; i0 += RS_D) {
-#pragma unroll
-        for (int st = 0; st < RS_D; ++st) {
-            const int i = i0 + st;
-            if (i < nloc) {
-                const int lv = lenL[i];
-                double2 acc = make_double2(0.0, 0.0);
-                row_sum(acc, F[st], Cc[st], lv & 0x7f, (lv & 0x80) != 0, off_c, colL + off_c);
-                off_c += lv & 0x7f;
-                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
-                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
-                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
-                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
-                const double2 yi = make_double2(Rv[st].x + acc.x, Rv[st].y + acc.y);
-                if (q == 0) {
-                    ring[ri * RS_PITCH] = yi;
-                    scr[(size_t)i * RS_B] = yi;
-                }
-                ri = ri + 1 == R ? 0 : ri + 1;
-                issue_fwd(F[st], Cc[st], Rv[st]);
-                prefetch_fwd();
-                __syncwarp();
-            }
-        }
-    }
-
-    // ------------- backward sweep: x_i = inv(D_i) (y_i - sum_j U_ij x_j) -------------
-    double4 Di[RS_D];
-    double2 Yv[RS_D];
-    int bl_i = nloc - 1, bl_off = nL, bl_offu = 0;
-    auto issue_bwd = [&](double4 (&f)[3], int (&c)[3], double4 &di, double2 &yv) {
-        if (bl_i >= 0) {
-            const int len = lenU[bl_i] & 0x7f;
-            di = ldg_stream(A + (size_t)bl_off * RS_B, pol);
-#pragma unroll
-            for (int u = 0; u < 3; ++u) {
-                const int t = 4 * u + q;
-                if (t < len) {
-                    f[u] = ldg_stream(A + (size_t)(bl_off + 1 + t) * RS_B, pol);
-                    c[u] = operand(colU[bl_offu + t]);
-                }
-            }
-            yv = scr[(size_t)bl_i * RS_B];   // coherent load: written by this warp above
-            bl_off += 1 + len;
-            bl_offu += len;
-            --bl_i;
-        }
-    };
-    int pb_i = nloc - 1, pb_off = nL;
-    auto prefetch_bwd = [&]() {
-        if (pb_i >= 0) {
-            const int len = 1 + (lenU[pb_i] & 0x7f);
-            if (lane == 0) prefetch_l2(Abatch + (size_t)pb_off * RS_B * 32, (unsigned)len * RS_B * 32);
-            pb_off += len;
-            --pb_i;
-        }
-    };
-    for (int k = 0; k < pf_rows; ++k) prefetch_bwd();
-#pragma unroll
-    for (int st = 0; st < RS_D; ++st) issue_bwd(F[st], Cc[st], Di[st], Yv[st]);
-    ri = (nloc - 1) % R;
-    int cx = lx - 1, cy = ly - 1, cz = lz - 1, offb_c = nL, offu_c = 0;
-    const long long eoff = VARIANT != 1 ? sub_ext_off[s] : 0;
-    for (int k0 = 0; k0 < nloc; k0 += RS_D) {
-#pragma unroll
-        for (int st = 0; st < RS_D; ++st) {
-            const int i = nloc - 1 - (k0 + st);
-            if (i >= 0) {
-                const int lv = lenU[i];
-                double2 acc = make_double2(0.0, 0.0);
-                // U block t of row i: slot offb_c + 1 + t, code colU[offu_c + t]
-                row_sum(acc, F[st], Cc[st], lv & 0x7f, (lv & 0x80) != 0, offb_c + 1, colU + offu_c);
-                offb_c += 1 + (lv & 0x7f);
-                offu_c += lv & 0x7f;
-                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 8);
-                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 8);
-                acc.x += __shfl_xor_sync(0xffffffffu, acc.x, 16);
-                acc.y += __shfl_xor_sync(0xffffffffu, acc.y, 16);
-                const double2 v = make_double2(Yv[st].x + acc.x, Yv[st].y + acc.y);
-                const double4 d = Di[st];
-                const double2 xi = make_double2(d.x * v.x + d.y * v.y, d.z * v.x + d.w * v.y);
-                if (q == 0) {
-                    ring[ri * RS_PITCH] = xi;
-                    if (any_far) scr[(size_t)i * RS_B] = xi;   // far columns of later rows read x here
-                    if (bval) {
-                        if (VARIANT == 1) {
-                            if (own[i]) z[cell(cx, cy, cz)] = xi;
-                        } else {
-                            ext_out[eoff + i] = xi;
-                        }
-                    }
-                }
-                ri = ri == 0 ? R - 1 : ri - 1;
-                if (--cx < 0) {
-                    cx = lx - 1;
-                    if (--cy < 0) {
-                        cy = ly - 1;
-                        --cz;
-                    }
-                }
-                issue_bwd(F[st], Cc[st], Di[st], Yv[st]);
-                prefetch_bwd();
-                __syncwarp();
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// TMA-streamed warp solver.  Same sweeps as apply_warp_kernel, but each
-// level's factor slots and column ids are brought into a per-warp
-// shared-memory ring by cp.async.bulk (TMA) several levels ahead, completion
-// tracked by mbarriers, so the level loop computes from shared memory while
-// HBM streams the next levels.  Ring placement is a contiguous circular
-// allocator over levels consumed strictly in order.
-// ---------------------------------------------------------------------------
-
-constexpr int kRingSlots = 16;   // mbarriers = max levels in flight
-
-__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
-{
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
-{
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
-{
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
-{
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-
-struct TmaSmem {
-    WarpSmem w;
-    int ring_bytes;
-    __host__ __device__ size_t meta_end() const { return w.bytes(); }
-    __host__ __device__ size_t bar_off() const { return (meta_end() + 15) / 16 * 16; }
-    __host__ __device__ size_t ring_off() const { return bar_off() + sizeof(uint64_t) * kRingSlots + 16 * 2; }
-    __host__ __device__ size_t bytes() const { return ring_off() + (size_t)ring_bytes; }
-};
-
-template <int VARIANT, int MAXW = 12>
-__global__ void __launch_bounds__(32)
-apply_tma_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
-                 const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
-                 const long long *__restrict__ sub_ext_off, const double4 *__restrict__ vals,
-                 const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out,
-                 TmaSmem L, long long nsub)
-{
-    ACCH_SKIP_IF(g);
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int lane = threadIdx.x;
-    const long long s = blockIdx.x;
-    if (s >= nsub) return;
-    const ClassDev C = classes[sub_class[s]];
-    const int4 o = sub_origin[s];
-    const double4 *__restrict__ A = vals + sub_off[s];
-    double2 *y = reinterpret_cast<double2 *>(smem_raw);
-    int *f_ptr = reinterpret_cast<int *>(smem_raw + L.w.y_bytes());
-    int *f_bs = f_ptr + (C.nlev + 1);
-    int *b_ptr = f_bs + C.nlev;
-    int *b_bs = b_ptr + (C.nlevb + 1);
-    unsigned short *f_rows = reinterpret_cast<unsigned short *>(b_bs + C.nlevb);
-    unsigned short *b_rows = f_rows + C.nloc;
-    unsigned short *f_len = b_rows + C.nloc;
-    unsigned short *b_len = f_len + C.nloc;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem_raw + L.bar_off());
-    unsigned char *ring = smem_raw + L.ring_off();
-
-    for (int i = lane; i <= C.nlev; i += 32) f_ptr[i] = C.lev_ptr[i];
-    for (int i = lane; i < C.nlev; i += 32) f_bs[i] = C.f_base[i];
-    for (int i = lane; i <= C.nlevb; i += 32) b_ptr[i] = C.levb_ptr[i];
-    for (int i = lane; i < C.nlevb; i += 32) b_bs[i] = C.b_base[i];
-    for (int i = lane; i < C.nloc; i += 32) {
-        f_rows[i] = C.f_rows16[i];
-        b_rows[i] = C.b_rows16[i];
-        f_len[i] = C.f_len8[i];
-        b_len[i] = C.b_len8[i];
-    }
-    if (lane == 0) {
-        for (int i = 0; i < kRingSlots; ++i) mbar_init(bars + i, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-
-    const int K = C.nlev + C.nlevb;
-    // slot range [lo, hi) of level k (forward levels, then backward levels)
-    auto range = [&](int k, int &lo, int &hi) {
-        if (k < C.nlev) {
-            lo = f_bs[k];
-            hi = k + 1 < C.nlev ? f_bs[k + 1] : (C.nlevb > 0 ? b_bs[0] : C.ell_total);
-        } else {
-            const int kb = k - C.nlev;
-            lo = b_bs[kb];
-            hi = kb + 1 < C.nlevb ? b_bs[kb + 1] : C.ell_total;
-        }
-    };
-    auto seg_bytes = [&](int ns) { return 32 * ns + 4 * ((ns + 3) & ~3); };
-    // uniform (all lanes) ring bookkeeping; lane 0 issues the copies
-    int issued = 0, head = 0, tail = 0;
-    int offs[kRingSlots];
-#pragma unroll
-    for (int i = 0; i < kRingSlots; ++i) offs[i] = 0;
-    auto try_issue = [&](int consumed) -> bool {
-        if (issued >= K || issued - consumed >= kRingSlots) return false;
-        int lo, hi;
-        range(issued, lo, hi);
-        const int ns = hi - lo;
-        const int bytes = seg_bytes(ns);
-        if (issued == consumed) head = tail = 0;   // ring empty
-        int at = -1;
-        if (head >= tail) {
-            if (head + bytes <= L.ring_bytes) at = head;
-            else if (bytes < tail) at = 0;
-        } else if (head + bytes < tail) {
-            at = head;
-        }
-        if (at < 0) return false;
-        const int slot = issued % kRingSlots;
-#pragma unroll
-        for (int i = 0; i < kRingSlots; ++i)
-            if (i == slot) offs[i] = at;
-        if (lane == 0) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            const unsigned eb = 4u * (unsigned)((ns + 3) & ~3);
-            mbar_expect_tx(bars + slot, 32u * ns + eb);
-            if (ns > 0) bulk_g2s(ring + at, A + lo, 32u * ns, bars + slot);
-            if (eb > 0) bulk_g2s(ring + at + 32 * ns, C.ecol + lo, eb, bars + slot);
-        }
-        head = at + bytes;
-        ++issued;
-        return true;
-    };
-
-    const long long nx = g.nx, ny = g.ny;
-    for (int l = lane; l < C.nloc; l += 32) {
-        int gx, gy, gz;
-        local_to_global(g, C, o, l, gx, gy, gz);
-        double2 v = r[cell_at(g, gx, gy, zplane(g, gz))];
-        if (VARIANT == 2 && !C.owned[l]) v = make_double2(0.0, 0.0);
-        y[l] = v;
-    }
-    (void)nx;
-    (void)ny;
-    __syncwarp();
-
-    for (int k = 0; k < K; ++k) {
-        while (try_issue(k)) {
-        }
-        const int slot = k % kRingSlots;
-        int at = 0;
-#pragma unroll
-        for (int i = 0; i < kRingSlots; ++i)
-            if (i == slot) at = offs[i];
-        mbar_wait(bars + slot, (unsigned)((k / kRingSlots) & 1));
-        int lo, hi;
-        range(k, lo, hi);
-        const int ns = hi - lo;
-        const double4 *sa = reinterpret_cast<const double4 *>(ring + at);
-        const int *se = reinterpret_cast<const int *>(ring + at + 32 * ns);
-        const bool fwd = k < C.nlev;
-        const int lv = fwd ? k : k - C.nlev;
-        const int r0 = fwd ? f_ptr[lv] : b_ptr[lv];
-        const int m = (fwd ? f_ptr[lv + 1] : b_ptr[lv + 1]) - r0;
-        const unsigned short *rows = fwd ? f_rows : b_rows;
-        const unsigned short *lens = fwd ? f_len : b_len;
-        // lane owns rows lane and lane + 32 of the level (levels <= 64 wide).
-        // Slot offsets first (ballots only read the row lengths), then every
-        // shared-memory load of the row, then the FMA chain: ILP, not a
-        // load-use chain per slot.
-        const int first = fwd ? 0 : 1;            // backward: slot 0 is the inverted diagonal
-        const int len0 = lane < m ? (int)lens[r0 + lane] - first : 0;
-        const int len1 = lane + 32 < m ? (int)lens[r0 + lane + 32] - first : 0;
-        const int i0 = lane < m ? rows[r0 + lane] : 0;
-        const int i1 = lane + 32 < m ? rows[r0 + lane + 32] : 0;
-        int offs[MAXW];
-        int off = fwd ? 0 : m;
-#pragma unroll
-        for (int t = 0; t < MAXW; ++t) {
-            offs[t] = off;
-            off += __popc(__ballot_sync(0xffffffffu, len0 > t)) + __popc(__ballot_sync(0xffffffffu, len1 > t));
-        }
-        double2 acc0 = y[i0], acc1 = y[i1];
-        {
-            double4 a[MAXW];
-            int c[MAXW];
-#pragma unroll
-            for (int t = 0; t < MAXW; ++t)
-                if (t < len0) {
-                    a[t] = sa[offs[t] + lane];
-                    c[t] = se[offs[t] + lane];
-                }
-#pragma unroll
-            for (int t = 0; t < MAXW; ++t)
-                if (t < len0) blk_sub(acc0, a[t], y[c[t]]);
-            if (len1 > 0) {
-#pragma unroll
-                for (int t = 0; t < MAXW; ++t)
-                    if (t < len1) {
-                        a[t] = sa[offs[t] + lane + 32];
-                        c[t] = se[offs[t] + lane + 32];
-                    }
-#pragma unroll
-                for (int t = 0; t < MAXW; ++t)
-                    if (t < len1) blk_sub(acc1, a[t], y[c[t]]);
-            }
-        }
-        for (int t = MAXW;; ++t) {   // rows longer than MAXW slots (wrapped boxes, fill-in)
-            const unsigned b0 = __ballot_sync(0xffffffffu, len0 > t), b1 = __ballot_sync(0xffffffffu, len1 > t);
-            if (!(b0 | b1)) break;
-            if (t < len0) blk_sub(acc0, sa[off + lane], y[se[off + lane]]);
-            if (t < len1) blk_sub(acc1, sa[off + lane + 32], y[se[off + lane + 32]]);
-            off += __popc(b0) + __popc(b1);
-        }
-        if (fwd) {
-            if (lane < m) y[i0] = acc0;
-            if (lane + 32 < m) y[i1] = acc1;
-        } else {
-            if (lane < m) {
-                const double4 di = sa[lane];
-                y[i0] = make_double2(di.x * acc0.x + di.y * acc0.y, di.z * acc0.x + di.w * acc0.y);
-            }
-            if (lane + 32 < m) {
-                const double4 di = sa[lane + 32];
-                y[i1] = make_double2(di.x * acc1.x + di.y * acc1.y, di.z * acc1.x + di.w * acc1.y);
-            }
-        }
-        __syncwarp();
-        // level k consumed: the oldest live level is now k + 1
-        if (k + 1 < issued) {
-            const int ns2 = (k + 1) % kRingSlots;
-#pragma unroll
-            for (int i = 0; i < kRingSlots; ++i)
-                if (i == ns2) tail = offs[i];
-        } else {
-            tail = head;
-        }
-    }
-    if (VARIANT == 1) {
-        for (int l = lane; l < C.nloc; l += 32) {
-            if (!C.owned[l]) continue;
-            int gx, gy, gz;
-            local_to_global(g, C, o, l, gx, gy, gz);
-            z[cell_at(g, gx, gy, zplane(g, gz))] = y[l];
-        }
-    } else {
-        for (int l = lane; l < C.nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
-    }
-}
-
-// z[c] = sum over subdomains containing c, in subdomain order, of their local solution
 __global__ void gather_kernel(long long n, const long long *__restrict__ cell_ptr, const long long *__restrict__ cell_src,
                               const double2 *__restrict__ ext_out, double2 *__restrict__ z, const int *skip)
 {
@@ -1789,18 +1113,9 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
                 const int a = C.jmap[(size_t)l * noff + q], b = C.jmap[(size_t)l * noff + q2];
                 if (a >= 0 && a == b) C.jdup = 1;
             }
-    C.jmap_local.assign(C.jmap.size(), -1);
-    for (int l = 0; l < nloc; ++l)
-        for (int q = 0; q < noff; ++q) {
-            const int j = C.jmap[(size_t)l * noff + q];
-            if (j >= 0) C.jmap_local[(size_t)l * noff + q] = j - C.rowptr[l];
-        }
-    C.rmax = 0;
-    for (int i = 0; i < nloc; ++i) C.rmax = std::max(C.rmax, C.rowptr[i + 1] - C.rowptr[i]);
     // IKJ update lists: for lower entry t=(i,k), pairs (U entry (k,j), entry (i,j))
     C.upd_ptr.assign(C.nnzb + 1, 0);
     C.upd.clear();
-    C.upd_dl.clear();
     std::vector<int> where(nloc, -1);
     for (int i = 0; i < nloc; ++i) {
         for (int t = C.rowptr[i]; t < C.rowptr[i + 1]; ++t) where[C.col[t]] = t;
@@ -1809,83 +1124,12 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
             if (k < i) {
                 for (int u = C.diag[k] + 1; u < C.rowptr[k + 1]; ++u) {
                     const int w = where[C.col[u]];
-                    if (w >= 0) {
-                        C.upd.push_back(make_int2(u, w));
-                        C.upd_dl.push_back(w - C.rowptr[i]);
-                    }
+                    if (w >= 0) C.upd.push_back(make_int2(u, w));
                 }
             }
             C.upd_ptr[t + 1] = (int)C.upd.size();
         }
         for (int t = C.rowptr[i]; t < C.rowptr[i + 1]; ++t) where[C.col[t]] = -1;
-    }
-    C.jmap_csr = C.jmap;
-    C.upd_csr = C.upd;
-    // row-sequential layout (apply_rs_kernel): eligible when every L / U row
-    // has <= 24 blocks (blocks 0..11 of a row are prefetched, 3 per lane of a
-    // 4-lane row group; the wrapped layer of a periodic box makes some rows
-    // longer, whose tail blocks are loaded when the row is solved).  A column within
-    // 255 rows of its row is read from the per-warp ring of the last R rows;
-    // a farther one (the wrapped layer of a periodic box sorts to the other
-    // end of the local order) from the warp's y / x scratch in L2.
-    {
-        C.rs_pos.assign(C.nnzb, -1);
-        int slot = 0, near = 0, maxlen = 0;
-        for (int i = 0; i < nloc; ++i) {
-            for (int t = C.rowptr[i]; t < C.diag[i]; ++t) C.rs_pos[t] = slot++;
-            maxlen = std::max(maxlen, C.diag[i] - C.rowptr[i]);
-            for (int t = C.rowptr[i]; t < C.rowptr[i + 1]; ++t) {
-                const int d = std::abs(C.col[t] - i);
-                if (d <= 255) near = std::max(near, d);
-            }
-        }
-        C.rs_nL = slot;
-        for (int i = nloc - 1; i >= 0; --i) {
-            for (int t = C.diag[i]; t < C.rowptr[i + 1]; ++t) C.rs_pos[t] = slot++;
-            maxlen = std::max(maxlen, C.rowptr[i + 1] - C.diag[i] - 1);
-        }
-        const int R = near + 1;
-        C.rs_ring = R;
-        C.rs_ok = maxlen <= 24 && nloc <= 32767;
-        const int nL = C.rs_nL, nU = C.nnzb - nloc - nL;
-        size_t at = 0;
-        auto seg = [&](size_t bytes) { size_t o = at; at += (bytes + 15) / 16 * 16; return (int)o; };
-        seg(nloc);
-        C.rs_m[0] = seg(nloc);                     // lenU
-        C.rs_m[1] = seg(nloc);                     // own
-        C.rs_m[2] = seg(2 * (size_t)nL);           // colL (uint16)
-        C.rs_m[3] = seg(2 * (size_t)std::max(nU, 1));   // colU (uint16)
-        C.rs_m[4] = seg(sizeof(int) * (lx + ly + lz));
-        C.rs_meta.assign(at, 0);
-        unsigned char *m = C.rs_meta.data();
-        unsigned short *cl = reinterpret_cast<unsigned short *>(m + C.rs_m[2]);
-        unsigned short *cu = reinterpret_cast<unsigned short *>(m + C.rs_m[3]);
-        // entry code: ring slot j mod R (near) or 0x8000 | j (far); bit 7 of a
-        // row length flags a row with a far entry
-        auto code = [&](int i, int j, bool &far) -> unsigned short {
-            if (std::abs(j - i) < R) return (unsigned short)(j % R);
-            far = true;
-            return (unsigned short)(0x8000 | j);
-        };
-        int kl = 0, ku = 0;
-        C.rs_far = 0;
-        for (int i = 0; i < nloc; ++i) {
-            bool far = false;
-            for (int t = C.rowptr[i]; t < C.diag[i]; ++t) cl[kl++] = code(i, C.col[t], far);
-            m[i] = (unsigned char)((C.diag[i] - C.rowptr[i]) | (far ? 0x80 : 0));
-            C.rs_far |= far;
-        }
-        for (int i = nloc - 1; i >= 0; --i) {
-            bool far = false;
-            for (int t = C.diag[i] + 1; t < C.rowptr[i + 1]; ++t) cu[ku++] = code(i, C.col[t], far);
-            m[C.rs_m[0] + i] = (unsigned char)((C.rowptr[i + 1] - C.diag[i] - 1) | (far ? 0x80 : 0));
-            C.rs_far |= far;
-        }
-        int *rl = reinterpret_cast<int *>(m + C.rs_m[4]);
-        for (int a = 0, k = 0; a < 3; ++a) {
-            const int la = a == 0 ? lx : (a == 1 ? ly : lz);
-            for (int i = 0; i < la; ++i) rl[k++] = a < dim ? rel[a][i] : 0;
-        }
     }
     // level schedules from the factor DAG
     std::vector<int> lev(nloc, 0), levb(nloc, 0);
@@ -2042,18 +1286,7 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
         C.owned[l] = own ? 1 : 0;
         if (own) C.own_list.push_back(l);
     }
-    for (int l = 0; l < nloc; ++l) C.rs_meta[C.rs_m[1] + l] = C.owned[l];
     return true;
-}
-
-// switch a class to the row-sequential slot layout (factor kernels address
-// slots through pos / jmap / upd)
-void use_rs_layout(ClassHost &C)
-{
-    C.pos = C.rs_pos;
-    for (size_t k = 0; k < C.jmap.size(); ++k) C.jmap[k] = C.jmap_csr[k] >= 0 ? C.pos[C.jmap_csr[k]] : -1;
-    for (size_t u = 0; u < C.upd.size(); ++u) C.upd[u] = make_int2(C.pos[C.upd_csr[u].x], C.pos[C.upd_csr[u].y]);
-    C.ell_total = C.nnzb;
 }
 
 template <typename T>
@@ -2145,9 +1378,6 @@ acch_status upload_class(ClassHost &C)
     const size_t o_meta = add(C.meta.size());
     const size_t o_lin = add(sizeof(int) * C.lin.size());
     const size_t o_own = add(sizeof(int) * std::max<size_t>(1, C.own_list.size()));
-    const size_t o_jml = add(sizeof(int) * C.jmap_local.size());
-    const size_t o_udl = add(sizeof(int) * std::max<size_t>(1, C.upd_dl.size()));
-    const size_t o_rsm = add(C.rs_meta.size());
     ACCH_CUDA(cudaMalloc(&C.dev_mem, total));
     std::vector<unsigned char> h(total, 0);
     auto put = [&](size_t o, const void *src, size_t bytes) { if (bytes) memcpy(h.data() + o, src, bytes); };
@@ -2180,9 +1410,6 @@ acch_status upload_class(ClassHost &C)
     put(o_meta, C.meta.data(), C.meta.size());
     put(o_lin, C.lin.data(), sizeof(int) * C.lin.size());
     put(o_own, C.own_list.data(), sizeof(int) * C.own_list.size());
-    put(o_jml, C.jmap_local.data(), sizeof(int) * C.jmap_local.size());
-    put(o_udl, C.upd_dl.data(), sizeof(int) * C.upd_dl.size());
-    put(o_rsm, C.rs_meta.data(), C.rs_meta.size());
     ACCH_CUDA(cudaMemcpy(C.dev_mem, h.data(), total, cudaMemcpyHostToDevice));
     unsigned char *b = (unsigned char *)C.dev_mem;
     ClassDev &d = C.dev;
@@ -2223,19 +1450,6 @@ acch_status upload_class(ClassHost &C)
     d.lin = (const int *)(b + o_lin);
     d.own_list = (const int *)(b + o_own);
     d.n_owned = (int)C.own_list.size();
-    d.jmap_local = (const int *)(b + o_jml);
-    d.upd_dl = (const int *)(b + o_udl);
-    d.rmax = C.rmax;
-    d.rs_meta = b + o_rsm;
-    d.rs_meta_bytes = (int)C.rs_meta.size();
-    d.rs_m_lenU = C.rs_m[0];
-    d.rs_m_own = C.rs_m[1];
-    d.rs_m_colL = C.rs_m[2];
-    d.rs_m_colU = C.rs_m[3];
-    d.rs_m_rel = C.rs_m[4];
-    d.rs_nL = C.rs_nL;
-    d.rs_ring = C.rs_ring;
-    d.rs_far = C.rs_far;
     d.jdup = C.jdup;
     d.meta_bytes = (int)C.meta.size();
     d.m_fbs = C.m_off[1];
@@ -2276,8 +1490,6 @@ struct acch_precond {
     long long *d_sub_off = nullptr, *d_sub_ext_off = nullptr;
     double4 *d_vals = nullptr;
     int wide = 0;                 // some factor row exceeds kWideLen blocks (LU / high fill): warp-wide rows
-    float4 *d_vals32 = nullptr;   // opt-in fp32 copy of the factors for the group solver (ACCH_FACTOR_F32=1)
-    int f32 = 0;
     long long total_blocks = 0, total_ext = 0, total_nnzb = 0;
     int *d_bad = nullptr;
     double2 *d_ext_out = nullptr;
@@ -2289,27 +1501,15 @@ struct acch_precond {
     int tps = 32;          // threads per subdomain in the solves
     int max_nloc = 0;
     int warp_mode = 0;     // apply_warp_kernel usable
-    int tma_mode = 0;      // apply_tma_kernel (TMA ring) in use
     // class-group solver (apply_group_kernel): groups of <= group_nw subdomains of one class
     int group_mode = 0, group_nw = 8, group_per_warp = 1, meta_max = 0, y_stride = 0;
-    int factor_warp = 0, factor_rstride = 0;   // factor_warp_kernel (opt-in: ACCH_FACTOR_WARP=1)
-    int dbg = 0;   // ACCH_APPLY_DBG (timing experiments only; results are wrong): 1 no factor loads, 2 loads only
+    int factor_threads = 0;   // threads per subdomain CTA of factor_kernel (32 / 64 / 128)
     size_t group_smem = 0;
     std::vector<int4> groups;
     int4 *d_groups = nullptr;
     int *d_grp_sub = nullptr;
-    TmaSmem tl{};
     int pf_depth = 3;      // levels prefetched ahead into L2 (ACCH_PREFETCH_DEPTH overrides; 3 measured best for the group solver with capped levels)
     WarpSmem wl{0, 0, 0};
-    // row-sequential batched solver (apply_rs_kernel)
-    int rs_mode = 0, rs_nw = 0, rs_meta_pad = 0, rs_ring_stride = 0, slot_stride = 1, rs_pf_rows = 8;
-    size_t rs_smem = 0;
-    std::vector<int4> rs_items, rs_batches;
-    std::vector<long long> rs_batch_base;
-    int4 *d_rs_items = nullptr, *d_rs_batches = nullptr;
-    long long *d_rs_batch_base = nullptr;
-    int *d_rs_members = nullptr;
-    double2 *d_rs_scratch = nullptr;
 };
 
 // cudaFuncAttributeMaxDynamicSharedMemorySize is process-wide per kernel, so
@@ -2333,18 +1533,12 @@ static void free_precond(acch_precond *pc)
     cudaFree(pc->d_sub_off);
     cudaFree(pc->d_sub_ext_off);
     cudaFree(pc->d_vals);
-    cudaFree(pc->d_vals32);
     cudaFree(pc->d_bad);
     cudaFree(pc->d_ext_out);
     cudaFree(pc->d_cell_ptr);
     cudaFree(pc->d_cell_src);
     cudaFree(pc->d_groups);
     cudaFree(pc->d_grp_sub);
-    cudaFree(pc->d_rs_items);
-    cudaFree(pc->d_rs_batches);
-    cudaFree(pc->d_rs_batch_base);
-    cudaFree(pc->d_rs_members);
-    cudaFree(pc->d_rs_scratch);
 }
 
 extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t overlap, const int64_t *owned_lo,
@@ -2444,81 +1638,18 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         }
         pc->sub_origin.push_back(make_int4(lo3[0], lo3[1], lo3[2], nowrap));
     }
-    // row-sequential batched solver (opt-in, ACCH_RS=1) when every class
-    // qualifies and the shared-memory image + rings of >= 2 warps fit.  At
-    // 256^3 / 8^3 boxes it measured 7.8 ms per apply against the group
-    // solver's 5.0 (profiles/r01_apply_rs.txt): 2000 dependent row steps per
-    // batch at 6 warps / SM stay latency-bound.
-    {
-        int ok = 0, ring = 0;
-        if (const char *e = getenv("ACCH_RS")) ok = atoi(e) != 0;
-        size_t meta = 0;
-        for (const auto &C : pc->classes) {
-            ok = ok && C.rs_ok;
-            ring = std::max(ring, C.rs_ring);
-            meta = std::max(meta, C.rs_meta.size());
-        }
-        const size_t limit = 227 * 1024;
-        pc->rs_meta_pad = (int)((meta + 127) / 128 * 128);
-        pc->rs_ring_stride = ring * RS_PITCH;
-        const size_t per_warp = sizeof(double2) * (size_t)pc->rs_ring_stride;
-        int nw = 8;
-        while (nw > 2 && pc->rs_meta_pad + nw * per_warp > limit) --nw;
-        if (const char *e = getenv("ACCH_RS_WARPS")) nw = std::min(nw, std::max(2, atoi(e)));
-        if (const char *e = getenv("ACCH_RS_PF")) pc->rs_pf_rows = std::max(0, atoi(e));
-        if (getenv("ACCH_DEBUG")) {
-            int nok = 0;
-            for (const auto &C : pc->classes) nok += C.rs_ok;
-            fprintf(stderr, "[acch] row-sequential: %d/%zu classes eligible, ring %d rows, meta %zu B, %d warps -> %zu B\n",
-                    nok, pc->classes.size(), ring, meta, nw, pc->rs_meta_pad + nw * per_warp);
-        }
-        ok = ok && pc->rs_meta_pad + nw * per_warp <= limit;
-        if (ok) {
-            pc->rs_mode = 1;
-            pc->rs_nw = nw;
-            // one resident CTA per SM (the scratch slot is indexed by %smid)
-            pc->rs_smem = std::max<size_t>(pc->rs_meta_pad + nw * per_warp, 116 * 1024);
-            pc->slot_stride = RS_B;
-            for (auto &C : pc->classes) use_rs_layout(C);
-        }
-    }
     // offsets
     long long vo = 0, eo = 0;
     int max_nloc = 0;
     pc->sub_off.assign(n_sub, 0);
     for (long long s = 0; s < n_sub; ++s) {
         const ClassHost &C = pc->classes[pc->sub_class[s]];
-        if (!pc->rs_mode) {
-            pc->sub_off[s] = vo;
-            vo += C.ell_total;
-        }
+        pc->sub_off[s] = vo;
+        vo += C.ell_total;
         pc->sub_ext_off.push_back(eo);
         eo += C.nloc;
         pc->total_nnzb += C.nnzb;
         max_nloc = std::max(max_nloc, C.nloc);
-    }
-    std::vector<int> rs_members;
-    if (pc->rs_mode) {
-        // batches of RS_B subdomains of one class; items of <= rs_nw batches of one class
-        std::vector<std::vector<int>> members(pc->classes.size());
-        for (long long s = 0; s < n_sub; ++s) members[pc->sub_class[s]].push_back((int)s);
-        for (size_t c = 0; c < members.size(); ++c) {
-            const int first_batch = (int)pc->rs_batches.size();
-            for (size_t i = 0; i < members[c].size(); i += RS_B) {
-                const int cnt = (int)std::min<size_t>(RS_B, members[c].size() - i);
-                pc->rs_batches.push_back(make_int4((int)rs_members.size(), cnt, 0, 0));
-                pc->rs_batch_base.push_back(vo);
-                for (int b = 0; b < cnt; ++b) {
-                    const int s = members[c][i + b];
-                    rs_members.push_back(s);
-                    pc->sub_off[s] = vo + b;
-                }
-                vo += (long long)RS_B * pc->classes[c].ell_total;
-            }
-            const int nb = (int)pc->rs_batches.size() - first_batch;
-            for (int k = 0; k < nb; k += pc->rs_nw)
-                pc->rs_items.push_back(make_int4((int)c, first_batch + k, std::min(pc->rs_nw, nb - k), 0));
-        }
     }
     int max_width = 0;
     for (const auto &C : pc->classes) max_width = std::max(max_width, std::max(C.max_fwidth, C.max_bwidth));
@@ -2544,32 +1675,11 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         if (const char *e = getenv("ACCH_PREFETCH_DEPTH")) pc->pf_depth = atoi(e);
         if (const char *e = getenv("ACCH_SCHWARZ_BLOCK_SOLVER"))   // testing: force the CTA-wide solver
             if (atoi(e)) pc->warp_mode = 0, pc->tps = 128;
-        // TMA ring: at least two of the largest level segments
-        int max_seg = 0;
-        for (const auto &C : pc->classes) {
-            std::vector<int> bases(C.f_base.begin(), C.f_base.end());
-            bases.insert(bases.end(), C.b_base.begin(), C.b_base.end());
-            bases.push_back(C.ell_total);
-            for (size_t k = 0; k + 1 < bases.size(); ++k) {
-                const int ns = bases[k + 1] - bases[k];
-                max_seg = std::max(max_seg, 32 * ns + 4 * ((ns + 3) & ~3));
-            }
-        }
-        int ring_kb = 32;
-        if (const char *e = getenv("ACCH_RING_KB")) ring_kb = std::max(4, atoi(e));
-        pc->tl = TmaSmem{pc->wl, std::max(ring_kb * 1024, max_seg + 64)};
-        pc->tl.ring_bytes = (pc->tl.ring_bytes + 15) / 16 * 16;
-        // opt-in (ACCH_SCHWARZ_TMA=1): at 3-5 warps per SM the ring solver is
-        // latency-bound on its per-level compute and measured slower than the
-        // register-prefetch warp solver (profiles/r01_apply_variants.txt)
-        pc->tma_mode = 0;
-        if (const char *e = getenv("ACCH_SCHWARZ_TMA"))
-            if (atoi(e)) pc->tma_mode = pc->warp_mode && pc->tl.bytes() <= 220 * 1024;
         if (getenv("ACCH_DEBUG"))
             fprintf(stderr, "[acch] precond: %lld subdomains, %zu classes, max_nloc %d, max level width %d, "
                             "max row %d, warp smem %zu B -> %s solver\n",
                     (long long)n_sub, pc->classes.size(), max_nloc, max_width, max_len, pc->wl.bytes(),
-                    pc->tma_mode ? "TMA-ring warp" : (pc->warp_mode ? "warp" : "CTA"));
+                    pc->warp_mode ? "warp" : "CTA");
     }
     const int groups = 128 / pc->tps;
     pc->apply_smem = sizeof(double2) * (size_t)max_nloc * groups;
@@ -2606,35 +1716,6 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
     PC_CUDA(cudaMalloc(&pc->d_sub_ext_off, sizeof(long long) * n_sub));
     PC_CUDA(cudaMemcpy(pc->d_sub_ext_off, pc->sub_ext_off.data(), sizeof(long long) * n_sub, cudaMemcpyHostToDevice));
     PC_CUDA(cudaMalloc(&pc->d_vals, sizeof(double4) * std::max<long long>(1, pc->total_blocks)));
-    if (pc->rs_mode) {
-        PC_CUDA(cudaMalloc(&pc->d_rs_items, sizeof(int4) * pc->rs_items.size()));
-        PC_CUDA(cudaMemcpy(pc->d_rs_items, pc->rs_items.data(), sizeof(int4) * pc->rs_items.size(), cudaMemcpyHostToDevice));
-        PC_CUDA(cudaMalloc(&pc->d_rs_batches, sizeof(int4) * pc->rs_batches.size()));
-        PC_CUDA(cudaMemcpy(pc->d_rs_batches, pc->rs_batches.data(), sizeof(int4) * pc->rs_batches.size(),
-                           cudaMemcpyHostToDevice));
-        PC_CUDA(cudaMalloc(&pc->d_rs_batch_base, sizeof(long long) * pc->rs_batch_base.size()));
-        PC_CUDA(cudaMemcpy(pc->d_rs_batch_base, pc->rs_batch_base.data(), sizeof(long long) * pc->rs_batch_base.size(),
-                           cudaMemcpyHostToDevice));
-        PC_CUDA(cudaMalloc(&pc->d_rs_members, sizeof(int) * rs_members.size()));
-        PC_CUDA(cudaMemcpy(pc->d_rs_members, rs_members.data(), sizeof(int) * rs_members.size(), cudaMemcpyHostToDevice));
-        // forward-sweep scratch: one slot per (SM id, warp); SM ids may exceed the SM count
-        int dev = 0, nsm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        const size_t slots = (size_t)std::max(256, 2 * nsm) * pc->rs_nw;
-        PC_CUDA(cudaMalloc(&pc->d_rs_scratch, sizeof(double2) * slots * (size_t)max_nloc * RS_B));
-        const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-        const int optin = smem_optin();
-#define RS_ATTR(NW)                                                        \
-        PC_CUDA(cudaFuncSetAttribute(apply_rs_kernel<0, NW>, attr, optin)); \
-        PC_CUDA(cudaFuncSetAttribute(apply_rs_kernel<1, NW>, attr, optin)); \
-        PC_CUDA(cudaFuncSetAttribute(apply_rs_kernel<2, NW>, attr, optin));
-        RS_ATTR(2) RS_ATTR(3) RS_ATTR(4) RS_ATTR(5) RS_ATTR(6) RS_ATTR(7) RS_ATTR(8)
-#undef RS_ATTR
-        if (getenv("ACCH_DEBUG"))
-            fprintf(stderr, "[acch] row-sequential solver: %zu batches, %zu items, %d warps/CTA, smem %zu B\n",
-                    pc->rs_batches.size(), pc->rs_items.size(), pc->rs_nw, pc->rs_smem);
-    }
     PC_CUDA(cudaMalloc(&pc->d_bad, sizeof(int) * n_sub));
     const bool need_ext = variant != 1 || !pc->use_smem;
     if (need_ext) PC_CUDA(cudaMalloc(&pc->d_ext_out, sizeof(double2) * std::max<long long>(1, pc->total_ext)));
@@ -2681,13 +1762,6 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<1, 128>, attr, b));
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 128>, attr, b));
     }
-    if (pc->tma_mode && pc->tl.bytes() > 48 * 1024) {
-        const int b = smem_optin();   // per-function state: never lower it under another live preconditioner
-        const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<0>, attr, b));
-        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<1>, attr, b));
-        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<2>, attr, b));
-    }
     {
         // the solvers live on shared memory: ask for the full L1/shared carveout
         const auto co = cudaFuncAttributePreferredSharedMemoryCarveout;
@@ -2709,9 +1783,6 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 16, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<2, 12, 16, true>, co, 100));
-        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<0>, co, 100));
-        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<1>, co, 100));
-        PC_CUDA(cudaFuncSetAttribute(apply_tma_kernel<2>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<0, 32>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<1, 32>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 32>, co, 100));
@@ -2749,7 +1820,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         for (const auto &C : pc->classes) meta_max = std::max(meta_max, (int)C.meta.size());
         pc->meta_max = (meta_max + 15) / 16 * 16;
         pc->y_stride = (int)((sizeof(double2) * (size_t)max_nloc + 15) / 16 * 16);
-        int enable = pc->warp_mode && !pc->tma_mode && !pc->rs_mode;
+        int enable = pc->warp_mode;
         if (const char *e = getenv("ACCH_GROUP")) enable = enable && atoi(e) != 0;
         int nw = 8;
         if (const char *e = getenv("ACCH_GROUP_WARPS")) nw = atoi(e) <= 4 ? 4 : 8;
@@ -2784,23 +1855,12 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4>, attr, b));
             PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 1>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 2>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 8, 12, 0, float4>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 0, float4>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 8, 12, 0, float4>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4, 12, 0, float4>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4, 12, 0, float4>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4, 12, 0, float4>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 8, 12, 0, double4, true>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, 0, double4, true>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 8, 12, 0, double4, true>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4, 12, 0, double4, true>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4, 12, 0, double4, true>, attr, b));
-            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4, 12, 0, double4, true>, attr, b));
-            if (const char *e = getenv("ACCH_FACTOR_F32")) pc->f32 = atoi(e) != 0;
-            if (pc->f32) PC_CUDA(cudaMalloc(&pc->d_vals32, sizeof(float4) * std::max<long long>(1, pc->total_blocks)));
-            if (const char *e = getenv("ACCH_APPLY_DBG")) pc->dbg = atoi(e);
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 8, 12, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 8, 12, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 8, 12, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<0, 4, 12, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<1, 4, 12, double4, true>, attr, b));
+            PC_CUDA(cudaFuncSetAttribute(apply_group_kernel<2, 4, 12, double4, true>, attr, b));
         }
         if (getenv("ACCH_DEBUG"))
         {
@@ -2815,21 +1875,24 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         }
     }
     {
-        // warp factorisation: 4 warps x 32 row buffers of the longest row must fit
-        int rmax = 0;
-        for (const auto &C : pc->classes) rmax = std::max(rmax, C.rmax);
-        pc->factor_rstride = rmax;
-        const size_t sm = (size_t)4 * 32 * rmax * sizeof(double4);
-        // opt-in (ACCH_FACTOR_WARP=1): 4.1x less DRAM traffic than the CTA
-        // kernel (55 vs 226 GB at 256^3) but latency-bound at 8 warps/SM and
-        // measured slower (158 vs 124 ms; profiles/r01_factor.txt)
-        pc->factor_warp = 0;
-        if (const char *e = getenv("ACCH_FACTOR_WARP")) pc->factor_warp = sm <= 200 * 1024 && atoi(e) != 0;
-        if (pc->factor_warp) {
-            const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-            PC_CUDA(cudaFuncSetAttribute(factor_warp_kernel<3, 4>, attr, smem_optin()));
-            PC_CUDA(cudaFuncSetAttribute(factor_warp_kernel<2, 4>, attr, smem_optin()));
+        // threads per subdomain CTA of factor_kernel, fixed at creation: a 3D
+        // ILU level is at most 32 rows wide, so one warp per subdomain keeps
+        // every lane busy and fits 4x the subdomains per SM (128^3 ILU(2)
+        // 455 -> 262 ms, 256^3 ILU(0) 101.7 -> 86.6 ms, profiles/r01_factor_threads.txt);
+        // in 2D (LU) 128 measured faster.  ACCH_FACTOR_THREADS = 32 | 64 | 128
+        // overrides (the factors are bitwise the same for every choice -- the
+        // per-row update order does not depend on it; tested).
+        int nt = dim == 3 ? 32 : kFactorThreads;
+        if (const char *e = getenv("ACCH_FACTOR_THREADS")) {
+            nt = atoi(e);
+            if (nt != 32 && nt != 64 && nt != 128) {
+                free_precond(pc);
+                delete pc;
+                acch_set_error("ACCH_FACTOR_THREADS must be 32, 64 or 128");
+                return ACCH_ERR_INVALID_ARG;
+            }
         }
+        pc->factor_threads = nt;
     }
 #undef PC_CUDA
     *out = pc;
@@ -2854,17 +1917,6 @@ extern "C" acch_status acch_precond_invalidate(acch_precond *pc)
     return ACCH_OK;
 }
 
-// fp32 storage copy of the fp64 factors (round to nearest), read by the
-// group solver when ACCH_FACTOR_F32=1; the factorisation itself stays fp64
-__global__ void factors_to_f32_kernel(const double4 *__restrict__ src, float4 *__restrict__ dst, long long n)
-{
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const double4 a = src[i];
-        dst[i] = make_float4(__double2float_rn(a.x), __double2float_rn(a.y), __double2float_rn(a.z),
-                             __double2float_rn(a.w));
-    }
-}
-
 extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef, double dt, int32_t reuse,
                                            int32_t *refactored, int64_t *bad_cell, int32_t *bad_comp)
 {
@@ -2877,30 +1929,11 @@ extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef,
     acch_ctx *ctx = pc->ctx;
     ACCH_CUDA(cudaMemsetAsync(pc->d_bad, 0x7f, sizeof(int) * pc->nsub, ctx->stream));
     ProfScope prof_scope(ctx, PC_FACTOR, 32.0 * pc->total_nnzb + 56.0 * pc->total_ext);
-    if (pc->factor_warp) {
-        constexpr int NW = 4;
-        const unsigned nb = (unsigned)((pc->nsub + NW - 1) / NW);
-        const size_t sm = (size_t)NW * 32 * pc->factor_rstride * sizeof(double4);
-        if (pc->dim == 3)
-            factor_warp_kernel<3, NW><<<nb, NW * 32, sm, ctx->stream>>>(ctx->g, ctx->p, dt, coef, pc->d_classes,
-                pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, pc->d_bad, pc->nsub, pc->factor_rstride,
-                pc->slot_stride);
-        else
-            factor_warp_kernel<2, NW><<<nb, NW * 32, sm, ctx->stream>>>(ctx->g, ctx->p, dt, coef, pc->d_classes,
-                pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, pc->d_bad, pc->nsub, pc->factor_rstride,
-                pc->slot_stride);
-    } else {
-        // threads per subdomain CTA (ACCH_FACTOR_THREADS = 32 / 64 / 128 overrides):
-        // a 3D ILU level is at most 32 rows wide, so one warp per subdomain
-        // keeps every lane busy in the elimination and fits 4x the subdomains
-        // per SM (same per-row update order: bitwise the same factors).
-        // 128^3 ILU(2) 455 -> 262 ms, 256^3 ILU(0) 101.7 -> 86.6 ms
-        // (profiles/r01_factor_threads.txt)
-        int nt = pc->dim == 3 ? 32 : kFactorThreads;
-        if (const char *e = getenv("ACCH_FACTOR_THREADS")) nt = atoi(e);
+    {
+        const int nt = pc->factor_threads;
 #define FK(D, NT) factor_kernel<D, NT><<<(unsigned)pc->nsub, NT, 0, ctx->stream>>>( \
             ctx->g, ctx->p, dt, coef, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_vals, \
-            pc->d_bad, pc->slot_stride)
+            pc->d_bad, 1)
         if (pc->dim == 3) {
             if (nt == 32) FK(3, 32);
             else if (nt == 64) FK(3, 64);
@@ -2938,10 +1971,6 @@ extern "C" acch_status acch_precond_update(acch_precond *pc, const double *coef,
             return ACCH_ERR_ZERO_PIVOT;
         }
     }
-    if (pc->f32) {
-        factors_to_f32_kernel<<<148 * 8, 256, 0, ctx->stream>>>(pc->d_vals, pc->d_vals32, pc->total_blocks);
-        ACCH_LAUNCHED(ctx);
-    }
     pc->have_factors = true;
     if (refactored) *refactored = 1;
     return ACCH_OK;
@@ -2970,26 +1999,16 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
         (double2 *)z, pc->d_ext_out, pc->wl, pc->nsub); } while (0)
 #define GAPPLY_W(V, NW)                                                                                       \
-    do { if (pc->wide && !pc->f32) apply_group_kernel<V, NW, 12, 0, double4, true><<<(unsigned)pc->groups.size(),    \
+    do { if (pc->wide) apply_group_kernel<V, NW, 12, double4, true><<<(unsigned)pc->groups.size(),                \
         NW * 32, pc->group_smem, ctx->stream>>>(ctx->g, pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, \
         pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max,  \
         pc->y_stride, 0, pc->pf_depth);                                                                           \
-    else if (pc->f32) apply_group_kernel<V, NW, 12, 0, float4><<<(unsigned)pc->groups.size(), NW * 32, pc->group_smem,     \
-        ctx->stream>>>(ctx->g, pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off,          \
-        pc->d_sub_ext_off, pc->d_vals32, (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride,\
-        0, pc->pf_depth);                                                                                         \
     else apply_group_kernel<V, NW><<<(unsigned)pc->groups.size(), NW * 32, pc->group_smem, ctx->stream>>>(ctx->g,         \
         pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, \
         (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride, 0, pc->pf_depth); } while (0)
-#define GAPPLY_DBG(D)                                                                                          \
-    apply_group_kernel<1, 8, 12, D><<<(unsigned)pc->groups.size(), 256, pc->group_smem, ctx->stream>>>(ctx->g,      \
-        pc->d_classes, pc->d_groups, pc->d_grp_sub, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, \
-        (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->meta_max, pc->y_stride, 0, pc->pf_depth)
 #define GAPPLY(V)                                                            \
     do {                                                                     \
-        if (V == 1 && pc->group_nw == 8 && pc->dbg == 1) GAPPLY_DBG(1);      \
-        else if (V == 1 && pc->group_nw == 8 && pc->dbg == 2) GAPPLY_DBG(2); \
-        else if (pc->group_nw == 8) GAPPLY_W(V, 8);                          \
+        if (pc->group_nw == 8) GAPPLY_W(V, 8);                               \
         else GAPPLY_W(V, 4);                                                 \
     } while (0)
 #define WAPPLY(V)                                            \
@@ -2998,39 +2017,12 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         else if (pc->pf_depth <= 8) WAPPLY_D(V, 8);          \
         else WAPPLY_D(V, 16);                                \
     } while (0)
-#define TAPPLY(V)                                                                                             \
-    apply_tma_kernel<V><<<(unsigned)pc->nsub, 32, pc->tl.bytes(), ctx->stream>>>(ctx->g, pc->d_classes,             \
-        pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r,       \
-        (double2 *)z, pc->d_ext_out, pc->tl, pc->nsub)
-#define RSAPPLY_W(V, NW)                                                                                        \
-    apply_rs_kernel<V, NW><<<(unsigned)pc->rs_items.size(), NW * 32, pc->rs_smem, ctx->stream>>>(ctx->g, pc->d_classes, \
-        pc->d_rs_items, pc->d_rs_batches, pc->d_rs_batch_base, pc->d_rs_members, pc->d_sub_origin, pc->d_sub_ext_off,  \
-        pc->d_vals, (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->d_rs_scratch, pc->rs_meta_pad,              \
-        pc->rs_ring_stride, pc->max_nloc, pc->rs_pf_rows)
-#define RSAPPLY(V)                                 \
-    do {                                           \
-        switch (pc->rs_nw) {                       \
-        case 2: RSAPPLY_W(V, 2); break;            \
-        case 3: RSAPPLY_W(V, 3); break;            \
-        case 4: RSAPPLY_W(V, 4); break;            \
-        case 5: RSAPPLY_W(V, 5); break;            \
-        case 6: RSAPPLY_W(V, 6); break;            \
-        case 7: RSAPPLY_W(V, 7); break;            \
-        default: RSAPPLY_W(V, 8); break;           \
-        }                                          \
-    } while (0)
-    if (pc->rs_mode) {
-        if (pc->variant == 1) RSAPPLY(1);
-        else if (pc->variant == 0) RSAPPLY(0);
-        else RSAPPLY(2);
-    } else if (pc->group_mode) {
+    // class-group solver (default), else one warp per subdomain (class image
+    // too large for a group), else one CTA-wide solver per subdomain
+    if (pc->group_mode) {
         if (pc->variant == 1) GAPPLY(1);
         else if (pc->variant == 0) GAPPLY(0);
         else GAPPLY(2);
-    } else if (pc->tma_mode) {
-        if (pc->variant == 1) TAPPLY(1);
-        else if (pc->variant == 0) TAPPLY(0);
-        else TAPPLY(2);
     } else if (pc->warp_mode) {
         if (pc->variant == 1) WAPPLY(1);
         else if (pc->variant == 0) WAPPLY(0);
@@ -3045,14 +2037,10 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         else APPLY(2, 128);
     }
 #undef APPLY
-#undef RSAPPLY
-#undef RSAPPLY_W
 #undef WAPPLY
 #undef WAPPLY_D
 #undef GAPPLY
 #undef GAPPLY_W
-#undef GAPPLY_DBG
-#undef TAPPLY
     ACCH_LAUNCHED(ctx);
     if (pc->variant != 1) {
         const long long n = ctx->g.n;

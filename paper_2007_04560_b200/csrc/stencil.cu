@@ -27,7 +27,6 @@
 namespace {
 
 constexpr int RTX = 32, RTY = 8;     // residual tile
-constexpr int MTX = 32, MTY = 8, MRPT = 1;    // matvec tile (rows per thread)
 constexpr int ZCHUNK = 32;           // z planes per block (3D)
 
 __host__ __device__ constexpr int ring_depth(int dim) { return dim == 3 ? 3 : 1; }
@@ -637,230 +636,6 @@ __global__ void jac_prepare_kernel(GridDev g, ParamsDev P, const double2 *__rest
 //   y_u  = w_u/dt - div(cbar grad dG_u) - div(eta_face grad G_u)
 //   y_v  = w_v/dt + cbar/rho (D w_u + (-beta/2 + S) w_v - gamma/2 lap(w_v)) + G_v/rho eta
 // term-for-term the operator assembled at scheme.py:471-482.
-// ---------------------------------------------------------------------------
-
-template <int DIM, int TX, int TY>
-struct MatvecSmem {
-    static constexpr int HX = TX + 4, HY = TY + 4, GX = TX + 2, GY = TY + 2, R = ring_depth(DIM);
-    static constexpr size_t bytes = sizeof(double2) * R * HX * HY + 4 * sizeof(double) * R * GX * GY;
-};
-
-template <int DIM, int TX, int TY, int RPT>
-__global__ void __launch_bounds__(TX *(TY / RPT))
-matvec_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef,
-              const double2 *__restrict__ w_g, double2 *__restrict__ yout)
-{
-    ACCH_SKIP_IF(g);
-    using L = MatvecSmem<DIM, TX, TY>;
-    constexpr int HX = L::HX, HY = L::HY, GX = L::GX, GY = L::GY, R = L::R, TB = TY / RPT, NT = TX * TB;
-    constexpr int NJ = (GX * GY + NT - 1) / NT;   // tile+1-halo cells per thread
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    double2 *sw = reinterpret_cast<double2 *>(smem_raw);
-    double *sdG = reinterpret_cast<double *>(sw + R * HX * HY);
-    double *sEt = sdG + R * GX * GY;
-    double *sCb = sEt + R * GX * GY;
-    double *sGu = sCb + R * GX * GY;
-
-    const long long N = g.nstore;
-    const double4 *__restrict__ cA = co_A(coef);
-    const double2 *__restrict__ cB = co_B(coef, N);
-    const double *__restrict__ cGv = co_Gv(coef, N);
-
-    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int nx = g.nx, ny = g.ny, nz = g.nz;
-    const int zb = (DIM == 3) ? blockIdx.z * ZCHUNK : 0;
-    const int ze = (DIM == 3) ? min(zb + ZCHUNK, nz) : 1;
-    const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
-    const double hg = 0.5 * P.gamma;
-    const double idt = 1.0 / dt, irho = 1.0 / P.rho;
-    const bool per = g.periodic != 0;
-
-    auto load_plane = [&](int kk) {
-        const int slot = (DIM == 3) ? mod3(kk) : 0;
-        const int gz = zplane(g, kk);
-        for (int i = tid; i < HX * HY; i += NT) {
-            const int hx = i % HX, hy = i / HX;
-            const int gx = wrap_coord(x0 + hx - 2, nx, g.periodic);
-            const int gy = wrap_coord(y0 + hy - 2, ny, g.periodic);
-            cp_async16(sw + slot * HX * HY + i, w_g + ((long long)gz * ny + gy) * nx + gx);
-        }
-        cp_async_commit();
-    };
-
-    // coefficient planes for this thread's tile+1-halo cells, fetched one
-    // plane ahead into registers (latency hidden behind a whole plane)
-    double pS[NJ], pD[NJ], pU[NJ], pV[NJ], pC[NJ], pG[NJ];
-    auto prefetch_coef = [&](int kk) {
-        const int gz = zplane(g, kk);
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int i = tid + j * NT;
-            if (i < GX * GY) {
-                const int ex = wrap_coord(x0 + i % GX - 1, nx, g.periodic);
-                const int ey = wrap_coord(y0 + i / GX - 1, ny, g.periodic);
-                const long long c = ((long long)gz * ny + ey) * nx + ex;
-                const double4 a = ldg256(cA + c);
-                const double2 b = __ldg(cB + c);
-                pS[j] = a.x;
-                pD[j] = a.y;
-                pU[j] = a.z;
-                pV[j] = a.w;
-                pC[j] = b.x;
-                pG[j] = b.y;
-            }
-        }
-    };
-
-    // dG_u and eta on tile + 1 halo of plane kk (coefficients already in registers)
-    auto compute_dg = [&](int kk) {
-        const int s0 = (DIM == 3) ? mod3(kk) : 0;
-        const int sm = (DIM == 3) ? mod3(kk - 1) : 0;
-        const int sp = (DIM == 3) ? mod3(kk + 1) : 0;
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-            const int i = tid + j * NT;
-            if (i < GX * GY) {
-                const int h = (i / GX + 1) * HX + (i % GX + 1);
-                const double2 *w = sw + s0 * HX * HY;
-                const double2 w0 = w[h];
-                double lap = (w[h + 1].x - 2.0 * w0.x + w[h - 1].x) * ihx;
-                lap += (w[h + HX].x - 2.0 * w0.x + w[h - HX].x) * ihy;
-                if (DIM == 3) lap += (sw[sp * HX * HY + h].x - 2.0 * w0.x + sw[sm * HX * HY + h].x) * ihz;
-                const int o = s0 * GX * GY + i;
-                sdG[o] = (-0.5 * P.alpha + pS[j]) * w0.x + pD[j] * w0.y - hg * lap;
-                sEt[o] = 0.5 * (pU[j] * w0.x + pV[j] * w0.y);
-                sCb[o] = pC[j];
-                sGu[o] = pG[j];
-            }
-        }
-    };
-
-    // each thread owns RPT output rows of the tile: ty, ty + TB, ...
-    const int x = x0 + tx;
-    int yr[RPT], gcr[RPT], hcr[RPT];
-    bool act[RPT];
-#pragma unroll
-    for (int r = 0; r < RPT; ++r) {
-        yr[r] = y0 + ty + r * TB;
-        act[r] = x < nx && yr[r] < ny;
-        gcr[r] = (ty + r * TB + 1) * GX + (tx + 1);
-        hcr[r] = (ty + r * TB + 2) * HX + (tx + 2);
-    }
-
-    // xy part of lap(w_v) at the thread's own cell of plane k (read before the
-    // ring slot of plane k is recycled for plane k + 3)
-    auto lapv_xy = [&](int k, int hc) {
-        const double2 *w = sw + ((DIM == 3) ? mod3(k) : 0) * HX * HY;
-        const double c = w[hc].y;
-        return (w[hc + 1].y - 2.0 * c + w[hc - 1].y) * ihx + (w[hc + HX].y - 2.0 * c + w[hc - HX].y) * ihy;
-    };
-
-    // y at plane k: w(k) centre, xy lap(w_v), w_v(k -/+ 1) centres passed in
-    auto output = [&](int k, int y, int gc, const double2 &w0, double lxy, double wvm, double wvp) {
-        const int s0 = (DIM == 3) ? mod3(k) : 0;
-        const int sm = (DIM == 3) ? mod3(k - 1) : 0;
-        const int sp = (DIM == 3) ? mod3(k + 1) : 0;
-        const int b0 = s0 * GX * GY + gc;
-        const double dG0 = sdG[b0], E0 = sEt[b0], C0 = sCb[b0], G0 = sGu[b0];
-        double d1 = 0.0, d2 = 0.0;
-        auto face = [&](int bn, double ih, bool lo_ok, bool hi_ok, int bm) {
-            if (hi_ok) {
-                d1 += 0.5 * (C0 + sCb[bn]) * (sdG[bn] - dG0) * ih;
-                d2 += 0.5 * (E0 + sEt[bn]) * (sGu[bn] - G0) * ih;
-            }
-            if (lo_ok) {
-                d1 -= 0.5 * (C0 + sCb[bm]) * (dG0 - sdG[bm]) * ih;
-                d2 -= 0.5 * (E0 + sEt[bm]) * (G0 - sGu[bm]) * ih;
-            }
-        };
-        face(b0 + 1, ihx, per || x > 0, per || x < nx - 1, b0 - 1);
-        face(b0 + GX, ihy, per || y > 0, per || y < ny - 1, b0 - GX);
-        if (DIM == 3) face(sp * GX * GY + gc, ihz, zstep_ok(g, k, -1), zstep_ok(g, k, +1), sm * GX * GY + gc);
-        double lapv = lxy;
-        if (DIM == 3) lapv += (wvp - 2.0 * w0.y + wvm) * ihz;
-        const long long c = cell_at(g, x, y, zplane(g, k));
-        const double4 a = ldg256(cA + c);
-        const double S = a.x, D = a.y, Gv = __ldg(cGv + c);
-        double2 out;
-        // reciprocals as in the reference's assembled blocks (idt = 1/dt,
-        // scheme.py:471); 1/rho once per thread instead of two divisions per cell
-        out.x = w0.x * idt - d1 - d2;
-        out.y = w0.y * idt + (C0 * irho) * (D * w0.x + (-0.5 * P.beta + S) * w0.y - hg * lapv) + (Gv * irho) * E0;
-        yout[c] = out;
-    };
-
-    if (DIM == 2) {
-        prefetch_coef(0);
-        load_plane(0);
-        cp_async_wait_all();
-        __syncthreads();
-        compute_dg(0);
-        __syncthreads();
-#pragma unroll
-        for (int r = 0; r < RPT; ++r)
-            if (act[r]) output(0, yr[r], gcr[r], sw[hcr[r]], lapv_xy(0, hcr[r]), 0.0, 0.0);
-    } else {
-        // pipeline: w ring {k, k+1, k+2} with w(k+3) in flight; dG ring {k-1, k, k+1}
-        prefetch_coef(zb - 1);
-        load_plane(zb - 2);
-        load_plane(zb - 1);
-        load_plane(zb);
-        cp_async_wait_all();
-        __syncthreads();
-        compute_dg(zb - 1);
-        prefetch_coef(zb);
-        __syncthreads();
-        load_plane(zb + 1);
-        cp_async_wait_all();
-        __syncthreads();
-        compute_dg(zb);
-        prefetch_coef(zb + 1);
-        double wvm[RPT];
-#pragma unroll
-        for (int r = 0; r < RPT; ++r) wvm[r] = sw[mod3(zb - 1) * HX * HY + hcr[r]].y;
-        __syncthreads();
-        load_plane(zb + 2);
-        for (int k = zb; k < ze; ++k) {
-            cp_async_wait_all();
-            __syncthreads();
-            double2 w0[RPT];
-            double wvp[RPT], lxy[RPT];
-#pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                w0[r] = sw[mod3(k) * HX * HY + hcr[r]];
-                wvp[r] = sw[mod3(k + 1) * HX * HY + hcr[r]].y;
-                lxy[r] = lapv_xy(k, hcr[r]);
-            }
-            compute_dg(k + 1);
-            if (k + 2 <= ze) prefetch_coef(k + 2);
-            __syncthreads();
-            if (k + 3 <= ze + 1) load_plane(k + 3);
-#pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                if (act[r]) output(k, yr[r], gcr[r], w0[r], lxy[r], wvm[r], wvp[r]);
-                wvm[r] = w0[r].y;
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// z-marching fused matvec, one barrier per plane (3D default).
-//
-// CTA = TX x TY threads over an x-y tile, marching a z range.  Every input
-// byte comes from HBM once per sweep (halo re-reads are L2 hits):
-//   * w: 3-slot smem ring of tile+2 planes, cp.async one plane ahead;
-//   * the tile+1 "columns" (TX*TY centre columns, one per thread, plus the
-//     2 GX + 2 TY ring columns owned by the first threads) carry
-//     dG_u = (-alpha/2 + S) w_u + D w_v - gamma/2 lap w_u and
-//     eta = (c_u w_u + c_v w_v)/2, computed once per column and plane into a
-//     3-slot smem ring B = {(dG_u, cbar), (eta, G_u)};
-//   * coefficient planes are prefetched one plane ahead into registers; the
-//     z-neighbours of a column's w_u stay in the owning thread's registers.
-// Iteration k: wait W(k+2), barrier, issue W(k+3), compute B(k+1), emit y(k)
-// from B(k) (written before the barrier) and the own column's B(k+-1).
-// All per-thread offsets are computed once; the z loop is loads + flops.
 // ---------------------------------------------------------------------------
 
 template <int TX, int TY>
@@ -1568,51 +1343,24 @@ static acch_status launch_matvec_zm_t(acch_ctx *ctx, const double *coef, double 
 
 static acch_status launch_matvec_zm(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
-    const char *e = getenv("ACCH_ZM_MINB");
-    const bool per = ctx->g.periodic != 0;
-    const char *rw = getenv("ACCH_ZM_RW");
-    if (rw && atoi(rw))
-        return per ? launch_matvec_zm_t<2, true, true>(ctx, coef, dt, w, y) : launch_matvec_zm_t<2, false, true>(ctx, coef, dt, w, y);
-    if (e && atoi(e) == 3)
-        return per ? launch_matvec_zm_t<3, true, false>(ctx, coef, dt, w, y) : launch_matvec_zm_t<3, false, false>(ctx, coef, dt, w, y);
-    return per ? launch_matvec_zm_t<2, true, false>(ctx, coef, dt, w, y) : launch_matvec_zm_t<2, false, false>(ctx, coef, dt, w, y);
+    return ctx->g.periodic ? launch_matvec_zm_t<2, true, false>(ctx, coef, dt, w, y)
+                           : launch_matvec_zm_t<2, false, false>(ctx, coef, dt, w, y);
 }
 
 acch_status launch_matvec(acch_ctx *ctx, const double *coef, double dt, const double *w, double *y)
 {
-    // ACCH_MATVEC = zm (3D default) | twopass (2D default) | fused (read per
-    // call so tests can exercise every form on one context)
+    // 3D: the z-marching one-barrier kernel (nz >= 3); 2D: the two-pass form.
+    // ACCH_MATVEC = zm | twopass selects a form (read per call, so the tests
+    // exercise both on one context)
     const char *mode = getenv("ACCH_MATVEC");
     int m = ctx->g.dim == 3 ? 2 : 1;
-    if (mode && strcmp(mode, "fused") == 0) m = 0;
     if (mode && strcmp(mode, "twopass") == 0) m = 1;
     if (mode && strcmp(mode, "zm") == 0 && ctx->g.dim == 3) m = 2;
     if (m == 2 && ctx->g.nz < 3) m = 1;   // the z-marching kernel's plane map assumes nz >= 3
     ctx->matvec_mode = m;
     ProfScope prof_scope(ctx, PC_MATVEC, 88.0 * ctx->g.n);
     if (m == 2) return launch_matvec_zm(ctx, coef, dt, w, y);
-    if (m == 1) return launch_matvec_twopass(ctx, coef, dt, w, y);
-    const GridDev &g = ctx->g;
-    const dim3 block(MTX, MTY / MRPT);
-    if (g.dim == 3) {
-        using L = MatvecSmem<3, MTX, MTY>;
-        static bool configured = false;
-        if (!configured) {
-            acch_status st = set_smem(matvec_kernel<3, MTX, MTY, MRPT>, L::bytes);
-            if (st != ACCH_OK) return st;
-            configured = true;
-        }
-        const dim3 grid((g.nx + MTX - 1) / MTX, (g.ny + MTY - 1) / MTY, (g.nz + ZCHUNK - 1) / ZCHUNK);
-        matvec_kernel<3, MTX, MTY, MRPT><<<grid, block, L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
-                                                                         (double2 *)y);
-    } else {
-        using L = MatvecSmem<2, MTX, MTY>;
-        const dim3 grid((g.nx + MTX - 1) / MTX, (g.ny + MTY - 1) / MTY, 1);
-        matvec_kernel<2, MTX, MTY, MRPT><<<grid, block, L::bytes, ctx->stream>>>(g, ctx->p, dt, coef, (const double2 *)w,
-                                                                         (double2 *)y);
-    }
-    ACCH_LAUNCHED(ctx);
-    return ACCH_OK;
+    return launch_matvec_twopass(ctx, coef, dt, w, y);
 }
 
 acch_status launch_jacobian_blocks(acch_ctx *ctx, const double *coef, double dt, double *out)
