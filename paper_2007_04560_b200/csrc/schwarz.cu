@@ -67,6 +67,11 @@ struct ClassDev {
     const int *lin;   // local cell -> storage offset from the box origin (boxes that do not wrap)
     const int *own_list;   // local ids of the owned cells, ascending
     int n_owned;
+    // left RAS keeps only the owned rows: a backward row i < b_min_row (the
+    // first owned local row) feeds no owned row (row i reads rows j > i only),
+    // so its sweep is skipped, and backward levels >= nlevb_ras hold only
+    // such rows
+    int b_min_row, nlevb_ras;
     int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
     int m_lin, m_ixyz, m_own, m_rel;   // gather / scatter tables in the group image
     int jdup;   // some row has two stencil entries on one pattern position (tiny periodic axes)
@@ -84,6 +89,8 @@ struct ClassHost {
     std::vector<unsigned char> meta;   // ClassDev::meta image
     std::vector<int> lin, own_list;
     int jdup = 0;
+    int b_min_row = 0, nlevb_ras = 0;
+    long long skip_blocks = 0;   // factor blocks of the backward rows below b_min_row
     int m_off[17] = {0};
     int nloc = 0, nnzb = 0, ell_total = 0, max_fwidth = 0, max_bwidth = 0;
     void *dev_mem = nullptr;
@@ -710,16 +717,21 @@ template <int MAXW, typename FT = double4>
 __device__ __forceinline__ void sweep_level(const FT *__restrict__ A, const unsigned short *__restrict__ ecol,
                                             const unsigned short *__restrict__ jo, double2 *y, int base, int m,
                                             int len0, int len1, int i0, int i1, bool backward, int lane, int zero,
-                                            uint64_t pol)
+                                            uint64_t pol, int bmin = 0)
 {
+    // rows below bmin (left-RAS backward sweep: they feed no owned row) are
+    // neither loaded nor written
+    const bool act0 = lane < m && i0 >= bmin, act1 = lane + 32 < m && i1 >= bmin;
+    if (!act0) len0 = 0;
+    if (!act1) len1 = 0;
     // jo[t]: level-relative slot offset of diagonal t (jagged layout; shared
     // memory, warp-uniform), so lane q's slot t is base + jo[t] + q
     FT a[MAXW];
     int c[MAXW];
     FT d0, d1;
     if (backward) {
-        ldg4_pred(d0, A + base + lane, lane < m, pol);
-        ldg4_pred(d1, A + base + lane + 32, lane + 32 < m, pol);
+        ldg4_pred(d0, A + base + lane, act0, pol);
+        ldg4_pred(d1, A + base + lane + 32, act1, pol);
     }
 #pragma unroll
     for (int t = 0; t < MAXW; ++t) {
@@ -771,8 +783,8 @@ __device__ __forceinline__ void sweep_level(const FT *__restrict__ A, const unsi
         acc0 = make_double2(d0.x * acc0.x + d0.y * acc0.y, d0.z * acc0.x + d0.w * acc0.y);
         acc1 = make_double2(d1.x * acc1.x + d1.y * acc1.y, d1.z * acc1.x + d1.w * acc1.y);
     }
-    if (lane < m) y[i0] = acc0;
-    if (lane + 32 < m) y[i1] = acc1;
+    if (act0) y[i0] = acc0;
+    if (act1) y[i1] = acc1;
     __syncwarp();
 }
 
@@ -790,11 +802,12 @@ __device__ __forceinline__ void sweep_rows_wide(const FT *__restrict__ A, const 
                                                 const unsigned short *__restrict__ jo,
                                                 const unsigned short *__restrict__ rows,
                                                 const unsigned short *__restrict__ lens, double2 *y, int base,
-                                                int m, bool backward, int lane, uint64_t pol)
+                                                int m, bool backward, int lane, uint64_t pol, int bmin = 0)
 {
     for (int q = 0; q < m; ++q) {
         const int len = lens[q] - (backward ? 1 : 0);
         const int i = rows[q];
+        if (i < bmin) continue;   // left-RAS backward rows that feed no owned row
         double2 acc = make_double2(0.0, 0.0);
         for (int t0 = 0; t0 < len; t0 += 4 * 32) {
             FT a[4];
@@ -858,7 +871,11 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     const int4 o = sub_origin[s];
     const long long obase = cell_at(g, o.x, o.y, zplane(g, o.z));   // used when o.w (no wrap)
     const FT *__restrict__ A = vals + sub_off[s];
-    const int nall = nlev + nlevb;
+    // left RAS: the backward levels past nlevb_ras and the rows below
+    // b_min_row feed no owned row (see ClassDev) -- skipped
+    const int nlevb_run = VARIANT == 1 ? C.nlevb_ras : nlevb;
+    const int bmin = VARIANT == 1 ? C.b_min_row : 0;
+    const int nall = nlev + nlevb_run;
     auto prefetch_level = [&](int k) {
         if (k >= nall) return;
         int lo, hi;
@@ -926,12 +943,12 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         const int i1 = lane + 32 < m ? f_rows[r0 + lane + 32] : 0;
         sweep_level<MAXW, FT>(A, ecol, f_jo + f_jp[lev], y, f_bs[lev], m, len0, len1, i0, i1, false, lane, zero, pol);
     }
-    for (int lev = 0; lev < nlevb; ++lev) {
+    for (int lev = 0; lev < nlevb_run; ++lev) {
         if (lane == 0) prefetch_level(nlev + lev + pd);
         const int r0 = b_ptr[lev], m = b_ptr[lev + 1] - r0;
         if (WIDE && m <= kWideRows && b_len[r0] > kWideLen + 1) {
             sweep_rows_wide<FT>(A, ecol, b_jo + b_jp[lev] + 1, b_rows + r0, b_len + r0, y, b_bs[lev], m, true, lane,
-                                pol);
+                                pol, bmin);
             continue;
         }
         // slot 0 of every backward row is its inverted diagonal block; U slots follow
@@ -940,7 +957,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
         const int i0 = lane < m ? b_rows[r0 + lane] : 0;
         const int i1 = lane + 32 < m ? b_rows[r0 + lane + 32] : 0;
         sweep_level<MAXW, FT>(A, ecol, b_jo + b_jp[lev] + 1, y, b_bs[lev], m, len0, len1, i0, i1, true, lane, zero,
-                          pol);
+                          pol, bmin);
     }
     if (VARIANT == 1) {
         // owned cells only (left RAS), from the class's owned-cell list
@@ -1286,6 +1303,14 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
         C.owned[l] = own ? 1 : 0;
         if (own) C.own_list.push_back(l);
     }
+    C.b_min_row = C.own_list.empty() ? 0 : C.own_list.front();
+    C.nlevb_ras = 0;
+    for (int k = 0; k + 1 < (int)C.levb_ptr.size(); ++k)
+        for (int q = C.levb_ptr[k]; q < C.levb_ptr[k + 1]; ++q)
+            if (C.levb_rows[q] >= C.b_min_row) C.nlevb_ras = k + 1;
+    C.skip_blocks = 0;
+    for (size_t q = 0; q < C.levb_rows.size(); ++q)
+        if (C.levb_rows[q] < C.b_min_row) C.skip_blocks += C.b_len[q];
     return true;
 }
 
@@ -1450,6 +1475,8 @@ acch_status upload_class(ClassHost &C)
     d.lin = (const int *)(b + o_lin);
     d.own_list = (const int *)(b + o_own);
     d.n_owned = (int)C.own_list.size();
+    d.b_min_row = C.b_min_row;
+    d.nlevb_ras = C.nlevb_ras;
     d.jdup = C.jdup;
     d.meta_bytes = (int)C.meta.size();
     d.m_fbs = C.m_off[1];
@@ -1491,6 +1518,7 @@ struct acch_precond {
     double4 *d_vals = nullptr;
     int wide = 0;                 // some factor row exceeds kWideLen blocks (LU / high fill): warp-wide rows
     long long total_blocks = 0, total_ext = 0, total_nnzb = 0;
+    long long total_skip = 0;   // left-RAS backward blocks the class-group solver never reads
     int *d_bad = nullptr;
     double2 *d_ext_out = nullptr;
     long long *d_cell_ptr = nullptr, *d_cell_src = nullptr;
@@ -1649,6 +1677,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         pc->sub_ext_off.push_back(eo);
         eo += C.nloc;
         pc->total_nnzb += C.nnzb;
+        pc->total_skip += C.skip_blocks;
         max_nloc = std::max(max_nloc, C.nloc);
     }
     int max_width = 0;
@@ -1986,7 +2015,11 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     const int groups = 128 / pc->tps;
     const unsigned nb = (unsigned)((pc->nsub + groups - 1) / groups);
     const size_t sm = pc->apply_smem;
-    ProfScope prof_scope(ctx, PC_APPLY, 32.0 * pc->total_nnzb + 16.0 * pc->total_ext + 16.0 * ctx->g.n);
+    // algorithmic bytes: every factor block the sweeps need (left RAS in the
+    // class-group solver skips the backward rows that feed no owned cell),
+    // the gather of r over the extended boxes, the write of z
+    const long long blocks = pc->total_nnzb - (pc->group_mode && pc->variant == 1 ? pc->total_skip : 0);
+    ProfScope prof_scope(ctx, PC_APPLY, 32.0 * blocks + 16.0 * pc->total_ext + 16.0 * ctx->g.n);
 #define APPLY(V, T)                                                                                    \
     apply_kernel<V, T><<<nb, 128, sm, ctx->stream>>>(ctx->g, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, \
         pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals, (const double2 *)r, (double2 *)z, pc->d_ext_out,      \

@@ -160,6 +160,21 @@ __device__ __forceinline__ double cell_gap_fast(double u, double v)
     return (v != v) ? v : g;
 }
 
+// 1/x for 0 < x <= 1/4 (x = z (1 - z) of an admissible chord pair): the
+// hardware reciprocal seed and three Newton steps, no special-case branch
+// (the argument is never 0, denormal, inf or NaN on the path that uses it)
+__device__ __forceinline__ double rcp_quarter(double x)
+{
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+    double e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-x, y, 1.0);
+    return fma(y, e, y);
+}
+
 template <int ORDER>
 __device__ __forceinline__ double chord_res(double a, double b, const ParamsDev &P)
 {
@@ -178,7 +193,7 @@ __device__ __forceinline__ double chord_res(double a, double b, const ParamsDev 
     const bool near = !exact && as <= 0.4 * zeta && as <= 0.4 * w;   // 0.4 min(zeta, 1 - zeta)
     double val = lg;
     if (__any_sync(0xffffffffu, near)) {
-        const double r = 1.0 / (zeta * w);              // 1/zeta = w r, 1/w = zeta r
+        const double r = rcp_quarter(zeta * w);         // 1/zeta = w r, 1/w = zeta r
         const double rz = sigma * (w * r), rw = sigma * (zeta * r);
         const double tz = rz * rz, tw = rw * rw;
         double pz, pw;
@@ -435,14 +450,24 @@ res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__re
     const bool fxl = PER || x > 0, fxh = PER || x < nx - 1, fyl = PER || y > 0, fyh = PER || y < ny - 1;
     const int jn = has_ring ? 2 : 1;
 
+    // shared-memory addresses of this thread's copy targets in slot 0 and
+    // its source pointers, computed once (per plane only the offsets move)
+    const unsigned sn0 = (unsigned)__cvta_generic_to_shared(sN + tid);
+    const unsigned so0 = (unsigned)__cvta_generic_to_shared(sO + tid);
+    const double2 *srcn_r[NWR], *srco_r[NWR];
+#pragma unroll
+    for (int r = 0; r < NWR; ++r) {
+        srcn_r[r] = xn_g + woff[r];
+        srco_r[r] = xo_g + woff[r];
+    }
     auto load_x = [&](long long poff, int slot) {
-        const double2 *srcn = xn_g + poff, *srco = xo_g + poff;
-        double2 *dn = sN + slot * NW + tid, *dO = sO + slot * NW + tid;
+        const unsigned so = (unsigned)(slot * NW) * (unsigned)sizeof(double2);
 #pragma unroll
         for (int r = 0; r < NWR; ++r)
             if (r < NWR - 1 || tid + r * NTA < NW) {
-                cp_async16(dn + r * NTA, srcn + woff[r]);
-                cp_async16(dO + r * NTA, srco + woff[r]);
+                const unsigned ro = so + (unsigned)(r * NTA) * (unsigned)sizeof(double2);
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sn0 + ro), "l"(srcn_r[r] + poff));
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(so0 + ro), "l"(srco_r[r] + poff));
             }
     };
 

@@ -19,7 +19,7 @@ if [ -z "${NOLAUNCH:-}" ]; then
   python tools/ncu_summary.py $TMP/launches.csv > $OUT/launches_${TAG}_summary.txt
   gzip -c $TMP/launches.csv > $OUT/launches_$TAG.csv.gz
 fi
-for k in apply_group lagupd32 "lagupd_kernel" mdot_grouped mv_zm res_zm factor_kernel; do
+for k in apply_group lagupd_dev mdot_grouped mv_zm res_zm factor_kernel; do
   name=$(echo "$k" | tr -c 'a-z0-9_\n' '_')
   timeout 300 ncu --set full --clock-control none --import-source on -k regex:"$k" -s 2 -c 1 \
       -o $TMP/${TAG}_full_$name python tools/micro.py > $OUT/ncu_${TAG}_$name.log 2>&1
