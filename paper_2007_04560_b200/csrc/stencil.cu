@@ -1228,10 +1228,10 @@ static int choose_zchunks(int tiles, int nz, int per_sm, int sms, double startup
     return best;
 }
 
-template <int MINB, bool PER, bool RW, int ORDER>
+template <int MINB, bool PER, bool RW, int ORDER, int TY = 8>
 static acch_status launch_residual_zm_t(acch_ctx *ctx, const double *x_old, double dt, const double *x, double *F)
 {
-    constexpr int TX = 32, TY = 8;
+    constexpr int TX = 32;
     using L = RzmSmem<TX, TY>;
     constexpr int NTA = TX * TY + (RW ? 32 * ((L::NRING + 31) / 32) : 0);
     auto kern = res_zm_kernel<TX, TY, MINB, PER, RW, ORDER>;
@@ -1264,6 +1264,11 @@ acch_status launch_residual(acch_ctx *ctx, const double *x_old, double dt, const
         // ring warps (every thread one column, measured fastest); the
         // reference's default series order 10 compiled in
         if (ctx->p.order == 10) {
+            static const int ty = getenv("ACCH_RES_TY") ? atoi(getenv("ACCH_RES_TY")) : 8;   // experiment
+            if (ty == 16) {
+                if (g.periodic) return launch_residual_zm_t<1, true, true, 10, 16>(ctx, x_old, dt, x, F);
+                return launch_residual_zm_t<1, false, true, 10, 16>(ctx, x_old, dt, x, F);
+            }
             if (g.periodic) return launch_residual_zm_t<2, true, true, 10>(ctx, x_old, dt, x, F);
             return launch_residual_zm_t<2, false, true, 10>(ctx, x_old, dt, x, F);
         }
