@@ -318,3 +318,30 @@ def test_operator_conservation_sbp_and_semipositivity(bc, counts):
     assert abs(lhs - rhs) <= 1e-9 * (abs(lhs) + abs(rhs))
     assert float(np.dot(gv, A[:, 1])) >= 0.0
     np.testing.assert_allclose(A[:, 1], cbar / PARAMS.rho * gv, rtol=1e-9, atol=1e-9 * np.max(np.abs(A[:, 1])))
+
+
+# --------------------------------------------------------------------------- output files
+
+def test_simulate_writes_history_and_snapshots(tmp_path):
+    """simulate(out_dir=...) writes the reference's history CSV (flushed per
+    step) and VTK snapshots (requested times, every k steps, final), and the
+    files read back to the run's values (cli/drivers.py:76-184, io.py)."""
+    from paper_2007_04560_b200.drivers import (InitialSpec, OutputSpec, RunConfig, SolverSpec, TimeSpec,
+                                               simulate)
+    from paper_2007_04560_b200.io import read_history, read_vtk, state_from_vtk
+    g = Grid((16, 16), (1.0, 1.0), BoundaryCondition.PERIODIC)
+    cfg = RunConfig(g, PARAMS, InitialSpec("random_uniform", 0.5, 0.05, 1234),
+                    TimeSpec(horizon=4e-4, mode="fixed", dt=1e-4), SolverSpec(subdomains=4),
+                    OutputSpec(history="h.csv", snapshot_times=(2e-4,), snapshot_every=3))
+    res = simulate(cfg, out_dir=str(tmp_path), device=DEV)
+    rows = read_history(str(tmp_path / "h.csv"))
+    assert [r.step for r in rows] == [r.step for r in res.history] == [0, 1, 2, 3, 4]
+    for a, b in zip(rows, res.history):
+        assert (a.time, a.dt, a.energy, a.mass_u, a.newton, a.gmres) == (b.time, b.dt, b.energy, b.mass_u, b.newton,
+                                                                          b.gmres)
+    assert (tmp_path / "snapshot_t0.0002.vtk").exists() and (tmp_path / "step_000003.vtk").exists()
+    u, v = res.final_state.to_numpy()
+    meta = read_vtk(str(tmp_path / "final.vtk"))
+    np.testing.assert_array_equal(meta["arrays"]["u"], u.ravel())
+    back = state_from_vtk(str(tmp_path / "final.vtk"), BoundaryCondition.PERIODIC, device=DEV)
+    assert torch.equal(back.x, res.final_state.x)

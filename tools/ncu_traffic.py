@@ -16,8 +16,8 @@ CATEGORY = {"apply_group_kernel": "precond_apply", "apply_warp_kernel": "precond
             "residual_kernel": "residual", "factor_kernel": "precond_factor",
             "mdot_grouped_kernel": "krylov_dot", "mupdate_kernel": "krylov_update",
             "mupdate_mdot_kernel": "krylov_update", "mupdate_mdot32_kernel": "krylov_update",
-            "mv_zm_kernel": "matvec", "res_zm_kernel": "residual", "lagupd_kernel": "krylov_update",
-            "lagupd32_kernel": "krylov_update", "apply_rs_kernel": None}
+            "mv_zm_kernel": "matvec", "res_zm_kernel": "residual", "lagupd_dev_kernel": "krylov_update",
+            "lagupd_kernel": "krylov_update"}
 UNIT = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
 
 out = {}
