@@ -409,14 +409,15 @@ def test_schwarz_tiny_periodic_axis_matches_oracle(counts):
 
 @pytest.mark.parametrize("solver", ["ilu0", "ilu2", "lu"])
 @pytest.mark.parametrize("bc", [BoundaryCondition.PERIODIC, BoundaryCondition.NEUMANN])
-def test_factorisation_threads_bitwise_equal(solver, bc, monkeypatch):
+@pytest.mark.parametrize("counts", [(12, 12, 12), (4, 10, 12), (16, 12)])
+def test_factorisation_threads_bitwise_equal(solver, bc, counts, monkeypatch):
     """factor_kernel with 32 / 64 / 128 threads per subdomain CTA (read once
     at preconditioner creation, ACCH_FACTOR_THREADS) performs every row's
     updates in the same order -- the one-warp default in 3D, the CTA-wide
     elimination of narrow levels with long rows at 128: the factors, and so
     the applies, agree bitwise.  Unsupported values are rejected."""
     rng = np.random.default_rng(9)
-    g = Grid((12, 12, 12), (1.0, 1.0, 1.0), bc)
+    g = Grid(counts, (1.0,) * len(counts), bc)
     uo, vo = 0.5 + rng.uniform(-0.05, 0.05, g.array_shape), rng.uniform(-0.05, 0.05, g.array_shape)
     un, vn = uo + rng.uniform(-0.01, 0.01, g.array_shape), vo + rng.uniform(-0.01, 0.01, g.array_shape)
     prob = StepProblem.create(g, PARAMS, st(g, uo, vo), 1e-3)
