@@ -57,6 +57,7 @@ def parse_args():
     ap.add_argument("--dim", type=int, default=3)
     ap.add_argument("--box", type=int, default=8, help="RAS box edge in cells")
     ap.add_argument("--solver", default="ilu0")
+    ap.add_argument("--overlap", type=int, default=1)
     ap.add_argument("--variant", default="ras-left")
     ap.add_argument("--restart", type=int, default=30)
     ap.add_argument("--ortho", default="dcgs2", choices=["cgs2", "dcgs2", "mgs"])
@@ -148,7 +149,7 @@ def make_config(args, world=1, rank=0):
     cfg = RunConfig(grid, Params(4.0, 2.0, 0.005, 0.1, 0.001),
                     InitialSpec("random_uniform", 0.5, 0.01, 1234),
                     TimeSpec(horizon=10.0, mode="adaptive", dt_min=1e-4, dt_max=10.0),
-                    SolverSpec(preconditioner=SchwarzVariant(args.variant), overlap=1,
+                    SolverSpec(preconditioner=SchwarzVariant(args.variant), overlap=args.overlap,
                                subdomain_solver=SubdomainSolverSpec.from_string(args.solver), subdomains=nsub,
                                gmres_restart=args.restart, orthogonalization=args.ortho))
     return cfg, nsub
@@ -156,7 +157,7 @@ def make_config(args, world=1, rank=0):
 
 def workload_name(args):
     return (f"AC/CH {args.dim}D {args.n}^{args.dim} periodic fp64, adaptive dt (eta=1e2), NKS: Newton + "
-            f"GMRES({args.restart}) + {args.variant} {args.box}^{args.dim}-cell boxes overlap 1 {args.solver}")
+            f"GMRES({args.restart}) + {args.variant} {args.box}^{args.dim}-cell boxes overlap {args.overlap} {args.solver}")
 
 
 # ---------------------------------------------------------------------------
@@ -200,7 +201,8 @@ def import_reference():
 
 
 def window_key(args):
-    return f"{args.n}^{args.dim}:box{args.box}:{args.solver}:{args.variant}:r{args.restart}:W{args.warmup}:K{args.steps}"
+    ov = "" if args.overlap == 1 else f"ov{args.overlap}:"
+    return f"{args.n}^{args.dim}:box{args.box}:{ov}{args.solver}:{args.variant}:r{args.restart}:W{args.warmup}:K{args.steps}"
 
 
 def load_counts(args):
