@@ -316,9 +316,13 @@ __device__ __forceinline__ void ldg4_pred(double4 &v, const double4 *p, bool pre
                  : "l"(p), "r"((unsigned)pred), "l"(pol));
 }
 
-// levels of at most kWideRows rows whose longest row exceeds kWideLen blocks
-// are swept warp-wide (sweep_rows_wide*, exact LU / high fill)
-constexpr int kWideRows = 4, kWideLen = 32;
+// A preconditioner whose longest factor row exceeds kWideLen blocks (exact LU,
+// ILU(k >= 1)) runs the WIDE kernel instances.  There, a level of at most
+// kWideRows rows whose longest row has more than kWideMin blocks -- past the
+// lane-per-row sweep's MAXW slots in flight, where every extra block costs
+// that sweep a round trip -- is swept warp-wide (sweep_level_wide): a single
+// row by all 32 lanes, 2..8 rows together by groups of 16 / 8 / 4 lanes.
+constexpr int kWideRows = 8, kWideLen = 32, kWideMin = 12;
 
 __device__ __forceinline__ int anchor_bits(const double4 &a) { return __double2hiint(a.x); }
 
@@ -434,6 +438,82 @@ apply_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restr
     }
 }
 
+// Narrow level (<= kWideRows rows) with long rows (exact LU / ILU(k >= 1)
+// fill): the level's rows are swept TOGETHER, each by its own group of
+// G = 32 / m2 lanes (m2 = 1, 2, 4 or 8 >= the row count).  Lane j of a group
+// takes blocks j, j + G, ... of its row -- every load of the level in flight
+// at once -- a shuffle tree inside the group sums the partial products and
+// the group's first lane finishes the row.  One memory round trip per LEVEL
+// instead of one per row: ILU(2) on 10^3 boxes has 343 + 343 levels of <= 4
+// rows of up to 90 blocks (128^3 apply 8.0 -> 4.7 ms), ILU(1) 163 levels of
+// <= 8 rows of up to 34 blocks (8.0 -> 3.4 ms); exact LU levels are single
+// rows (G = 32).  profiles/r02/wide_sweep_variants.txt.
+// UB = 6 blocks in flight per lane (4 and 8 measured slower; 12 spills next
+// to the lane-per-row sweep's own 12-slot arrays).
+constexpr int kWideUB = 6;
+// Slot addressing: TABLE = the group solver's shared-memory tables (jo[t]:
+// level-relative offset of jagged diagonal t, ecol as uint16 in shared
+// memory); else the warp solver's closed form (rows sorted by decreasing
+// length L[0..7]: offset of diagonal t = sum_q min(L[q], t); ecol in global).
+template <typename FT, bool TABLE, int UB>
+__device__ __forceinline__ void sweep_level_wide(const FT *__restrict__ A, const void *__restrict__ ecol_v,
+                                              const unsigned short *__restrict__ jo, int4 L4, int4 L8, int base, int first,
+                                              const unsigned short *__restrict__ rows,
+                                              const unsigned short *__restrict__ lens, double2 *y, int m,
+                                              bool backward, int lane, int bmin, uint64_t pol)
+{
+    const int m2 = m <= 1 ? 1 : (m == 2 ? 2 : (m <= 4 ? 4 : 8));
+    const int G = 32 / m2;
+    const int q = lane / G, j = lane - q * G;
+    const bool has = q < m;
+    const int i = has ? rows[q] : 0;
+    // left-RAS backward rows below bmin feed no owned row: neither loaded nor written
+    const bool act = has && i >= bmin;
+    const int len = act ? lens[q] - (backward ? 1 : 0) : 0;
+    auto slot = [&](int t) {
+        if (TABLE) return base + jo[t] + q;
+        return base + first + min(L4.x, t) + min(L4.y, t) + min(L4.z, t) + min(L4.w, t) + min(L8.x, t) +
+               min(L8.y, t) + min(L8.z, t) + min(L8.w, t) + q;
+    };
+    double2 acc = make_double2(0.0, 0.0);
+    for (int t0 = 0; __any_sync(0xffffffffu, t0 < len); t0 += UB * G) {
+        FT a[UB];
+        int c[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int t = t0 + u * G + j;
+            if (t < len) {
+                const int e = slot(t);
+                // the group solver's streaming loads skip L1 and are evicted first from L2
+                if (TABLE) ldg4_pred(a[u], A + e, true, pol);
+                else a[u] = ldg4(A + e);
+                c[u] = TABLE ? (int)reinterpret_cast<const unsigned short *>(ecol_v)[e]
+                             : __ldg(reinterpret_cast<const int *>(ecol_v) + e);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u)
+            if (t0 + u * G + j < len) blk_sub(acc, a[u], y[c[u]]);
+    }
+    for (int off = G >> 1; off > 0; off >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
+    }
+    if (act && j == 0) {
+        double2 v = y[i];
+        v.x += acc.x;
+        v.y += acc.y;
+        if (backward) {
+            FT d;
+            if (TABLE) ldg4_pred(d, A + base + q, true, pol);
+            else d = ldg4(A + base + q);
+            v = make_double2(d.x * v.x + d.y * v.y, d.z * v.x + d.w * v.y);
+        }
+        y[i] = v;
+    }
+    __syncwarp();
+}
+
 // Warp-per-subdomain solver (boxes with <= 32767 cells and levels <= 64 wide).
 // Shared memory per subdomain: y (double2 per cell) plus the class's level
 // metadata (row lists as uint16, row lengths as uint8, level starts/bases), so
@@ -451,57 +531,21 @@ struct WarpSmem {
     }
 };
 
-// Warp-wide sweep of a narrow level (<= 4 rows) with long rows in the
-// ballot-offset layout of apply_warp_kernel: slot (t, q) = base + first +
-// sum_q' min(len_q', t) + q, rows sorted by decreasing length (see
-// sweep_rows_wide for the group solver's table-offset layout).
+// Warp solver's narrow long-row levels: slot (t, q) = base + first +
+// sum_q' min(len_q', t) + q, rows sorted by decreasing length (closed form of
+// the jagged-diagonal offsets; the group solver reads them from a table).
 __device__ __forceinline__ void sweep_rows_wide_warp(const double4 *__restrict__ A,
                                                      const int *__restrict__ ecol,
                                                      const unsigned short *__restrict__ rows,
                                                      const unsigned short *__restrict__ lens, double2 *y, int base,
                                                      int m, bool backward, int lane)
 {
-    int L[4];
+    int L[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) L[q] = q < m ? lens[q] - (backward ? 1 : 0) : 0;
-    const int first = backward ? m : 0;
-    for (int q = 0; q < m; ++q) {
-        const int len = L[q];
-        const int i = rows[q];
-        double2 acc = make_double2(0.0, 0.0);
-        for (int t0 = 0; t0 < len; t0 += 4 * 32) {
-            double4 a[4];
-            int c[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = t0 + u * 32 + lane;
-                if (t < len) {
-                    const int e = base + first + min(L[0], t) + min(L[1], t) + min(L[2], t) + min(L[3], t) + q;
-                    a[u] = ldg4(A + e);
-                    c[u] = __ldg(ecol + e);
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (t0 + u * 32 + lane < len) blk_sub(acc, a[u], y[c[u]]);
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-        }
-        if (lane == 0) {
-            double2 v = y[i];
-            v.x += acc.x;
-            v.y += acc.y;
-            if (backward) {
-                const double4 d = ldg4(A + base + q);
-                v = make_double2(d.x * v.x + d.y * v.y, d.z * v.x + d.w * v.y);
-            }
-            y[i] = v;
-        }
-        __syncwarp();
-    }
+    for (int q = 0; q < 8; ++q) L[q] = q < m ? lens[q] - (backward ? 1 : 0) : 0;
+    sweep_level_wide<double4, false, kWideUB>(A, ecol, nullptr, make_int4(L[0], L[1], L[2], L[3]),
+                                                   make_int4(L[4], L[5], L[6], L[7]), base, backward ? m : 0, rows,
+                                                   lens, y, m, backward, lane, 0, 0ull);
 }
 
 template <int VARIANT, int MAXW = 12, int PREFETCH_DEPTH = 4, bool WIDE = false>
@@ -578,7 +622,7 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     for (int lev = 0; lev < C.nlev; ++lev) {
         if (lane == 0) prefetch_level(lev + PREFETCH_DEPTH);
         const int r0 = f_ptr[lev], m = f_ptr[lev + 1] - r0, base = f_bs[lev];
-        if (WIDE && m <= kWideRows && f_len[r0] > kWideLen) {
+        if (WIDE && m <= kWideRows && f_len[r0] > kWideMin) {
             sweep_rows_wide_warp(A, C.ecol, f_rows + r0, f_len + r0, y, base, m, false, lane);
             continue;
         }
@@ -628,7 +672,7 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     for (int lev = 0; lev < C.nlevb; ++lev) {
         if (lane == 0) prefetch_level(C.nlev + lev + PREFETCH_DEPTH);
         const int r0 = b_ptr[lev], m = b_ptr[lev + 1] - r0, base = b_bs[lev];
-        if (WIDE && m <= kWideRows && b_len[r0] > kWideLen + 1) {
+        if (WIDE && m <= kWideRows && b_len[r0] > kWideMin + 1) {
             sweep_rows_wide_warp(A, C.ecol, b_rows + r0, b_len + r0, y, base, m, true, lane);
             continue;
         }
@@ -788,15 +832,6 @@ __device__ __forceinline__ void sweep_level(const FT *__restrict__ A, const unsi
     __syncwarp();
 }
 
-// A level of at most kWideRows rows whose longest row has more than kWideLen
-// blocks (exact LU / high fill: the factor's levels shrink to single rows of
-// 30-80 blocks): the whole warp works on one row at a time -- lane l takes
-// blocks l, l + 32, ... (all loads in flight at once), then a shuffle tree
-// sums the partial products.  One memory round trip per row instead of one
-// per 4-block batch of a single lane.  (ILU(0) rows never exceed 21 blocks,
-// so the ILU(0) sweeps -- and their bitwise agreement across solvers -- are
-// untouched.)
-
 template <typename FT>
 __device__ __forceinline__ void sweep_rows_wide(const FT *__restrict__ A, const unsigned short *__restrict__ ecol,
                                                 const unsigned short *__restrict__ jo,
@@ -804,43 +839,9 @@ __device__ __forceinline__ void sweep_rows_wide(const FT *__restrict__ A, const 
                                                 const unsigned short *__restrict__ lens, double2 *y, int base,
                                                 int m, bool backward, int lane, uint64_t pol, int bmin = 0)
 {
-    for (int q = 0; q < m; ++q) {
-        const int len = lens[q] - (backward ? 1 : 0);
-        const int i = rows[q];
-        if (i < bmin) continue;   // left-RAS backward rows that feed no owned row
-        double2 acc = make_double2(0.0, 0.0);
-        for (int t0 = 0; t0 < len; t0 += 4 * 32) {
-            FT a[4];
-            int c[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int t = t0 + u * 32 + lane;
-                const int e = base + jo[t < len ? t : 0] + q;
-                ldg4_pred(a[u], A + e, t < len, pol);
-                c[u] = t < len ? ecol[e] : 0;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u)
-                if (t0 + u * 32 + lane < len) blk_sub(acc, a[u], y[c[u]]);
-        }
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            acc.x += __shfl_xor_sync(0xffffffffu, acc.x, off);
-            acc.y += __shfl_xor_sync(0xffffffffu, acc.y, off);
-        }
-        if (lane == 0) {
-            double2 v = y[i];
-            v.x += acc.x;
-            v.y += acc.y;
-            if (backward) {
-                FT d;
-                ldg4_pred(d, A + base + q, true, pol);
-                v = make_double2(d.x * v.x + d.y * v.y, d.z * v.x + d.w * v.y);
-            }
-            y[i] = v;
-        }
-        __syncwarp();
-    }
+    // jo[t]: level-relative offset of jagged diagonal t (for backward levels
+    // the caller passes jo + 1: diagonal 0 holds the inverted diagonal blocks)
+    sweep_level_wide<FT, true, kWideUB>(A, ecol, jo, make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0), base, 0, rows, lens, y, m, backward, lane, bmin, pol);
 }
 
 // one subdomain of a class group: gather, forward and backward sweeps, scatter
@@ -932,7 +933,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     for (int lev = 0; lev < nlev; ++lev) {
         if (lane == 0) prefetch_level(lev + pd);
         const int r0 = f_ptr[lev], m = f_ptr[lev + 1] - r0;
-        if (WIDE && m <= kWideRows && f_len[r0] > kWideLen) {
+        if (WIDE && m <= kWideRows && f_len[r0] > kWideMin) {
             sweep_rows_wide<FT>(A, ecol, f_jo + f_jp[lev], f_rows + r0, f_len + r0, y, f_bs[lev], m, false, lane,
                                 pol);
             continue;
@@ -946,7 +947,7 @@ __device__ __forceinline__ void group_solve_one(const GridDev &g, const ClassDev
     for (int lev = 0; lev < nlevb_run; ++lev) {
         if (lane == 0) prefetch_level(nlev + lev + pd);
         const int r0 = b_ptr[lev], m = b_ptr[lev + 1] - r0;
-        if (WIDE && m <= kWideRows && b_len[r0] > kWideLen + 1) {
+        if (WIDE && m <= kWideRows && b_len[r0] > kWideMin + 1) {
             sweep_rows_wide<FT>(A, ecol, b_jo + b_jp[lev] + 1, b_rows + r0, b_len + r0, y, b_bs[lev], m, true, lane,
                                 pol, bmin);
             continue;
