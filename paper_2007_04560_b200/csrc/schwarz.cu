@@ -75,6 +75,11 @@ struct ClassDev {
     int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
     int m_lin, m_ixyz, m_own, m_rel;   // gather / scatter tables in the group image
     int jdup;   // some row has two stencil entries on one pattern position (tiny periodic axes)
+    // column-major layout of a narrow class (apply_cols_kernel): step words
+    // (forward steps, then backward), row index of every slot, first backward slot
+    const unsigned *col_steps;
+    const unsigned short *col_ridx;
+    int col_nf, col_nb, col_nb_ras, col_bstart, col_end, col_end_ras;
 };
 
 struct ClassHost {
@@ -86,6 +91,11 @@ struct ClassHost {
     std::vector<unsigned short> f_len8, b_len8;
     std::vector<int2> upd;
     std::vector<unsigned char> owned;
+    std::vector<int> jmap_csr;          // jmap / upd by CSR entry (before the slot layout is applied)
+    std::vector<int2> upd_csr;
+    std::vector<unsigned> col_steps;
+    std::vector<unsigned short> col_ridx;
+    int col_nf = 0, col_nb = 0, col_nb_ras = 0, col_bstart = 0, col_end = 0, col_end_ras = 0;
     std::vector<unsigned char> meta;   // ClassDev::meta image
     std::vector<int> lin, own_list;
     int jdup = 0;
@@ -739,6 +749,214 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
 }
 
 // ---------------------------------------------------------------------------
+// Column-sweep solver for narrow classes: every level of every class has at
+// most kWideRows rows (exact LU: single rows; ILU(1) / ILU(2) on 10^3 boxes:
+// <= 8 / <= 4 rows), so the solve is latency-bound on its dependency chain.
+// A row-oriented sweep ends every row with a warp-wide reduction tree; the
+// column-oriented one has none: once x_j is final, lane l subtracts
+// L_ij x_j from y_i for its entry (i, j) of column j -- distinct rows, so
+// distinct shared-memory words -- and the chain per column is one
+// shared-memory broadcast of x_j, one 2x2 block product and one store.
+// The factors of these classes are stored COLUMN-major (relayout_columns):
+// the forward sweep streams the L columns 0..n-1, the backward sweep the U
+// columns n-1..0 (inverted diagonal block first): ONE contiguous stream of
+// slots, which the TMA engine copies tile by tile (cp.async.bulk + mbarrier)
+// into a shared-memory ring kColRing tiles ahead of the sweep -- register
+// prefetching cannot run that deep (six scoreboards per warp: waiting for
+// the oldest of many loads in flight waits for the newest too; measured).
+// A step is a column, or a 64-entry piece of a longer one:
+// word = column | entries << 16 | tiles to wait for << 23 | tiles to hand back << 25 | first << 31.
+// Row i accumulates its terms in column order, which is the reference's own
+// order (_ilu.py:123-137).
+// ---------------------------------------------------------------------------
+constexpr int kColChunk = 64;   // entries per step (two per lane)
+#ifndef ACCH_COL_TILE
+#define ACCH_COL_TILE 256
+#endif
+#ifndef ACCH_COL_RING
+#define ACCH_COL_RING 2
+#endif
+constexpr int kColTile = ACCH_COL_TILE;    // factor slots per TMA tile (4 KB of blocks + 256 B of row ids)
+constexpr int kColRing = ACCH_COL_RING;     // tiles in the shared-memory ring
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, unsigned bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, unsigned parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+struct ColSmem {
+    int max_nloc, max_steps;
+    __host__ __device__ size_t y_bytes() const { return (sizeof(double2) * (size_t)max_nloc + 127) / 128 * 128; }
+    __host__ __device__ size_t steps_bytes() const { return (sizeof(unsigned) * (size_t)max_steps + 127) / 128 * 128; }
+    __host__ __device__ size_t bytes() const
+    {
+        return y_bytes() + steps_bytes() + (size_t)kColRing * kColTile * (sizeof(double4) + sizeof(unsigned short)) +
+               sizeof(uint64_t) * kColRing;
+    }
+};
+
+template <int VARIANT>
+__global__ void __launch_bounds__(32, 8)
+apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
+                  const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
+                  const long long *__restrict__ sub_ext_off, const double4 *__restrict__ vals,
+                  const double2 *__restrict__ r, double2 *__restrict__ z, double2 *__restrict__ ext_out, ColSmem L,
+                  long long nsub)
+{
+    ACCH_SKIP_IF(g);
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int lane = threadIdx.x;
+    const long long s = blockIdx.x;
+    if (s >= nsub) return;
+    const ClassDev C = classes[sub_class[s]];
+    const int4 o = sub_origin[s];
+    const double4 *__restrict__ A = vals + sub_off[s];
+    double2 *y = reinterpret_cast<double2 *>(smem_raw);
+    unsigned *steps = reinterpret_cast<unsigned *>(smem_raw + L.y_bytes());
+    double4 *ringA = reinterpret_cast<double4 *>(smem_raw + L.y_bytes() + L.steps_bytes());
+    unsigned short *ringI = reinterpret_cast<unsigned short *>(ringA + kColRing * kColTile);
+    uint64_t *bars = reinterpret_cast<uint64_t *>(ringI + kColRing * kColTile);
+    // left RAS: the backward columns below the first owned row update only
+    // rows that are never scattered
+    const int nf = C.col_nf, nb = VARIANT == 1 ? C.col_nb_ras : C.col_nb;
+    const int end_slot = VARIANT == 1 ? C.col_end_ras : C.col_end;
+    const int ntiles = (end_slot + kColTile - 1) / kColTile;
+    if (lane == 0) {
+        for (int i = 0; i < kColRing; ++i) mbar_init(bars + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    // tile c of the factor stream (blocks + row ids) into ring slot c % kColRing
+    auto issue = [&](int c) {
+        if (c >= ntiles || lane != 0) return;
+        const int k = c % kColRing;
+#ifdef ACCH_COL_FENCE
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+#endif
+        mbar_expect_tx(bars + k, kColTile * (unsigned)(sizeof(double4) + sizeof(unsigned short)));
+        bulk_g2s(ringA + k * kColTile, A + (size_t)c * kColTile, kColTile * (unsigned)sizeof(double4), bars + k);
+        bulk_g2s(ringI + k * kColTile, C.col_ridx + (size_t)c * kColTile, kColTile * (unsigned)sizeof(unsigned short),
+                 bars + k);
+        // and pull the stream into L2 further ahead
+        if (c + 2 * kColRing < ntiles)
+            prefetch_l2(A + (size_t)(c + 2 * kColRing) * kColTile, kColTile * (unsigned)sizeof(double4));
+    };
+#pragma unroll
+    for (int c = 0; c < kColRing; ++c) issue(c);
+    for (int i = lane; i < nf + nb; i += 32) steps[i] = C.col_steps[i];
+    for (int l = lane; l < C.nloc; l += 32) {
+        int gx, gy, gz;
+        local_to_global(g, C, o, l, gx, gy, gz);
+        double2 v = r[cell_at(g, gx, gy, zplane(g, gz))];
+        if (VARIANT == 2 && !C.owned[l]) v = make_double2(0.0, 0.0);
+        y[l] = v;
+    }
+    __syncwarp();
+
+    constexpr int RM = kColRing * kColTile - 1;   // ring index mask
+    int e = 0;        // next slot of the stream (warp-uniform)
+    int ready = 0;    // tiles waited for
+    int freed = 0;    // tiles handed back (and refilled)
+    // the step word says how many new tiles the step reads (0 for most steps) ...
+    auto acquire = [&](unsigned w) {
+        for (int k = (int)((w >> 23) & 3u); k > 0; --k) {
+            mbar_wait(bars + (ready % kColRing), (unsigned)(ready / kColRing) & 1u);
+            ++ready;
+        }
+    };
+    // ... and how many the stream has left behind once it is done (after its __syncwarp)
+    auto release = [&](unsigned w) {
+        for (int k = (int)((w >> 25) & 3u); k > 0; --k) {
+            issue(freed + kColRing);
+            ++freed;
+        }
+    };
+    auto entries = [&](int n, const double2 x) {
+        if (lane < n) {
+            const int q = (e + lane) & RM;
+            const int i = ringI[q];
+            double2 acc = y[i];
+            blk_sub(acc, ringA[q], x);
+            y[i] = acc;
+        }
+        if (n > 32 && lane + 32 < n) {
+            const int q = (e + lane + 32) & RM;
+            const int i = ringI[q];
+            double2 acc = y[i];
+            blk_sub(acc, ringA[q], x);
+            y[i] = acc;
+        }
+        __syncwarp();
+        e += n;
+    };
+    // forward: x_j = y_j is final when its column comes up
+    for (int st = 0; st < nf; ++st) {
+        const unsigned w = steps[st];
+        acquire(w);
+        entries((int)((w >> 16) & 0x7fu), y[w & 0xffffu]);
+        release(w);
+    }
+    // backward: x_j = inv(D_j) y_j opens the column; it is stored one step late
+    // (the lanes of this step still read the old y_j)
+    {
+        double2 x = make_double2(0.0, 0.0), pend_x = x;
+        int pend_j = -1;
+        for (int st = nf; st < nf + nb; ++st) {
+            const unsigned w = steps[st];
+            acquire(w);
+            if (lane == 0 && pend_j >= 0) y[pend_j] = pend_x;
+            if (w >> 31) {
+                const int j = (int)(w & 0xffffu);
+                const double4 d = ringA[e & RM];
+                const double2 yj = y[j];
+                x = make_double2(d.x * yj.x + d.y * yj.y, d.z * yj.x + d.w * yj.y);
+                pend_j = j;
+                pend_x = x;
+                ++e;
+            }
+            entries((int)((w >> 16) & 0x7fu), x);
+            release(w);
+        }
+        if (lane == 0 && pend_j >= 0) y[pend_j] = pend_x;
+        __syncwarp();
+    }
+    if (VARIANT == 1) {
+        for (int l = lane; l < C.nloc; l += 32) {
+            if (!C.owned[l]) continue;
+            int gx, gy, gz;
+            local_to_global(g, C, o, l, gx, gy, gz);
+            z[cell_at(g, gx, gy, zplane(g, gz))] = y[l];
+        }
+    } else {
+        for (int l = lane; l < C.nloc; l += 32) ext_out[sub_ext_off[s] + l] = y[l];
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Class-group solver (default).  One CTA = NW warps = up to NW subdomains of
 // the SAME class: the class's symbolic data (level tables, row lists, row
 // lengths, slot column ids as uint16) is copied once into shared memory and
@@ -1285,6 +1503,8 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
     C.b_len8.assign(C.b_len.begin(), C.b_len.end());
     C.ecol.assign(C.ell_total, -1);
     for (int t = 0; t < C.nnzb; ++t) C.ecol[C.pos[t]] = C.col[t];
+    C.jmap_csr = C.jmap;
+    C.upd_csr = C.upd;
     for (auto &j : C.jmap)
         if (j >= 0) j = C.pos[j];
     for (auto &u : C.upd) {
@@ -1314,6 +1534,95 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
     for (size_t q = 0; q < C.levb_rows.size(); ++q)
         if (C.levb_rows[q] < C.b_min_row) C.skip_blocks += C.b_len[q];
     return true;
+}
+
+// Column-major slot layout for apply_cols_kernel (narrow classes): L columns
+// 0..n-1 (entries by ascending row), then U columns n-1..0, each led by the
+// column's inverted diagonal block.  Replaces the level-major layout: pos[],
+// the factorisation's slot tables and ell_total are rebuilt; the level
+// schedules stay (the factorisation still runs level by level).
+void relayout_columns(ClassHost &C)
+{
+    const int n = C.nloc;
+    std::vector<std::vector<int>> lcol(n), ucol(n);
+    for (int i = 0; i < n; ++i)
+        for (int t = C.rowptr[i]; t < C.rowptr[i + 1]; ++t) {
+            const int j = C.col[t];
+            if (j < i) lcol[j].push_back(t);
+            else if (j > i) ucol[j].push_back(t);
+        }
+    std::vector<int> row_of(C.nnzb);
+    for (int i = 0; i < n; ++i)
+        for (int t = C.rowptr[i]; t < C.rowptr[i + 1]; ++t) row_of[t] = i;
+    C.pos.assign(C.nnzb, -1);
+    C.col_steps.clear();
+    C.col_ridx.clear();
+    int slot = 0;
+    auto place = [&](int t, int i) {
+        C.pos[t] = slot++;
+        C.col_ridx.push_back((unsigned short)i);
+    };
+    // the ring bookkeeping of apply_cols_kernel is a function of the class
+    // only, so every step word carries it: how many new tiles the step must
+    // wait for, how many it hands back to the TMA engine when it is done
+    int ready = 0, freed = 0;
+    auto push_step = [&](int j, int cnt, bool first, int slot_before) {
+        const int total = cnt + (first ? 1 : 0);
+        int nwait = 0;
+        if (total > 0) {
+            const int cl = (slot_before + total - 1) / kColTile;
+            nwait = std::max(0, cl + 1 - ready);
+            ready += nwait;
+        }
+        const int cf = (slot_before + total) / kColTile;
+        const int nrel = cf - freed;
+        freed = cf;
+        C.col_steps.push_back((unsigned)j | ((unsigned)cnt << 16) | ((unsigned)nwait << 23) | ((unsigned)nrel << 25) |
+                              (first ? 0x80000000u : 0u));
+    };
+    for (int j = 0; j < n; ++j) {
+        const auto &e = lcol[j];
+        for (size_t k = 0; k < e.size(); k += kColChunk) {
+            const int cnt = (int)std::min<size_t>(kColChunk, e.size() - k);
+            push_step(j, cnt, false, slot);
+            for (int q = 0; q < cnt; ++q) place(e[k + q], row_of[e[k + q]]);
+        }
+    }
+    C.col_nf = (int)C.col_steps.size();
+    C.col_bstart = slot;
+    C.col_nb_ras = 0;
+    for (int j = n - 1; j >= 0; --j) {
+        const auto &e = ucol[j];
+        size_t k = 0;
+        do {
+            const int cnt = (int)std::min<size_t>(kColChunk, e.size() - k);
+            push_step(j, cnt, k == 0, slot);
+            if (k == 0) place(C.diag[j], j);
+            for (int q = 0; q < cnt; ++q) place(e[k + q], row_of[e[k + q]]);
+            k += cnt;
+        } while (k < e.size());
+        // left RAS stops after the first owned row's column (its entries update unowned rows only)
+        if (j >= C.b_min_row) {
+            C.col_nb_ras = (int)C.col_steps.size() - C.col_nf;
+            C.col_end_ras = slot;
+        }
+    }
+    C.col_nb = (int)C.col_steps.size() - C.col_nf;
+    C.col_end = slot;
+    // whole TMA tiles: the last tile of the stream is read to its end
+    C.ell_total = (slot + kColTile - 1) / kColTile * kColTile;
+    C.col_ridx.resize(C.ell_total, 0);
+    C.ecol.assign(C.ell_total, -1);
+    for (int t = 0; t < C.nnzb; ++t) C.ecol[C.pos[t]] = C.col[t];
+    C.jmap = C.jmap_csr;
+    C.upd = C.upd_csr;
+    for (auto &j : C.jmap)
+        if (j >= 0) j = C.pos[j];
+    for (auto &u : C.upd) {
+        u.x = C.pos[u.x];
+        u.y = C.pos[u.y];
+    }
+    C.skip_blocks = 0;
 }
 
 template <typename T>
@@ -1405,6 +1714,8 @@ acch_status upload_class(ClassHost &C)
     const size_t o_meta = add(C.meta.size());
     const size_t o_lin = add(sizeof(int) * C.lin.size());
     const size_t o_own = add(sizeof(int) * std::max<size_t>(1, C.own_list.size()));
+    const size_t o_cs = add(sizeof(unsigned) * std::max<size_t>(1, C.col_steps.size()));
+    const size_t o_cr = add(2 * std::max<size_t>(1, C.col_ridx.size()));
     ACCH_CUDA(cudaMalloc(&C.dev_mem, total));
     std::vector<unsigned char> h(total, 0);
     auto put = [&](size_t o, const void *src, size_t bytes) { if (bytes) memcpy(h.data() + o, src, bytes); };
@@ -1437,6 +1748,8 @@ acch_status upload_class(ClassHost &C)
     put(o_meta, C.meta.data(), C.meta.size());
     put(o_lin, C.lin.data(), sizeof(int) * C.lin.size());
     put(o_own, C.own_list.data(), sizeof(int) * C.own_list.size());
+    put(o_cs, C.col_steps.data(), sizeof(unsigned) * C.col_steps.size());
+    put(o_cr, C.col_ridx.data(), 2 * C.col_ridx.size());
     ACCH_CUDA(cudaMemcpy(C.dev_mem, h.data(), total, cudaMemcpyHostToDevice));
     unsigned char *b = (unsigned char *)C.dev_mem;
     ClassDev &d = C.dev;
@@ -1480,6 +1793,14 @@ acch_status upload_class(ClassHost &C)
     d.b_min_row = C.b_min_row;
     d.nlevb_ras = C.nlevb_ras;
     d.jdup = C.jdup;
+    d.col_steps = (const unsigned *)(b + o_cs);
+    d.col_ridx = (const unsigned short *)(b + o_cr);
+    d.col_nf = C.col_nf;
+    d.col_nb = C.col_nb;
+    d.col_nb_ras = C.col_nb_ras;
+    d.col_bstart = C.col_bstart;
+    d.col_end = C.col_end;
+    d.col_end_ras = C.col_end_ras;
     d.meta_bytes = (int)C.meta.size();
     d.m_fbs = C.m_off[1];
     d.m_bptr = C.m_off[2];
@@ -1531,6 +1852,8 @@ struct acch_precond {
     int tps = 32;          // threads per subdomain in the solves
     int max_nloc = 0;
     int warp_mode = 0;     // apply_warp_kernel usable
+    int col_mode = 0;      // apply_cols_kernel: narrow classes (every level <= kWideRows rows, long rows), column-major factors
+    ColSmem cl{0, 0};
     // class-group solver (apply_group_kernel): groups of <= group_nw subdomains of one class
     int group_mode = 0, group_nw = 8, group_per_warp = 1, meta_max = 0, y_stride = 0;
     int factor_threads = 0;   // threads per subdomain CTA of factor_kernel (32 / 64 / 128)
@@ -1668,9 +1991,35 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         }
         pc->sub_origin.push_back(make_int4(lo3[0], lo3[1], lo3[2], nowrap));
     }
+    int max_width = 0, max_nloc = 0, max_len = 0;
+    for (const auto &C : pc->classes) {
+        max_width = std::max(max_width, std::max(C.max_fwidth, C.max_bwidth));
+        max_nloc = std::max(max_nloc, C.nloc);
+        for (int v : C.f_len) max_len = std::max(max_len, v);
+        for (int v : C.b_len) max_len = std::max(max_len, v - 1);
+    }
+    // Narrow classes (every level <= kWideRows rows) with long rows -- exact
+    // LU, ILU(k >= 1) -- are solved by column sweeps on column-major factors
+    // (apply_cols_kernel); ACCH_NARROW=0 keeps the level-major solvers.
+    pc->col_mode = max_width <= kWideRows && max_len > kWideLen && max_nloc <= 65535;
+    if (const char *e = getenv("ACCH_NARROW")) pc->col_mode = pc->col_mode && atoi(e) != 0;
+    if (const char *e = getenv("ACCH_WIDE_ROWS")) pc->col_mode = pc->col_mode && atoi(e) != 0;
+    if (pc->col_mode) {
+        int max_steps = 0;
+        for (auto &C : pc->classes) {
+            relayout_columns(C);
+            max_steps = std::max(max_steps, C.col_nf + C.col_nb);
+        }
+        pc->cl = ColSmem{max_nloc, max_steps};
+        if (pc->cl.bytes() > 200 * 1024) {
+            free_precond(pc);
+            delete pc;
+            acch_set_error("acch_precond_create: subdomain too large for the column solver (set ACCH_NARROW=0)");
+            return ACCH_ERR_INVALID_ARG;
+        }
+    }
     // offsets
     long long vo = 0, eo = 0;
-    int max_nloc = 0;
     pc->sub_off.assign(n_sub, 0);
     for (long long s = 0; s < n_sub; ++s) {
         const ClassHost &C = pc->classes[pc->sub_class[s]];
@@ -1680,10 +2029,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         eo += C.nloc;
         pc->total_nnzb += C.nnzb;
         pc->total_skip += C.skip_blocks;
-        max_nloc = std::max(max_nloc, C.nloc);
     }
-    int max_width = 0;
-    for (const auto &C : pc->classes) max_width = std::max(max_width, std::max(C.max_fwidth, C.max_bwidth));
     pc->total_blocks = vo;
     pc->total_ext = eo;
     pc->max_nloc = max_nloc;
@@ -1695,11 +2041,6 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             mnb = std::max(mnb, (int)C.levb_ptr.size() - 1);
         }
         pc->wl = WarpSmem{max_nloc, mnl, mnb};
-        int max_len = 0;
-        for (const auto &C : pc->classes) {
-            for (int v : C.f_len) max_len = std::max(max_len, v);
-            for (int v : C.b_len) max_len = std::max(max_len, v - 1);
-        }
         pc->wide = max_len > kWideLen;   // exact LU / high fill: warp-wide sweeps of narrow levels
         if (const char *e = getenv("ACCH_WIDE_ROWS")) pc->wide = pc->wide && atoi(e) != 0;
         pc->warp_mode = (max_width <= 64 && max_nloc <= 65535 && pc->wl.bytes() <= 200 * 1024) ? 1 : 0;
@@ -1710,7 +2051,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             fprintf(stderr, "[acch] precond: %lld subdomains, %zu classes, max_nloc %d, max level width %d, "
                             "max row %d, warp smem %zu B -> %s solver\n",
                     (long long)n_sub, pc->classes.size(), max_nloc, max_width, max_len, pc->wl.bytes(),
-                    pc->warp_mode ? "warp" : "CTA");
+                    pc->col_mode ? "column-sweep" : (pc->warp_mode ? "warp" : "CTA"));
     }
     const int groups = 128 / pc->tps;
     pc->apply_smem = sizeof(double2) * (size_t)max_nloc * groups;
@@ -1796,6 +2137,9 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
     {
         // the solvers live on shared memory: ask for the full L1/shared carveout
         const auto co = cudaFuncAttributePreferredSharedMemoryCarveout;
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<0>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<1>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<2>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 4>, co, 100));
@@ -1820,6 +2164,13 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<0, 128>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<1, 128>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_kernel<2, 128>, co, 100));
+    }
+    if (pc->col_mode) {
+        const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        const int b = smem_optin();
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<0>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<1>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<2>, attr, b));
     }
     if (pc->warp_mode && pc->wl.bytes() > 48 * 1024) {
         const int b = smem_optin();   // per-function state: never lower it under another live preconditioner
@@ -1851,7 +2202,7 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
         for (const auto &C : pc->classes) meta_max = std::max(meta_max, (int)C.meta.size());
         pc->meta_max = (meta_max + 15) / 16 * 16;
         pc->y_stride = (int)((sizeof(double2) * (size_t)max_nloc + 15) / 16 * 16);
-        int enable = pc->warp_mode;
+        int enable = pc->warp_mode && !pc->col_mode;   // column-major factors: apply_cols_kernel only
         if (const char *e = getenv("ACCH_GROUP")) enable = enable && atoi(e) != 0;
         int nw = 8;
         if (const char *e = getenv("ACCH_GROUP_WARPS")) nw = atoi(e) <= 4 ? 4 : 8;
@@ -2058,7 +2409,15 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     } while (0)
     // class-group solver (default), else one warp per subdomain (class image
     // too large for a group), else one CTA-wide solver per subdomain
-    if (pc->group_mode) {
+#define NAPPLY(V)                                                                                             \
+    apply_cols_kernel<V><<<(unsigned)pc->nsub, 32, pc->cl.bytes(), ctx->stream>>>(                                \
+        ctx->g, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals,   \
+        (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->cl, pc->nsub)
+    if (pc->col_mode) {
+        if (pc->variant == 1) NAPPLY(1);
+        else if (pc->variant == 0) NAPPLY(0);
+        else NAPPLY(2);
+    } else if (pc->group_mode) {
         if (pc->variant == 1) GAPPLY(1);
         else if (pc->variant == 0) GAPPLY(0);
         else GAPPLY(2);
@@ -2075,6 +2434,7 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         else if (pc->variant == 0) APPLY(0, 128);
         else APPLY(2, 128);
     }
+#undef NAPPLY
 #undef APPLY
 #undef WAPPLY
 #undef WAPPLY_D
