@@ -809,9 +809,14 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
 }
 
 struct ColSmem {
-    int max_nloc, max_steps;
-    __host__ __device__ size_t y_bytes() const { return (sizeof(double2) * (size_t)max_nloc + 127) / 128 * 128; }
-    __host__ __device__ size_t steps_bytes() const { return (sizeof(unsigned) * (size_t)max_steps + 127) / 128 * 128; }
+    int max_nloc, max_steps, steps_smem;
+    // y: one scratch row past the box; steps: one spare word past the last step
+    __host__ __device__ size_t y_bytes() const { return (sizeof(double2) * (size_t)(max_nloc + 1) + 127) / 128 * 128; }
+    // steps_smem: the step table staged in shared memory (when that costs no resident CTA), else read from global
+    __host__ __device__ size_t steps_bytes() const
+    {
+        return steps_smem ? (sizeof(unsigned) * (size_t)(max_steps + 1) + 127) / 128 * 128 : 0;
+    }
     __host__ __device__ size_t bytes() const
     {
         return y_bytes() + steps_bytes() + (size_t)kColRing * kColTile * (sizeof(double4) + sizeof(unsigned short)) +
@@ -819,7 +824,7 @@ struct ColSmem {
     }
 };
 
-template <int VARIANT>
+template <int VARIANT, bool SSTEPS>
 __global__ void __launch_bounds__(32, 8)
 apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__restrict__ sub_class,
                   const int4 *__restrict__ sub_origin, const long long *__restrict__ sub_off,
@@ -836,7 +841,9 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     const int4 o = sub_origin[s];
     const double4 *__restrict__ A = vals + sub_off[s];
     double2 *y = reinterpret_cast<double2 *>(smem_raw);
-    unsigned *steps = reinterpret_cast<unsigned *>(smem_raw + L.y_bytes());
+    // (two spare words past the last step: the sweep reads one step ahead)
+    unsigned *ssteps = reinterpret_cast<unsigned *>(smem_raw + L.y_bytes());
+    const unsigned *steps = SSTEPS ? ssteps : C.col_steps;
     double4 *ringA = reinterpret_cast<double4 *>(smem_raw + L.y_bytes() + L.steps_bytes());
     unsigned short *ringI = reinterpret_cast<unsigned short *>(ringA + kColRing * kColTile);
     uint64_t *bars = reinterpret_cast<uint64_t *>(ringI + kColRing * kColTile);
@@ -867,7 +874,8 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     };
 #pragma unroll
     for (int c = 0; c < kColRing; ++c) issue(c);
-    for (int i = lane; i < nf + nb; i += 32) steps[i] = C.col_steps[i];
+    if (SSTEPS)
+        for (int i = lane; i <= nf + nb; i += 32) ssteps[i] = i < nf + nb ? C.col_steps[i] : 0u;
     for (int l = lane; l < C.nloc; l += 32) {
         int gx, gy, gz;
         local_to_global(g, C, o, l, gx, gy, gz);
@@ -895,17 +903,21 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
             ++freed;
         }
     };
+    // A lane without an entry in this step works on the scratch row y[nloc]
+    // (no divergent branch in the chain; whatever the ring holds at its
+    // slot is subtracted from a row nobody reads).
+    const int scratch = C.nloc;
     auto entries = [&](int n, const double2 x) {
-        if (lane < n) {
+        {
             const int q = (e + lane) & RM;
-            const int i = ringI[q];
+            const int i = lane < n ? (int)ringI[q] : scratch;
             double2 acc = y[i];
             blk_sub(acc, ringA[q], x);
             y[i] = acc;
         }
-        if (n > 32 && lane + 32 < n) {
+        if (n > 32) {   // warp-uniform
             const int q = (e + lane + 32) & RM;
-            const int i = ringI[q];
+            const int i = lane + 32 < n ? (int)ringI[q] : scratch;
             double2 acc = y[i];
             blk_sub(acc, ringA[q], x);
             y[i] = acc;
@@ -913,9 +925,12 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
         __syncwarp();
         e += n;
     };
-    // forward: x_j = y_j is final when its column comes up
+    // forward: x_j = y_j is final when its column comes up; the next step's
+    // word is read a step ahead (it does not depend on the sweep)
+    unsigned wn = nf + nb > 0 ? steps[0] : 0u;
     for (int st = 0; st < nf; ++st) {
-        const unsigned w = steps[st];
+        const unsigned w = wn;
+        wn = steps[st + 1];   // the table has one spare word past the last step
         acquire(w);
         entries((int)((w >> 16) & 0x7fu), y[w & 0xffffu]);
         release(w);
@@ -924,11 +939,12 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     // (the lanes of this step still read the old y_j)
     {
         double2 x = make_double2(0.0, 0.0), pend_x = x;
-        int pend_j = -1;
+        int pend_j = scratch;
         for (int st = nf; st < nf + nb; ++st) {
-            const unsigned w = steps[st];
+            const unsigned w = wn;
+            wn = steps[st + 1];
             acquire(w);
-            if (lane == 0 && pend_j >= 0) y[pend_j] = pend_x;
+            if (lane == 0) y[pend_j] = pend_x;
             if (w >> 31) {
                 const int j = (int)(w & 0xffffu);
                 const double4 d = ringA[e & RM];
@@ -941,7 +957,7 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
             entries((int)((w >> 16) & 0x7fu), x);
             release(w);
         }
-        if (lane == 0 && pend_j >= 0) y[pend_j] = pend_x;
+        if (lane == 0) y[pend_j] = pend_x;
         __syncwarp();
     }
     if (VARIANT == 1) {
@@ -1609,6 +1625,8 @@ void relayout_columns(ClassHost &C)
     }
     C.col_nb = (int)C.col_steps.size() - C.col_nf;
     C.col_end = slot;
+    C.col_steps.push_back(0u);   // spare words: the sweep reads one step ahead
+    C.col_steps.push_back(0u);
     // whole TMA tiles: the last tile of the stream is read to its end
     C.ell_total = (slot + kColTile - 1) / kColTile * kColTile;
     C.col_ridx.resize(C.ell_total, 0);
@@ -1853,7 +1871,7 @@ struct acch_precond {
     int max_nloc = 0;
     int warp_mode = 0;     // apply_warp_kernel usable
     int col_mode = 0;      // apply_cols_kernel: narrow classes (every level <= kWideRows rows, long rows), column-major factors
-    ColSmem cl{0, 0};
+    ColSmem cl{0, 0, 0};
     // class-group solver (apply_group_kernel): groups of <= group_nw subdomains of one class
     int group_mode = 0, group_nw = 8, group_per_warp = 1, meta_max = 0, y_stride = 0;
     int factor_threads = 0;   // threads per subdomain CTA of factor_kernel (32 / 64 / 128)
@@ -2010,7 +2028,14 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
             relayout_columns(C);
             max_steps = std::max(max_steps, C.col_nf + C.col_nb);
         }
-        pc->cl = ColSmem{max_nloc, max_steps};
+        // the step table goes to shared memory when every subdomain is resident anyway
+        pc->cl = ColSmem{max_nloc, max_steps, 1};
+        {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+            const long long fit = (long long)sms * std::min<long long>(8, (227 * 1024) / (long long)(pc->cl.bytes() + 1024));
+            if (n_sub > fit) pc->cl.steps_smem = 0;
+        }
         if (pc->cl.bytes() > 200 * 1024) {
             free_precond(pc);
             delete pc;
@@ -2137,9 +2162,12 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
     {
         // the solvers live on shared memory: ask for the full L1/shared carveout
         const auto co = cudaFuncAttributePreferredSharedMemoryCarveout;
-        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<0>, co, 100));
-        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<1>, co, 100));
-        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<2>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<0, true>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<1, true>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<2, true>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<0, false>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<1, false>, co, 100));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<2, false>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<0, 12, 4, true>, co, 100));
         PC_CUDA(cudaFuncSetAttribute(apply_warp_kernel<1, 12, 4>, co, 100));
@@ -2168,9 +2196,12 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
     if (pc->col_mode) {
         const cudaFuncAttribute attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
         const int b = smem_optin();
-        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<0>, attr, b));
-        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<1>, attr, b));
-        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<2>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<0, true>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<1, true>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<2, true>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<0, false>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<1, false>, attr, b));
+        PC_CUDA(cudaFuncSetAttribute(apply_cols_kernel<2, false>, attr, b));
     }
     if (pc->warp_mode && pc->wl.bytes() > 48 * 1024) {
         const int b = smem_optin();   // per-function state: never lower it under another live preconditioner
@@ -2409,10 +2440,15 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
     } while (0)
     // class-group solver (default), else one warp per subdomain (class image
     // too large for a group), else one CTA-wide solver per subdomain
-#define NAPPLY(V)                                                                                             \
-    apply_cols_kernel<V><<<(unsigned)pc->nsub, 32, pc->cl.bytes(), ctx->stream>>>(                                \
+#define NAPPLY_S(V, S)                                                                                        \
+    apply_cols_kernel<V, S><<<(unsigned)pc->nsub, 32, pc->cl.bytes(), ctx->stream>>>(                             \
         ctx->g, pc->d_classes, pc->d_sub_class, pc->d_sub_origin, pc->d_sub_off, pc->d_sub_ext_off, pc->d_vals,   \
         (const double2 *)r, (double2 *)z, pc->d_ext_out, pc->cl, pc->nsub)
+#define NAPPLY(V)                                \
+    do {                                         \
+        if (pc->cl.steps_smem) NAPPLY_S(V, true); \
+        else NAPPLY_S(V, false);                 \
+    } while (0)
     if (pc->col_mode) {
         if (pc->variant == 1) NAPPLY(1);
         else if (pc->variant == 0) NAPPLY(0);
@@ -2435,6 +2471,7 @@ acch_status precond_apply_impl(acch_precond *pc, const double *r, double *z)
         else APPLY(2, 128);
     }
 #undef NAPPLY
+#undef NAPPLY_S
 #undef APPLY
 #undef WAPPLY
 #undef WAPPLY_D
