@@ -155,6 +155,20 @@ def make_config(args, world=1, rank=0):
     return cfg, nsub
 
 
+def workload_config(args, world=None):
+    """The workload both arms are quoted on (identical dict in both JSON lines)."""
+    world = args.gpus if world is None else world
+    nsub = (args.n // args.box) ** args.dim
+    vec_mb = 16 * args.n ** args.dim / 1e6
+    return {"workload": workload_name(args), "grid": [args.n] * args.dim, "bc": "periodic",
+            "ic": "u0=0.5+0.01U(-1,1), v0=0.01U(-1,1), seed 1234", "subdomains": nsub,
+            "parallelism": "1 GPU" if world == 1 else
+            f"z-slabs over {world} GPUs (2 ghost planes; in-library NCCL halos + allreduces)",
+            "l2": f"every vector {vec_mb:.0f} MB vs 126 MB L2" + (" (no flush needed)" if vec_mb > 126 else ""),
+            "steps_timed": f"accepted steps {args.warmup + 1}..{args.warmup + args.steps} "
+                           f"(after {args.warmup} warm-up steps)"}
+
+
 def workload_name(args):
     return (f"AC/CH {args.dim}D {args.n}^{args.dim} periodic fp64, adaptive dt (eta=1e2), NKS: Newton + "
             f"GMRES({args.restart}) + {args.variant} {args.box}^{args.dim}-cell boxes overlap {args.overlap} {args.solver}")
@@ -386,10 +400,8 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": "time steps/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": True, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args), "grid": [args.n] * args.dim, "bc": "periodic",
-                       "ic": "u0=0.5+0.01U(-1,1), v0=0.01U(-1,1), seed 1234",
-                       "parallelism": f"host CPU, {threads} threads (the reference's WorkerPool)",
-                       "counts_window": key},
+            "config": workload_config(args),
+            "arm": {"runs_on": f"host CPU, {threads} threads (the reference's WorkerPool)", "counts_window": key},
             "cpu_baseline": {"value": value, "unit": "time steps/s", "cores": threads, "kind": sample["kind"],
                              "sample": sample["sample"], "parts_s": sample.get("parts_s")},
             "reference_microbench": micro,
@@ -653,12 +665,7 @@ def run_ours(args):
             "value": value, "unit": "time steps/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed * 1e3 / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_name(args), "grid": [args.n] * args.dim, "bc": "periodic",
-                       "ic": "u0=0.5+0.01U(-1,1), v0=0.01U(-1,1), seed 1234", "subdomains": nsub,
-                       "parallelism": "1 GPU" if world == 1 else
-                       f"z-slabs over {world} GPUs (2 ghost planes; in-library NCCL halos + allreduces)",
-                       "l2": "every vector 268 MB > 126 MB L2 (no flush needed)",
-                       "steps_timed": f"accepted steps {first_timed}..{first_timed + args.steps - 1} (after {args.warmup} warm-up steps)"},
+            "config": workload_config(args, world),
             "solver_stats": {"newton": newton_total, "gmres": gmres_total, "retries": retries,
                              "dt": [round(x, 6) for x in dts], "per_step": counts, "counts_check": counts_check,
                              "ms_per_gmres_iteration": elapsed * 1e3 / max(gmres_total, 1)},
