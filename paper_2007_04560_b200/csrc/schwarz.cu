@@ -868,9 +868,7 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
         bulk_g2s(ringA + k * kColTile, A + (size_t)c * kColTile, kColTile * (unsigned)sizeof(double4), bars + k);
         bulk_g2s(ringI + k * kColTile, C.col_ridx + (size_t)c * kColTile, kColTile * (unsigned)sizeof(unsigned short),
                  bars + k);
-        // and pull the stream into L2 further ahead
-        if (c + 2 * kColRing < ntiles)
-            prefetch_l2(A + (size_t)(c + 2 * kColRing) * kColTile, kColTile * (unsigned)sizeof(double4));
+        // (a bulk L2 prefetch further ahead measured no gain at 4 tiles and a loss at 8-12)
     };
 #pragma unroll
     for (int c = 0; c < kColRing; ++c) issue(c);
