@@ -328,9 +328,38 @@ def reference_microbench(args, threads):
             out["matvec_assembly_s"] = t_asm
         out[name] = {"grid": [n] * args.dim, "s": t, "gdof_s": 2 * g.n_cells / t / 1e9}
         del prob, new, old
+    out["config1"] = reference_config1(threads)
     out["threads"] = threads
     out["kind"] = "reference"
     return out
+
+
+def reference_config1(threads):
+    """BASELINE configs[0] (64^2 periodic, 10 fixed steps
+    of 1e-4, left-RAS 2x2, overlap 1, ILU(0)) run in full through the
+    unmodified reference's `simulate` (cli/drivers.py:76-184) at 1 and T host
+    threads, after one warm-up run (numba compilation)."""
+    try:
+        from acch.cli.config import InitialSpec as RI, RunConfig as RC, SolverSpec as RS, TimeSpec as RT
+        from acch.cli.drivers import simulate as rsim
+        from acch.grid import BoundaryCondition as RBC, Grid as RGrid
+        from acch.linalg import SchwarzVariant as RV, SubdomainSolverSpec as RSub
+        from acch.physics import Params as RParams
+        cfg = RC(RGrid((64, 64), (1.0, 1.0), RBC.PERIODIC), RParams(4.0, 2.0, 0.005, 0.1, 0.001),
+                 RI("random_uniform", 0.5, 0.05, 1234), RT(horizon=1e-3, mode="fixed", dt=1e-4),
+                 RS(RV.LEFT_RAS, 1, RSub("ilu", 0), subdomains=4))
+        rsim(cfg, threads=1, max_steps=2)
+        out = {}
+        for th in sorted({1, min(threads, 4)}):
+            t0 = time.perf_counter()
+            res = rsim(cfg, threads=th, max_steps=10)
+            t = time.perf_counter() - t0
+            rows = res.history
+            out[f"threads_{th}"] = {"steps": len(rows) - 1, "s": t, "steps_s": (len(rows) - 1) / t,
+                                    "energy_last": rows[-1].energy}
+        return out
+    except Exception as e:      # reported, never fatal for the arm
+        return {"error": f"{type(e).__name__}: {e}"}
 
 
 def cpu_sample(args, threads=1, counts=None, ns=None):
