@@ -770,14 +770,11 @@ apply_warp_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
 // order (_ilu.py:123-137).
 // ---------------------------------------------------------------------------
 constexpr int kColChunk = 64;   // entries per step (two per lane)
-#ifndef ACCH_COL_TILE
-#define ACCH_COL_TILE 256
-#endif
-#ifndef ACCH_COL_RING
-#define ACCH_COL_RING 2
-#endif
-constexpr int kColTile = ACCH_COL_TILE;    // factor slots per TMA tile (4 KB of blocks + 256 B of row ids)
-constexpr int kColRing = ACCH_COL_RING;     // tiles in the shared-memory ring
+// 2 tiles of 256 slots (8 KB of blocks + 512 B of row ids each) measured best
+// against 8 x 64, 4 x 128, 4 x 256 and 2 x 512: the ring competes with
+// resident CTAs for shared memory (profiles/r02/wide_sweep_variants.txt)
+constexpr int kColTile = 256;   // factor slots per TMA tile
+constexpr int kColRing = 2;     // tiles in the shared-memory ring
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(uint64_t *bar, unsigned count)
@@ -861,9 +858,8 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
     auto issue = [&](int c) {
         if (c >= ntiles || lane != 0) return;
         const int k = c % kColRing;
-#ifdef ACCH_COL_FENCE
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-#endif
+        // (the ring slot was last READ through the generic proxy, before the
+        // step's __syncwarp: write-after-read needs no proxy fence)
         mbar_expect_tx(bars + k, kColTile * (unsigned)(sizeof(double4) + sizeof(unsigned short)));
         bulk_g2s(ringA + k * kColTile, A + (size_t)c * kColTile, kColTile * (unsigned)sizeof(double4), bars + k);
         bulk_g2s(ringI + k * kColTile, C.col_ridx + (size_t)c * kColTile, kColTile * (unsigned)sizeof(unsigned short),
