@@ -163,17 +163,23 @@ __device__ __forceinline__ double cell_gap_fast(double u, double v)
 // 1/x for 0 < x <= 1/4 (x = z (1 - z) of an admissible chord pair): the
 // hardware reciprocal seed and three Newton steps, no special-case branch
 // (the argument is never 0, denormal, inf or NaN on the path that uses it)
+// STEPS = 2 leaves a relative error below 2^-36 even from a 9-bit seed: enough
+// where the ratio enters only through t = (sigma/z)^2 <= 6.3e-5 (the short
+// series: the term it scales is below 1.1e-5 of the chord)
+template <int STEPS = 3>
 __device__ __forceinline__ double rcp_quarter(double x)
 {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
-    double e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-    e = fma(-x, y, 1.0);
-    y = fma(y, e, y);
-    e = fma(-x, y, 1.0);
-    return fma(y, e, y);
+#pragma unroll
+    for (int k = 0; k < STEPS; ++k) {
+        const double e = fma(-x, y, 1.0);
+        y = fma(y, e, y);
+    }
+    return y;
 }
+// one more Newton step on a reciprocal
+__device__ __forceinline__ double rcp_refine(double x, double y) { return fma(y, fma(-x, y, 1.0), y); }
 
 template <int ORDER>
 __device__ __forceinline__ double chord_res(double a, double b, const ParamsDev &P)
@@ -193,14 +199,24 @@ __device__ __forceinline__ double chord_res(double a, double b, const ParamsDev 
     const bool near = !exact && as <= 0.4 * zeta && as <= 0.4 * w;   // 0.4 min(zeta, 1 - zeta)
     double val = lg;
     if (__any_sync(0xffffffffu, near)) {
-        const double r = rcp_quarter(zeta * w);         // 1/zeta = w r, 1/w = zeta r
-        const double rz = sigma * (w * r), rw = sigma * (zeta * r);
-        const double tz = rz * rz, tw = rw * rw;
+        const double zw = zeta * w;
+        double r = rcp_quarter<2>(zw);                  // 1/zeta = w r, 1/w = zeta r
+        double rz = sigma * (w * r), rw = sigma * (zeta * r);
+        double tz = rz * rz, tw = rw * rw;
         double pz, pw;
         // Newton iterates sit close to U^n: t = (sigma/z)^2 is tiny and 4
-        // terms leave a tail below 2^-60 of the sum (t <= 6.3e-5)
-        if (!__any_sync(0xffffffffu, near && (tz > 6.3e-5 || tw > 6.3e-5))) chord_poly2<4>(tz, tw, P, pz, pw);
-        else chord_poly2<ORDER>(tz, tw, P, pz, pw);
+        // terms leave a tail below 2^-60 of the sum (t <= 6.3e-5); otherwise
+        // the reciprocal gets its last Newton step and all S terms are summed
+        if (!__any_sync(0xffffffffu, near && (tz > 6.3e-5 || tw > 6.3e-5))) {
+            chord_poly2<4>(tz, tw, P, pz, pw);
+        } else {
+            r = rcp_refine(zw, r);
+            rz = sigma * (w * r);
+            rw = sigma * (zeta * r);
+            tz = rz * rz;
+            tw = rw * rw;
+            chord_poly2<ORDER>(tz, tw, P, pz, pw);
+        }
         if (near) val = lg - pz * tz + pw * tw;
     }
     if (!exact && !near) val = (entropy(a) - entropy(b)) / (a - b);   // direct quotient (physics.py:259-261)
@@ -413,7 +429,7 @@ res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__re
     const double ihx = g.ih2[0], ihy = g.ih2[1], ihz = g.ih2[2];
     const double c2lap = 2.0 * (ihx + ihy + ihz);
     const double ha = -0.5 * P.alpha, hb = -0.5 * P.beta, hg = 0.5 * P.gamma;
-    const double idt = 1.0 / dt, irho = 1.0 / P.rho;
+    const double idt = 1.0 / dt, irho2 = 2.0 * (1.0 / P.rho);
 
     int woff[NWR];
 #pragma unroll
@@ -501,8 +517,11 @@ res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__re
                     psi = chord_fast<0>(n0.x - n0.y, o0.x - o0.y, P);
                 }
                 const double Gu = ha * (n0.x + o0.x - 1.0) + P.theta * (phi + psi) - hg * lu;
-                const double cb = 0.5 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
-                sB[sb * NB + gc[j]] = make_double2(Gu, cb);
+                // half the averaged mobility: the face value (c(a) + c(b)) / 2 is then one
+                // addition, and the v row scales by 2 / rho (exact power-of-two shifts:
+                // bitwise the same fluxes)
+                const double cbh = 0.25 * (mobility(o0.x, o0.y) + mobility(n0.x, n0.y));
+                sB[sb * NB + gc[j]] = make_double2(Gu, cbh);
                 nz[j] = n0;
                 oz[j] = o0;
                 if (j == 0) {
@@ -558,29 +577,29 @@ res_zm_kernel(const GridDev g, const ParamsDev P, double dt, const double2 *__re
             const double2 *B = sB + sb1 * NB;
             const int c0 = gc[0];
             const double2 b0 = B[c0];
-            const double G0 = b0.x, C0 = b0.y;
+            const double G0 = b0.x, C0 = b0.y;   // C0 = cbar / 2
             double div = 0.0;
             {
                 const double2 bp = B[c0 + 1], bm = B[c0 - 1];
-                const double fp = fxh ? 0.5 * (C0 + bp.y) * (bp.x - G0) : 0.0;
-                const double fm = fxl ? 0.5 * (C0 + bm.y) * (G0 - bm.x) : 0.0;
+                const double fp = fxh ? (C0 + bp.y) * (bp.x - G0) : 0.0;
+                const double fm = fxl ? (C0 + bm.y) * (G0 - bm.x) : 0.0;
                 div += (fp - fm) * ihx;
             }
             {
                 const double2 bp = B[c0 + GX], bm = B[c0 - GX];
-                const double fp = fyh ? 0.5 * (C0 + bp.y) * (bp.x - G0) : 0.0;
-                const double fm = fyl ? 0.5 * (C0 + bm.y) * (G0 - bm.x) : 0.0;
+                const double fp = fyh ? (C0 + bp.y) * (bp.x - G0) : 0.0;
+                const double fm = fyl ? (C0 + bm.y) * (G0 - bm.x) : 0.0;
                 div += (fp - fm) * ihy;
             }
             {
                 const double2 bp = sB[sb2 * NB + c0], bm = sB[sb0 * NB + c0];
-                const double fp = (PER || zstep_ok(g, k, +1)) ? 0.5 * (C0 + bp.y) * (bp.x - G0) : 0.0;
-                const double fm = (PER || zstep_ok(g, k, -1)) ? 0.5 * (C0 + bm.y) * (G0 - bm.x) : 0.0;
+                const double fp = (PER || zstep_ok(g, k, +1)) ? (C0 + bp.y) * (bp.x - G0) : 0.0;
+                const double fm = (PER || zstep_ok(g, k, -1)) ? (C0 + bm.y) * (G0 - bm.x) : 0.0;
                 div += (fp - fm) * ihz;
             }
             double2 f;
             f.x = (nk.x - ok_.x) * idt - div;
-            f.y = (nk.y - ok_.y) * idt + (C0 * irho) * gvk;
+            f.y = (nk.y - ok_.y) * idt + (C0 * irho2) * gvk;
             F[poff(z0) + coff[0]] = f;
             acc_norm += f.x * f.x + f.y * f.y;
             acc_gap = red_combine(acc_gap, cell_gap_fast(nk.x, nk.y), RED_MIN);
