@@ -1,7 +1,9 @@
 """BASELINE.md section 3, configs 2 and 3 on the GPU box's HOST: the first K
 accepted steps of the unmodified reference (baseline/_ref) with the pinned
 solver settings both sides use -- config 2: 512^2 periodic, 16x16-cell boxes,
-exact LU; config 3: 128^3 Neumann, 8^3-cell boxes, ILU(2) -- reported as
+exact LU; config 3: 128^3 Neumann, 8^3-cell boxes, ILU(2); "4": the bench
+workload (config 4's solver: periodic, 8^3-cell boxes, ILU(0)) at 128^3, the
+largest size the reference fits in host memory -- reported as
 s/step next to the GPU path's own first K steps of the same run.
 
     python tools/ref_configs.py [--configs 2] [--steps 3] [--threads T] [--gpu]
@@ -31,6 +33,12 @@ def reference_run(cfg_id, steps, threads):
         cfg = RunConfig(Grid((512, 512), (1.0, 1.0), BoundaryCondition.PERIODIC), P,
                         InitialSpec("random_uniform", 0.4, 0.02, 1234), TimeSpec(horizon=1e9),
                         SolverSpec(SchwarzVariant.LEFT_RAS, 1, SubdomainSolverSpec("lu"), subdomains=1024))
+    elif cfg_id == 4:
+        # the bench workload (BASELINE config 4's solver) at 128^3 -- 256^3 needs ~160 GB in the reference
+        cfg = RunConfig(Grid((128, 128, 128), (1.0, 1.0, 1.0), BoundaryCondition.PERIODIC), P,
+                        InitialSpec("random_uniform", 0.5, 0.01, 1234), TimeSpec(horizon=1e9),
+                        SolverSpec(SchwarzVariant.LEFT_RAS, 1, SubdomainSolverSpec("ilu", 0), subdomains=4096,
+                                   gmres_restart=30))
     else:
         cfg = RunConfig(Grid((128, 128, 128), (1.0, 1.0, 1.0), BoundaryCondition.NEUMANN), P,
                         InitialSpec("random_uniform", 0.5, 0.01, 1234), TimeSpec(horizon=1e9),
@@ -51,7 +59,17 @@ def gpu_run(cfg_id, steps):
     from run_configs import configs
     from paper_2007_04560_b200.drivers import Stepper, build_initial_state
     from paper_2007_04560_b200.physics import diagnostics
-    _, cfg, _ = configs()[cfg_id]
+    if cfg_id == 4:
+        from paper_2007_04560_b200.drivers import InitialSpec, RunConfig, SolverSpec, TimeSpec
+        from paper_2007_04560_b200.grid import Grid
+        from paper_2007_04560_b200.linalg import SchwarzVariant, SubdomainSolverSpec
+        from paper_2007_04560_b200.physics import DEFAULT_PARAMS
+        cfg = RunConfig(Grid((128, 128, 128), (1.0, 1.0, 1.0), "periodic"), DEFAULT_PARAMS,
+                        InitialSpec("random_uniform", 0.5, 0.01, 1234), TimeSpec(horizon=1e9),
+                        SolverSpec(SchwarzVariant.LEFT_RAS, 1, SubdomainSolverSpec("ilu", 0), subdomains=4096,
+                                   gmres_restart=30))
+    else:
+        _, cfg, _ = configs()[cfg_id]
     dev = torch.device("cuda", 0)
     st = Stepper(cfg, build_initial_state(cfg, dev))
     out = {"dt": [], "newton": [], "gmres": [], "energy": []}
