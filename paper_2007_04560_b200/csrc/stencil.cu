@@ -128,6 +128,9 @@ __constant__ double c_atanh[12] = {1.0,        1.0 / 3.0,  1.0 / 5.0,  1.0 / 7.0
 template <int K>
 __device__ __forceinline__ double atanh_tail(double x)
 {
+    // (Estrin's scheme -- depth 5 instead of 10 at 3 extra multiplications --
+    // measured slower, 0.528 against 0.492 ms: the kernel is bound by FP64 /
+    // issue throughput, not by the length of this chain)
     double q = c_atanh[K - 1];
 #pragma unroll
     for (int k = K - 2; k >= 1; --k) q = fma(q, x, c_atanh[k]);
