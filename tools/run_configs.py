@@ -1,4 +1,4 @@
-"""Run BASELINE.json configs 1-3 through the public driver API on one B200 and
+"""Run BASELINE.json configs 1-4 through the public driver API on one B200 and
 record the per-step trace the reference's `simulate` writes (step, t, dt,
 energy, mass, max|v|, Newton, GMRES; drivers.py:62-73, drivers.py:118-167),
 then check the two acceptance properties the paper and SPEC name: the
@@ -46,6 +46,10 @@ def configs():
             RunConfig(Grid((128, 128, 128), (1.0, 1.0, 1.0), "neumann"), DEFAULT_PARAMS,
                       InitialSpec("random_uniform", 0.5, 0.01, 1234), TimeSpec(horizon=1e9),
                       SolverSpec(ras, 1, SubdomainSolverSpec("ilu", 2), subdomains=4096, gmres_restart=30)), 50),
+        4: ("3D 256^3 periodic, adaptive dt eta=1e2, 20 steps, GMRES(30), RAS 8^3-cell boxes (32768) ilu0 (the bench workload)",
+            RunConfig(Grid((256, 256, 256), (1.0, 1.0, 1.0), "periodic"), DEFAULT_PARAMS,
+                      InitialSpec("random_uniform", 0.5, 0.01, 1234), TimeSpec(horizon=1e9),
+                      SolverSpec(ras, 1, SubdomainSolverSpec("ilu", 0), subdomains=32768, gmres_restart=30)), 20),
     }
 
 
