@@ -905,6 +905,9 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
         {
             const int q = (e + lane) & RM;
             const int i = lane < n ? (int)ringI[q] : scratch;
+#ifdef ACCH_COL_CHECK
+            if (i < 0 || i > C.nloc || e + n > end_slot || (e + lane) / kColTile >= ready + 0 && lane < n) __trap();
+#endif
             double2 acc = y[i];
             blk_sub(acc, ringA[q], x);
             y[i] = acc;
@@ -912,6 +915,9 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
         if (n > 32) {   // warp-uniform
             const int q = (e + lane + 32) & RM;
             const int i = lane + 32 < n ? (int)ringI[q] : scratch;
+#ifdef ACCH_COL_CHECK
+            if (i < 0 || i > C.nloc || ((e + lane + 32) / kColTile >= ready && lane + 32 < n)) __trap();
+#endif
             double2 acc = y[i];
             blk_sub(acc, ringA[q], x);
             y[i] = acc;
@@ -954,6 +960,10 @@ apply_cols_kernel(GridDev g, const ClassDev *__restrict__ classes, const int *__
         if (lane == 0) y[pend_j] = pend_x;
         __syncwarp();
     }
+#ifdef ACCH_COL_CHECK
+    // the whole stream was consumed, every issued tile was waited for, no tile is still in flight
+    if (e != end_slot || ready != ntiles || freed + kColRing < ntiles) __trap();
+#endif
     if (VARIANT == 1) {
         for (int l = lane; l < C.nloc; l += 32) {
             if (!C.owned[l]) continue;
