@@ -47,11 +47,14 @@ def main():
     ap.add_argument("--solver", default="ilu0")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--dt", type=float, default=1e-3)
+    ap.add_argument("--shape", default="", help="nx,ny,nz instead of n^dim (e.g. 512,512,64: one z-slab of config 5 on 8 GPUs)")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     dev = torch.device("cuda", 0)
-    grid = Grid((args.n,) * args.dim, (1.0,) * args.dim, BoundaryCondition.PERIODIC)
+    counts = tuple(int(c) for c in args.shape.split(",")) if args.shape else (args.n,) * args.dim
+    args.dim = len(counts)
+    grid = Grid(counts, tuple(c / max(counts) for c in counts), BoundaryCondition.PERIODIC)
     params = Params(4.0, 2.0, 0.005, 0.1, 0.001)
     cfg = RunConfig(grid, params, InitialSpec("random_uniform", 0.5, 0.01, 1234), TimeSpec(1.0))
     st = build_initial_state(cfg, dev)
@@ -70,7 +73,9 @@ def main():
     out["residual"] = {"ms": t, "GB/s": 48 * N / t / 1e6, "frac": 48 * N / t / 1e6 / peak}
     t = timeit(lambda: J.matvec_into(w, y), args.reps)
     out["matvec"] = {"ms": t, "GB/s": 88 * N / t / 1e6, "frac": 88 * N / t / 1e6 / peak, "GDOF/s": 2 * N / t / 1e6}
-    nsub = (args.n // args.box) ** args.dim
+    nsub = 1
+    for c in counts:
+        nsub *= c // args.box
     pre = SchwarzPreconditioner(partition(grid, nsub, 1), SchwarzVariant.LEFT_RAS,
                                 SubdomainSolverSpec.from_string(args.solver))
     t = timeit(lambda: pre.update(J), 3)
