@@ -75,6 +75,7 @@ struct ClassDev {
     int meta_bytes, m_fbs, m_bptr, m_bbs, m_frows, m_brows, m_flen, m_blen, m_ecol, m_fjp, m_bjp, m_fjo, m_bjo;
     int m_lin, m_ixyz, m_own, m_rel;   // gather / scatter tables in the group image
     int jdup;   // some row has two stencil entries on one pattern position (tiny periodic axes)
+    int prezero;   // some slot receives no J entry (fill) or J entries are accumulated (jdup): zero before assembly
     // column-major layout of a narrow class (apply_cols_kernel): step words
     // (forward steps, then backward), row index of every slot, first backward slot
     const unsigned *col_steps;
@@ -99,6 +100,7 @@ struct ClassHost {
     std::vector<unsigned char> meta;   // ClassDev::meta image
     std::vector<int> lin, own_list;
     int jdup = 0;
+    int prezero = 1;
     int b_min_row = 0, nlevb_ras = 0;
     long long skip_blocks = 0;   // factor blocks of the backward rows below b_min_row
     int m_off[17] = {0};
@@ -152,8 +154,12 @@ factor_kernel(GridDev g, ParamsDev P, double dt, const double *__restrict__ coef
     const int4 o = sub_origin[s];
     StridedBlocks A{vals + sub_off[s], ss};
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int t = tid; t < C.ell_total; t += nt) A[t] = make_double4(0.0, 0.0, 0.0, 0.0);
-    __syncthreads();
+    // ILU(0) without folded stencil entries: the assembly writes every slot of the
+    // pattern (the padding slots were cleared at creation and are never written)
+    if (C.prezero) {
+        for (int t = tid; t < C.ell_total; t += nt) A[t] = make_double4(0.0, 0.0, 0.0, 0.0);
+        __syncthreads();
+    }
     for (int l = tid; l < C.nloc; l += nt) {
         int gx, gy, gz;
         local_to_global(g, C, o, l, gx, gy, gz);
@@ -1525,6 +1531,15 @@ bool build_class(const GridDev &g, const std::array<std::vector<int>, 3> &rel, c
     for (int t = 0; t < C.nnzb; ++t) C.ecol[C.pos[t]] = C.col[t];
     C.jmap_csr = C.jmap;
     C.upd_csr = C.upd;
+    {
+        // every pattern entry written by the assembly?  (then the slots need no zero-fill pass)
+        std::vector<char> hit(C.nnzb, 0);
+        for (int j : C.jmap_csr)
+            if (j >= 0) hit[j] = 1;
+        bool all = true;
+        for (int t = 0; t < C.nnzb; ++t) all = all && hit[t];
+        C.prezero = (C.jdup || !all) ? 1 : 0;
+    }
     for (auto &j : C.jmap)
         if (j >= 0) j = C.pos[j];
     for (auto &u : C.upd) {
@@ -1815,6 +1830,7 @@ acch_status upload_class(ClassHost &C)
     d.b_min_row = C.b_min_row;
     d.nlevb_ras = C.nlevb_ras;
     d.jdup = C.jdup;
+    d.prezero = C.prezero;
     d.col_steps = (const unsigned *)(b + o_cs);
     d.col_ridx = (const unsigned short *)(b + o_cr);
     d.col_nf = C.col_nf;
@@ -2117,6 +2133,8 @@ extern "C" acch_status acch_precond_create(acch_ctx *ctx, int64_t n_sub, int32_t
     PC_CUDA(cudaMalloc(&pc->d_sub_ext_off, sizeof(long long) * n_sub));
     PC_CUDA(cudaMemcpy(pc->d_sub_ext_off, pc->sub_ext_off.data(), sizeof(long long) * n_sub, cudaMemcpyHostToDevice));
     PC_CUDA(cudaMalloc(&pc->d_vals, sizeof(double4) * std::max<long long>(1, pc->total_blocks)));
+    // padding slots (level alignment, tile tails) are prefetched or copied but never used in arithmetic
+    PC_CUDA(cudaMemset(pc->d_vals, 0, sizeof(double4) * std::max<long long>(1, pc->total_blocks)));
     PC_CUDA(cudaMalloc(&pc->d_bad, sizeof(int) * n_sub));
     const bool need_ext = variant != 1 || !pc->use_smem;
     if (need_ext) PC_CUDA(cudaMalloc(&pc->d_ext_out, sizeof(double2) * std::max<long long>(1, pc->total_ext)));
