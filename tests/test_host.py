@@ -168,3 +168,28 @@ def test_initial_fields_bitwise_reference_draw_order():
     u, v = initial_fields(cfg)
     uo, vo = O.initial_fields(O.Mesh((16, 8), (1.0, 1.0), True), 0.5, 0.05, 1234)
     assert np.array_equal(u, uo) and np.array_equal(v, vo)
+
+
+def test_bench_arms_share_one_workload_config():
+    """Both bench arms print the same `config` dict (the driver compares them)
+    and the work-count table holds the windows the driver runs."""
+    import importlib.util
+    import json
+    import sys
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    argv, sys.argv = sys.argv, ["bench.py", "--gpus", "1", "--steps", "20", "--warmup", "5"]
+    try:
+        spec.loader.exec_module(bench)
+        args = bench.parse_args()
+    finally:
+        sys.argv = argv
+    a = bench.workload_config(args)
+    b = bench.workload_config(args, 1)
+    assert a == b and a["workload"] == bench.workload_name(args)
+    assert a["grid"] == [256, 256, 256] and a["subdomains"] == 32768
+    assert "steps 6..25" in a["steps_timed"]
+    counts, key = bench.load_counts(args)
+    assert key == bench.window_key(args) and counts["gmres"] > 0
+    table = json.load(open(os.path.join(ROOT, "bench_counts.json")))
+    assert "256^3:box8:ilu0:ras-left:r30:W3:K4" in table
