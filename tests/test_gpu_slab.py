@@ -106,7 +106,7 @@ def test_slab_residual_and_matvec_match_single_domain(counts, bc, nranks, rng):
 
 
 @pytest.mark.parametrize("counts,bc,nranks", CASES[:2])
-@pytest.mark.parametrize("solver", ["ilu0", "ilu1"])
+@pytest.mark.parametrize("solver", ["ilu0", "ilu1", "ilu2"])   # ilu2: the column-sweep solver on slab boxes
 def test_slab_schwarz_apply_matches_single_domain(counts, bc, nranks, solver, rng):
     g = Grid(counts, (1.0, 1.0, 1.0), bc)
     uo, vo = fields(g, rng)
