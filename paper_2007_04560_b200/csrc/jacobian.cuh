@@ -52,8 +52,13 @@ __device__ __forceinline__ void jac_row_emit(const GridDev &g, const ParamsDev &
         r[0] = q[0]; r[1] = q[1]; r[2] = q[2];
         r[a] = a == 2 ? q[a] + s : wrap_coord(q[a] + s, nn[a], g.periodic);
     };
+    // a cell's coefficients come as two vector loads: A = (S, D, c_u, c_v), B = (cbar, G_u)
+    const double4 *__restrict__ cA = co_A(coef);
+    const double2 *__restrict__ cB = co_B(coef, N);
     const long long c0 = cid(cc);
-    const double cb0 = coef[co_index(CO_CBAR, N, c0)], gu0 = coef[co_index(CO_GU, N, c0)];
+    const double2 b0 = cB[c0];
+    const double4 a0 = ldg256(cA + c0);
+    const double cb0 = b0.x, gu0 = b0.y;
     // weights of dG_u(m) and eta(m) in row c of the u equation
     double wdg[7], weta[7];
     int mo[3 * 7];   // relative offsets of m
@@ -67,8 +72,9 @@ __device__ __forceinline__ void jac_row_emit(const GridDev &g, const ParamsDev &
             int q[3];
             shifted(cc, a, s, q);
             const long long cn = cid(q);
-            const double K = 0.5 * (cb0 + coef[co_index(CO_CBAR, N, cn)]) * g.ih2[a];
-            const double dGn = coef[co_index(CO_GU, N, cn)] - gu0;
+            const double2 bn = cB[cn];
+            const double K = 0.5 * (cb0 + bn.x) * g.ih2[a];
+            const double dGn = bn.y - gu0;
             ktot += K;
             wdg[nm] = -K;
             weta[nm] = -0.5 * dGn * g.ih2[a];
@@ -99,15 +105,16 @@ __device__ __forceinline__ void jac_row_emit(const GridDev &g, const ParamsDev &
             }
         }
         const int om = offid(mo[3 * j], mo[3 * j + 1], mo[3 * j + 2]);
-        const double A = -0.5 * P.alpha + coef[co_index(CO_S, N, cm)] + hg * lsum;
-        emit(om, 0, wdg[j] * A + weta[j] * 0.5 * coef[co_index(CO_CU, N, cm)]);
-        emit(om, 1, wdg[j] * coef[co_index(CO_D, N, cm)] + weta[j] * 0.5 * coef[co_index(CO_CV, N, cm)]);
+        const double4 am = j == 0 ? a0 : ldg256(cA + cm);
+        const double A = -0.5 * P.alpha + am.x + hg * lsum;
+        emit(om, 0, wdg[j] * A + weta[j] * 0.5 * am.z);
+        emit(om, 1, wdg[j] * am.y + weta[j] * 0.5 * am.w);
     }
     const int o0 = offid(0, 0, 0);
     emit(o0, 0, 1.0 / dt);
     // v row
     const double cr = cb0 / P.rho;
-    const double S0 = coef[co_index(CO_S, N, c0)], D0 = coef[co_index(CO_D, N, c0)], Gv0 = coef[co_index(CO_GV, N, c0)];
+    const double S0 = a0.x, D0 = a0.y, Gv0 = co_Gv(coef, N)[c0];
     double lsum0 = 0.0;
     for (int a = 0; a < g.dim; ++a) {
         for (int s = -1; s <= 1; s += 2) {
@@ -117,8 +124,8 @@ __device__ __forceinline__ void jac_row_emit(const GridDev &g, const ParamsDev &
             emit(o, 3, -hg * cr * g.ih2[a]);
         }
     }
-    emit(o0, 2, cr * D0 + Gv0 * coef[co_index(CO_CU, N, c0)] / (2.0 * P.rho));
-    emit(o0, 3, 1.0 / dt + cr * (-0.5 * P.beta + S0) + hg * cr * lsum0 + Gv0 * coef[co_index(CO_CV, N, c0)] / (2.0 * P.rho));
+    emit(o0, 2, cr * D0 + Gv0 * a0.z / (2.0 * P.rho));
+    emit(o0, 3, 1.0 / dt + cr * (-0.5 * P.beta + S0) + hg * cr * lsum0 + Gv0 * a0.w / (2.0 * P.rho));
 }
 
 template <int DIM>
